@@ -1,0 +1,249 @@
+/*
+ * orchsim_capi.h -- the drop-in C-ABI of the B200-native Batch Post-Balancing
+ * Dispatcher (OrchMLLM, arXiv 2503.23830). This is the ONLY boundary between
+ * host code and the sm_100a kernels: plain pointers and sizes, no C++ or
+ * torch types. Implemented in paper_2503_23830_b200/csrc/*.cu and exported by
+ * paper_2503_23830_b200/lib/liborchsim_b200.so.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj). The C++ API of the reference
+ * (include/orchsim/*.hpp in this repo, same names/signatures/exceptions) is
+ * implemented on top of these calls in liborchsim_b200_host.so.
+ *
+ * Conventions
+ *  - Item arrays are indexed by INPUT POSITION (the position of the SeqItem in
+ *    the reference's std::vector<SeqItem>); instance/bin arrays by instance.
+ *  - "d_" pointers are device memory (cudaMalloc / torch CUDA tensors),
+ *    "h_" pointers are host memory. Streams are cudaStream_t passed as void*.
+ *  - Device-pointer entry points are asynchronous on the given stream unless
+ *    stated; validation errors found on the device are reported through the
+ *    device-resident orch_summary (error, error_index) and make every later
+ *    kernel of the same pipeline a no-op. Host-pointer entry points (_host)
+ *    synchronise and return the reference's error class as a return code.
+ *  - Return codes mirror the reference's exception types.
+ */
+#ifndef ORCHSIM_CAPI_H
+#define ORCHSIM_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORCH_OK 0
+#define ORCH_INVALID_ARGUMENT 1 /* std::invalid_argument (balancers.cpp:30-33,157,196-241) */
+#define ORCH_CONFIG_ERROR 2     /* orchsim::ConfigError  (core.cpp:178)                    */
+#define ORCH_SIZE_CAP 3         /* orchsim::SizeCapError (balancers.cpp:383-387)           */
+#define ORCH_LOGIC_ERROR 4      /* std::logic_error      (balancers.cpp:175,286)           */
+#define ORCH_CUDA_ERROR 10      /* -> std::runtime_error                                   */
+#define ORCH_NCCL_ERROR 11      /* -> std::runtime_error                                   */
+#define ORCH_UNSUPPORTED 12     /* input beyond a documented device limit      */
+
+/* PolicyKind (balancers.hpp:12), same numbering. */
+#define ORCH_GREEDY_UNPADDED 0
+#define ORCH_BINARY_PADDED 1
+#define ORCH_QUADRATIC_TOLERANCE 2
+#define ORCH_CONVTRANSFORMER 3
+/* CostVariant (core.hpp:21), same numbering. */
+#define ORCH_LINEAR_ONLY 0
+#define ORCH_TRANSFORMER_QUADRATIC 1
+#define ORCH_CONV_TRANSFORMER_PADDED 2
+
+/* Device limits of this build (checked; ORCH_UNSUPPORTED beyond them). */
+#define ORCH_MAX_INSTANCES 4096        /* d: bins live in one CTA's shared memory */
+#define ORCH_MAX_ITEMS 16777215        /* n < 2^24                                */
+#define ORCH_MAX_LENGTH 4294967295LL   /* per-item length < 2^32                  */
+
+typedef struct orch_ctx orch_ctx;   /* per-device workspace; not thread-safe, one per host thread */
+typedef struct orch_comm orch_comm; /* NCCL communicator over the ranks of one box               */
+
+/* BalancePolicy (balancers.hpp:14-18). */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  int64_t tolerance_v;
+  double lambda;
+} orch_policy;
+
+/* CostModel (core.hpp:63-68). padded: PaddingMode::Padded == 1. */
+typedef struct {
+  double alpha;
+  double beta;
+  int32_t padded;
+  int32_t variant;
+} orch_cost_model;
+
+/* Device-resident result summary of one balance call. */
+typedef struct {
+  double objective;          /* BalanceResult::objective_value                     */
+  double algo_objective;     /* objective of the balancer's own packing             */
+  double identity_objective; /* objective of the identity arrangement               */
+  double pre_max, pre_mean, pre_ratio;    /* stats_of (orchestrator.cpp:91-102) of the  */
+  double post_max, post_mean, post_ratio; /* origin / destination batches, policy model */
+  int64_t bound;             /* BinaryPadded: the minimal feasible bound; Conv: seeding bound */
+  int64_t error_index;       /* first offending input position, or INT64_MAX       */
+  int32_t error;             /* 0 or an ORCH_* code raised on the device           */
+  int32_t used_identity;     /* never_worse (balancers.cpp:71-76) took the identity */
+  int64_t rounds;            /* greedy rounds executed (diagnostic)                 */
+} orch_summary;
+
+/* Flat BalanceResult (balancers.hpp:20-24): every pointer is device memory,
+ * caller-owned; any may be NULL except where a later call needs it. */
+typedef struct {
+  int32_t* dest_inst;  /* [n] Rearrangement dest instance      */
+  int32_t* dest_slot;  /* [n] Rearrangement dest slot          */
+  int32_t* src_slot;   /* [n] source slot (index_sources)      */
+  int64_t* src_off;    /* [n] token offset in origin batch     */
+  int64_t* dst_off;    /* [n] token offset in dest batch       */
+  int32_t* bin_count;  /* [d] new_batches[i].items.size()      */
+  int64_t* bin_len;    /* [d] batch_length(new_batches[i])     */
+  int64_t* bin_tokens; /* [d] unpadded_length(new_batches[i])  */
+  double* bin_cost;    /* [d] cost(policy model, new_batches[i]) */
+  int32_t* bin_offset; /* [d+1] CSR of new_batches              */
+  int32_t* bin_member; /* [n] input positions, (dest_inst, dest_slot) order */
+  int32_t* src_offset; /* [d+1] CSR of the origin batches (batches_from_items)     */
+  int32_t* src_member; /* [n] input positions, (origin, src_slot) order            */
+  orch_summary* summary; /* device, required */
+} orch_balance_out;
+
+/* Rank-level dispatch layout: P ranks, instance i
+ * on rank i / (d/P). All device memory. */
+typedef struct {
+  int64_t* rank_src_off; /* [n] row offset of the item in its origin rank's input buffer */
+  int64_t* rank_dst_off; /* [n] row offset of the item in its dest rank's output buffer   */
+  int64_t* pair_off;     /* [n] row offset inside the (origin rank -> dest rank) segment  */
+  int64_t* send_rows;    /* [P*P] rows from rank r to rank q (r-major)                    */
+  int64_t* send_displ;   /* [P*P] row offset of segment r->q in rank r's send buffer      */
+  int64_t* recv_displ;   /* [P*P] row offset of segment r->q in rank q's recv buffer (q-major) */
+  int64_t* in_rows;      /* [P] rows of each rank's input buffer                           */
+  int64_t* out_rows;     /* [P] rows of each rank's output buffer                          */
+  int32_t* status;       /* [1] 0, or ORCH_INVALID_ARGUMENT when a buffer capacity was short */
+} orch_layout_out;
+
+/* ------------------------------------------------------------- context */
+int orch_ctx_create(int device, orch_ctx** out);
+void orch_ctx_destroy(orch_ctx* ctx);
+/* Message of the last failing call on this host thread. */
+const char* orch_last_error(void);
+int orch_version(void);
+/* Number of kernels this library launched so far on ctx (for launch accounting). */
+int64_t orch_ctx_launches(const orch_ctx* ctx);
+
+/* ------------------------------------------------------------- balance */
+/* balance(policy, d, items)             balancers.hpp:53  (balancers.cpp:273-287)
+ * identity_arrangement(policy, d, items) balancers.hpp:59 (balancers.cpp:178-183)
+ * when identity_only != 0.                                                     */
+int orch_balance(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                 const int64_t* d_len, const int32_t* d_origin, int32_t identity_only,
+                 const orch_balance_out* out, void* stream);
+
+/* Host-buffer variant: copies h_len/h_origin in, runs orch_balance, copies
+ * the flat result out (any h_ output may be NULL) and synchronises. Returns
+ * the reference's error class. */
+int orch_balance_host(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                      const int64_t* h_len, const int32_t* h_origin, int32_t identity_only,
+                      int32_t* h_dest_inst, int32_t* h_dest_slot, int64_t* h_dst_off,
+                      int32_t* h_bin_count, double* h_bin_cost, orch_summary* h_summary,
+                      void* stream);
+
+/* min_feasible_padded_bound  balancers.hpp:64 (balancers.cpp:289-296)
+ * padded_bound_feasible      balancers.hpp:68 (balancers.cpp:298-307)
+ * Host buffers, synchronous. */
+int orch_min_feasible_padded_bound_host(orch_ctx* ctx, int32_t d, int64_t n,
+                                        const int64_t* h_len, const int32_t* h_origin,
+                                        int64_t* h_bound, void* stream);
+int orch_padded_bound_feasible_host(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* h_len,
+                                    const int32_t* h_origin, int64_t bound, int32_t* h_feasible,
+                                    void* stream);
+
+/* ---------------------------------------------------------- cost model */
+/* cost(model, batch) over many batches at once (core.cpp:91-118) plus
+ * stats_of (orchestrator.cpp:91-102): batches given as CSR over input
+ * positions. d_stats = {max, mean, ratio}. Requires model->padded == batch
+ * padding (the caller's MiniBatch mode), else ORCH_INVALID_ARGUMENT. */
+int orch_batch_costs(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded,
+                     int32_t d, int64_t n, const int64_t* d_len, const int32_t* d_bin_offset,
+                     const int32_t* d_bin_member, double* d_cost, double* d_stats, void* stream);
+
+/* batches_from_items (core.cpp:183-199): CSR of the origin batches. */
+int orch_group_by_origin(orch_ctx* ctx, int32_t d, int64_t n, const int32_t* d_origin,
+                         int32_t* d_bin_offset, int32_t* d_bin_member, void* stream);
+
+/* encode_lengths + interleaved_length (core.cpp:163-181), vectorised: parts
+ * of example e are [part_offset[e], part_offset[e+1]); encoded = ceil(meta /
+ * rate[modality]) with rate >= 1 (else ORCH_CONFIG_ERROR, host-checked);
+ * d_interleaved[e] = sum of encoded parts. */
+int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_part_offset,
+                        const int32_t* d_modality, const int64_t* d_meta_len,
+                        int32_t num_modalities, const int64_t* h_rates, int64_t* d_encoded,
+                        int64_t* d_interleaved, void* stream);
+
+/* ------------------------------------------------------ layout / movement */
+/* volume_matrix (topology.cpp:40-53): d_V[d*d] (src-major) token volumes. */
+int orch_volume_matrix(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
+                       const int32_t* d_origin, const int32_t* d_dest_inst, int64_t* d_V,
+                       void* stream);
+
+/* Send/recv layout of the exchange (make_exchange_plan, exchange.cpp:10-32,
+ * realised on ranks): offsets, per-pair counts. Needs the balance result's
+ * dest_inst, src_off, dst_off, bin_offset, bin_member. */
+int orch_layout(orch_ctx* ctx, int32_t d, int32_t nranks, int64_t n, const int64_t* d_len,
+                const int32_t* d_origin, const orch_balance_out* bal,
+                const orch_layout_out* layout, void* stream);
+
+/* The data movement of simulate_exchange (exchange.cpp:62 = apply,
+ * core.cpp:120-161) realised on token rows of row_bytes bytes (a multiple of
+ * 16; bf16 d_model=4096 -> 8192). Buffers are this rank's:
+ *   d_in   [in_cap rows]   origin batches of the rank's instances, in order
+ *   d_out  [out_cap rows]  destination batches of the rank's instances
+ *   d_send / d_recv        off-rank segments (layout send_displ / recv_displ)
+ * A rank buffer larger than its capacity sets layout->status and moves
+ * nothing. Split into the three stages of the exchange: */
+
+/* pack: rows of this rank's items -> d_out (staying on the rank) or d_send. */
+int orch_pack(orch_ctx* ctx, int32_t rank, int32_t nranks, int32_t d, int64_t n,
+              const int64_t* d_len, const int32_t* d_origin, const orch_balance_out* bal,
+              const orch_layout_out* layout, size_t row_bytes, const void* d_in, int64_t in_cap,
+              void* d_out, int64_t out_cap, void* d_send, int64_t send_cap, void* stream);
+/* exchange: one grouped ncclSend/ncclRecv over all peers (reads the per-peer
+ * counts on the host: one stream synchronisation). */
+int orch_exchange(orch_ctx* ctx, orch_comm* comm, const orch_layout_out* layout,
+                  size_t row_bytes, const void* d_send, void* d_recv, int64_t recv_cap,
+                  void* stream);
+/* unpack: received rows -> their destination slots in d_out. */
+int orch_unpack(orch_ctx* ctx, int32_t rank, int32_t nranks, int32_t d, int64_t n,
+                const int64_t* d_len, const int32_t* d_origin, const orch_balance_out* bal,
+                const orch_layout_out* layout, size_t row_bytes, const void* d_recv,
+                void* d_out, int64_t out_cap, void* stream);
+/* pack + exchange + unpack. comm == NULL: one rank, every item moves in one
+ * fused pass d_in -> d_out (no send/recv buffers, no synchronisation). */
+int orch_dispatch(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                  const int32_t* d_origin, const orch_balance_out* bal,
+                  const orch_layout_out* layout, size_t row_bytes, const void* d_in,
+                  int64_t in_cap, void* d_out, int64_t out_cap, void* d_send, int64_t send_cap,
+                  void* d_recv, int64_t recv_cap, void* stream);
+
+/* ----------------------------------------------------------- NCCL comm */
+/* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller. */
+int orch_comm_unique_id(unsigned char* h_id128);
+int orch_comm_create(int32_t nranks, int32_t rank, const unsigned char* h_id128,
+                     orch_comm** out);
+void orch_comm_destroy(orch_comm* comm);
+int32_t orch_comm_rank(const orch_comm* comm);
+int32_t orch_comm_size(const orch_comm* comm);
+
+/* gather_lengths (exchange.cpp:34-47) realised as ncclAllGather: every rank
+ * contributes its local items (global input position, length, origin) and
+ * receives the global arrays scattered into input order. Local counts are
+ * padded to max_local (>= every rank's local_n). */
+int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_t max_local,
+                         const int64_t* d_local_pos, const int64_t* d_local_len,
+                         const int32_t* d_local_origin, int64_t n, int64_t* d_len,
+                         int32_t* d_origin, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORCHSIM_CAPI_H */

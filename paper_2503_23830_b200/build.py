@@ -1,0 +1,120 @@
+"""Builds the sm_100a library and the host C++ adapter, in-tree.
+
+    python -m paper_2503_23830_b200.build        (also called by __graft_entry__.build())
+
+Outputs (git-ignored, travel to GPU boxes with the snapshot):
+    paper_2503_23830_b200/lib/liborchsim_b200.so       C-ABI + CUDA kernels (include/orchsim_capi.h)
+    paper_2503_23830_b200/lib/liborchsim_b200_host.so  the reference's C++ API over the C-ABI
+    paper_2503_23830_b200/lib/orchsim_b200_ref_tests   the reference's own unit tests compiled
+                                                       unmodified against the host adapter
+                                                       (only when /root/reference is present)
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib")
+INCLUDE = os.path.join(ROOT, "include")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+REF_TESTS = "/root/reference/proj/tests"
+
+
+def _nccl_dirs():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    cands = []
+    if spec and spec.submodule_search_locations:
+        for loc in spec.submodule_search_locations:
+            cands.append(os.path.join(loc, "nccl"))
+    for c in cands:
+        if os.path.exists(os.path.join(c, "include", "nccl.h")):
+            return os.path.join(c, "include"), os.path.join(c, "lib")
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu"]
+HOST_SOURCES = ["host/core.cpp", "host/balancers.cpp", "host/topology.cpp", "host/exchange.cpp",
+                "host/runtime.cpp"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd):
+    print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_cuda(force=False):
+    os.makedirs(LIB, exist_ok=True)
+    nccl_inc, nccl_lib = _nccl_dirs()
+    out = os.path.join(LIB, "liborchsim_b200.so")
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    deps.append(os.path.join(INCLUDE, "orchsim_capi.h"))
+    if not force and not _stale(out, deps):
+        return out
+    objs = []
+    for src in CU_SOURCES:
+        obj = os.path.join(LIB, src.replace(".cu", ".o"))
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if os.environ.get("ORCH_PTXAS_V") else "-O3",
+              "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj])
+        objs.append(obj)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
+          "-Xlinker", f"-rpath={nccl_lib}", "-lcudart"])
+    for o in objs:
+        os.remove(o)
+    return out
+
+
+def build_host(force=False):
+    """The reference's C++ API (include/orchsim/*.hpp) over the C-ABI."""
+    out = os.path.join(LIB, "liborchsim_b200_host.so")
+    srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES]
+    hdrs = [os.path.join(INCLUDE, "orchsim", f) for f in os.listdir(os.path.join(INCLUDE, "orchsim"))]
+    if not force and not _stale(out, srcs + hdrs + [os.path.join(INCLUDE, "orchsim_capi.h")]):
+        return out
+    _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-Wall", "-Wextra",
+          "-I", INCLUDE, "-o", out, *srcs, "-L", LIB, "-l:liborchsim_b200.so",
+          "-Wl,-rpath,$ORIGIN", "-L/usr/local/cuda/lib64", "-lcudart",
+          "-Wl,-rpath,/usr/local/cuda/lib64"])
+    return out
+
+
+def build_ref_tests(force=False):
+    """Compile the reference's unit tests UNCHANGED against the B200 host API."""
+    out = os.path.join(LIB, "orchsim_b200_ref_tests")
+    if not os.path.isdir(REF_TESTS):
+        return None
+    srcs = [os.path.join(REF_TESTS, f) for f in ("test_main.cpp", "test_core.cpp",
+                                                 "test_balancers.cpp")]
+    host = os.path.join(LIB, "liborchsim_b200_host.so")
+    if not force and not _stale(out, srcs + [host]):
+        return out
+    shim = os.path.join(ROOT, "oracle", "shim")
+    _run([CXX, "-std=c++20", "-O2", "-w", "-I", INCLUDE, "-I", shim, "-I", REF_TESTS, "-o", out,
+          *srcs, "-L", LIB, "-l:liborchsim_b200_host.so", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
+def build_all(force=False):
+    build_cuda(force)
+    build_host(force)
+    build_ref_tests(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

@@ -1,0 +1,507 @@
+// Host orchestration of the balance pipeline (C-ABI orch_balance*): a short
+// chain of sm_100a kernels on one stream, no host synchronisation.
+//
+//   K1 k_validate          index_sources checks + sort keys   (balancers.cpp:25-37)
+//   radix sort by origin   -> identity order (batches_from_items, core.cpp:183-199)
+//   K2 k_ident_*           source slots / offsets, origin batches
+//   radix sort by length   -> descending (stable) order        (balancers.cpp:78-88)
+//   K4 greedy              distribute_min_sum                  (balancers.cpp:92-107)
+//   K5 padded search       Alg.2 GetLeastBatches + search      (balancers.cpp:111-143)
+//   K6 quadratic tolerance champion scan                       (balancers.cpp:210-233)
+//   K7 k_bin_cost/k_decide cost(), objective, never_worse      (balancers.cpp:43-76)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <string>
+
+#include "balance_kernels.cuh"
+#include "plan.cuh"
+
+namespace orchb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <class F>
+void launch(orch_ctx* ctx, F&& f) {
+  f();
+  ++ctx->launches;
+}
+
+__global__ void k_init(orch_summary* s, Flags* f) {
+  s->objective = s->algo_objective = s->identity_objective = 0.0;
+  s->pre_max = s->pre_mean = s->post_max = s->post_mean = 0.0;
+  s->pre_ratio = s->post_ratio = 1.0;
+  s->bound = 0;
+  s->error_index = INT64_MAX;
+  s->error = 0;
+  s->used_identity = 0;
+  s->rounds = 0;
+  f->first_bad = ~0ull;
+  f->unsupported = 0;
+  f->total_tokens = 0;
+}
+
+orch_cost_model policy_model(const orch_policy& p) {  // balancers.cpp:162-176
+  orch_cost_model m{1.0, 0.0, 0, ORCH_LINEAR_ONLY};
+  switch (p.kind) {
+    case ORCH_BINARY_PADDED:
+      m.padded = 1;
+      break;
+    case ORCH_QUADRATIC_TOLERANCE:
+      m.beta = p.lambda;
+      m.variant = ORCH_TRANSFORMER_QUADRATIC;
+      break;
+    case ORCH_CONVTRANSFORMER:
+      m.beta = p.lambda;
+      m.variant = ORCH_CONV_TRANSFORMER_PADDED;
+      break;
+    default:
+      break;
+  }
+  return m;
+}
+
+size_t greedy_rounds_smem(int d) {
+  int p2 = 1;
+  while (p2 < d) p2 <<= 1;
+  return 3 * sizeof(uint64_t) * p2 + sizeof(int32_t) * d;
+}
+
+// distribute_min_sum on [first, n) of the descending order.
+int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const uint32_t* xs,
+                  const int32_t* order, const int64_t* init_load, const int32_t* init_count,
+                  int32_t* di, int32_t* ds, int64_t* doff, int32_t* bc, int64_t* bt,
+                  orch_summary* s, cudaStream_t st) {
+  if (d <= 32) {
+    launch(ctx, [&] {
+      k_greedy_warp<<<1, 32, 0, st>>>(d, n, first, xs, order, init_load, init_count, di, ds, doff,
+                                      bc, bt, s);
+    });
+  } else if (d <= 512) {
+    const size_t sm = greedy_rounds_smem(d);
+    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_greedy_rounds<256>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    launch(ctx, [&] {
+      k_greedy_rounds<256><<<1, 256, sm, st>>>(d, n, first, xs, order, init_load, init_count, di,
+                                               ds, doff, bc, bt, s);
+    });
+  } else {
+    const size_t sm = greedy_rounds_smem(d);
+    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_greedy_rounds<1024>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    launch(ctx, [&] {
+      k_greedy_rounds<1024><<<1, 1024, sm, st>>>(d, n, first, xs, order, init_load, init_count,
+                                                 di, ds, doff, bc, bt, s);
+    });
+  }
+  return ORCH_OK;
+}
+
+}  // namespace
+
+// Host-side argument checks in the reference's order (require_valid_d, then
+// the policy's own checks; index_sources is checked on the device).
+int check_policy_args(const orch_policy* p, int d, int64_t n, int identity_only) {
+  if (!p) return fail(ORCH_INVALID_ARGUMENT, "null policy");
+  if (p->kind < 0 || p->kind > 3) return fail(ORCH_LOGIC_ERROR, "unknown policy kind");
+  if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
+  if (d > ORCH_MAX_INSTANCES)
+    return fail(ORCH_UNSUPPORTED, "instance count exceeds ORCH_MAX_INSTANCES (" +
+                                      std::to_string(ORCH_MAX_INSTANCES) + ")");
+  if (n < 0 || n > ORCH_MAX_ITEMS) return fail(ORCH_UNSUPPORTED, "item count exceeds ORCH_MAX_ITEMS");
+  if (identity_only) return ORCH_OK;
+  switch (p->kind) {
+    case ORCH_BINARY_PADDED:
+      if (n == 0) return fail(ORCH_INVALID_ARGUMENT, "padded balancing needs at least one item");
+      break;
+    case ORCH_QUADRATIC_TOLERANCE:
+      if (p->lambda < 0.0 || p->tolerance_v < 0)
+        return fail(ORCH_INVALID_ARGUMENT, "lambda and tolerance_v must be nonnegative");
+      break;
+    case ORCH_CONVTRANSFORMER:
+      if (n == 0)
+        return fail(ORCH_INVALID_ARGUMENT, "convtransformer balancing needs at least one item");
+      if (p->lambda < 0.0) return fail(ORCH_INVALID_ARGUMENT, "lambda must be nonnegative");
+      break;
+    default:
+      break;
+  }
+  return ORCH_OK;
+}
+
+// mode: 0 balance, 1 identity only, 2 padded search only, 3 padded feasibility probe
+int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const int64_t* len,
+                const int32_t* origin, int mode, int64_t probe, const orch_balance_out* out,
+                int64_t* d_bound_out, int32_t* d_probe_out, cudaStream_t st) {
+  const int identity_only = mode == 1;
+  if (!out || !out->summary) return fail(ORCH_INVALID_ARGUMENT, "orch_balance: summary required");
+  orch_summary* S = out->summary;
+  const orch_cost_model model = policy_model(*pol);
+  const int kind = pol->kind;
+  const bool padded_only = mode >= 2;
+  const bool needs_desc = !identity_only && !padded_only && kind != ORCH_BINARY_PADDED;
+  const bool needs_asc = padded_only || (!identity_only && kind == ORCH_BINARY_PADDED);
+  const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+
+  // ---- workspace plan
+  Plan plan;
+  Flags* flags;
+  uint32_t *key_len, *key_org, *sorted_org, *xs;
+  int32_t *iota, *ident_order, *order, *ident_count, *ident_offset;
+  int64_t *ident_len, *ident_prefix;
+  int32_t* i_count;
+  int64_t *i_len, *i_tokens;
+  double* i_cost;
+  int32_t *dest_inst, *dest_slot, *src_slot, *bin_count, *bin_offset, *bin_member, *a_count;
+  int64_t *src_off, *dst_off, *bin_len, *bin_tokens, *a_tokens;
+  double* bin_cost;
+  void* cub_tmp;
+  plan.add(&flags, 1);
+  plan.add(&key_len, nn);
+  plan.add(&key_org, nn);
+  plan.add(&sorted_org, nn);
+  plan.add(&xs, nn);
+  plan.add(&iota, nn);
+  plan.add_or(&ident_order, out->src_member, nn);
+  plan.add(&order, nn);
+  plan.add(&ident_count, d + 1);
+  plan.add_or(&ident_offset, out->src_offset, d + 1);
+  plan.add(&ident_len, nn + 1);
+  plan.add(&ident_prefix, nn + 1);
+  plan.add(&i_count, d);
+  plan.add(&i_len, d);
+  plan.add(&i_tokens, d);
+  plan.add(&i_cost, d);
+  plan.add(&a_count, d + 1);
+  plan.add(&a_tokens, d);
+  plan.add_or(&dest_inst, out->dest_inst, nn);
+  plan.add_or(&dest_slot, out->dest_slot, nn);
+  plan.add_or(&src_slot, out->src_slot, nn);
+  plan.add_or(&src_off, out->src_off, nn);
+  plan.add_or(&dst_off, out->dst_off, nn);
+  plan.add_or(&bin_count, out->bin_count, d);
+  plan.add_or(&bin_len, out->bin_len, d);
+  plan.add_or(&bin_tokens, out->bin_tokens, d);
+  plan.add_or(&bin_cost, out->bin_cost, d);
+  plan.add_or(&bin_offset, out->bin_offset, d + 1);
+  plan.add_or(&bin_member, out->bin_member, nn);
+  // ConvTransformer / BinaryPadded extras
+  int32_t *g_di, *g_ds, *seed_count, *n_groups;
+  int64_t *g_doff, *seed_load, *consumed, *asc_len, *asc_prefix, *starts, *bound;
+  const bool conv = !identity_only && !padded_only && kind == ORCH_CONVTRANSFORMER;
+  plan.add(&g_di, conv ? nn : 1);
+  plan.add(&g_ds, conv ? nn : 1);
+  plan.add(&g_doff, conv ? nn : 1);
+  plan.add(&seed_load, d);
+  plan.add(&seed_count, d);
+  plan.add(&consumed, 1);
+  plan.add(&asc_len, needs_asc ? nn + 1 : 1);
+  plan.add(&asc_prefix, needs_asc ? nn + 1 : 1);
+  plan.add(&starts, d + 2);
+  plan.add(&n_groups, 1);
+  plan.add(&bound, 1);
+  // CUB temporary storage (max over the calls below)
+  size_t cub_bytes = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, key_org, sorted_org, iota, ident_order, (int)nn, 0,
+                                  obits, st);
+  cub_bytes = std::max(cub_bytes, b);
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, b, key_len, xs, iota, order, (int)nn, 0, 32,
+                                            st);
+  cub_bytes = std::max(cub_bytes, b);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, key_len, xs, iota, order, (int)nn, 0, 32, st);
+  cub_bytes = std::max(cub_bytes, b);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, ident_len, ident_prefix, (int)nn + 1, st);
+  cub_bytes = std::max(cub_bytes, b);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, ident_count, ident_offset, d + 1, st);
+  cub_bytes = std::max(cub_bytes, b);
+  plan.add(reinterpret_cast<char**>(&cub_tmp), cub_bytes);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+
+  const int gb = blocks_for(n, kThreads);
+  launch(ctx, [&] { k_init<<<1, 1, 0, st>>>(S, flags); });
+  ORCH_CUDA_TRY(cudaMemsetAsync(ident_count, 0, sizeof(int32_t) * (d + 1), st));
+  ORCH_CUDA_TRY(cudaMemsetAsync(a_count + d, 0, sizeof(int32_t), st));
+  ORCH_CUDA_TRY(cudaMemsetAsync(ident_len + n, 0, sizeof(int64_t), st));
+  if (n > 0)
+    launch(ctx, [&] {
+      k_validate<<<gb, kThreads, 0, st>>>(d, n, len, origin, key_len, key_org, iota, flags);
+    });
+  launch(ctx, [&] { k_validate_finish<<<1, 1, 0, st>>>(n, flags, S); });
+
+  // ---- identity (origin) batches: always needed (never_worse)
+  if (n > 0) {
+    size_t tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key_org, sorted_org, iota,
+                                                  ident_order, (int)n, 0, obits, st));
+    launch(ctx, [&] {
+      k_ident_count<<<gb, kThreads, 0, st>>>(n, ident_order, origin, len, ident_count, ident_len, S);
+    });
+  }
+  {
+    size_t tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ident_count, ident_offset, d + 1, st));
+  }
+  if (n > 0) {
+    size_t tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ident_len, ident_prefix, (int)n + 1, st));
+    launch(ctx, [&] {
+      k_ident_slots<<<gb, kThreads, 0, st>>>(n, ident_order, origin, ident_offset, ident_prefix,
+                                             src_slot, src_off, S);
+    });
+  }
+  const int cb = blocks_for(static_cast<int64_t>(d) * 32, kThreads);
+  launch(ctx, [&] {
+    k_bin_cost<<<cb, kThreads, 0, st>>>(model, d, ident_offset, ident_order, len, i_count, i_len,
+                                        i_tokens, i_cost, S);
+  });
+
+  // ---- the balancer's own packing
+  if (needs_desc && n > 0) {
+    size_t tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(cub_tmp, tb, key_len, xs, iota, order,
+                                                            (int)n, 0, 32, st));
+  }
+  if (needs_asc) {
+    size_t tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key_len, xs, iota, order, (int)n, 0,
+                                                  32, st));
+    launch(ctx, [&] { k_u32_to_i64<<<gb, kThreads, 0, st>>>(n, xs, asc_len); });
+    ORCH_CUDA_TRY(cudaMemsetAsync(asc_len + n, 0, sizeof(int64_t), st));
+    tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, asc_len, asc_prefix, (int)n + 1, st));
+    launch(ctx, [&] {
+      k_padded_search<<<1, 1024, 0, st>>>(d, n, xs, mode == 3 ? 1 : 0, probe, starts, n_groups,
+                                          bound, S);
+    });
+    if (padded_only) {
+      if (mode == 2 && d_bound_out)
+        ORCH_CUDA_TRY(cudaMemcpyAsync(d_bound_out, bound, sizeof(int64_t),
+                                      cudaMemcpyDeviceToDevice, st));
+      if (mode == 3 && d_probe_out)
+        ORCH_CUDA_TRY(cudaMemcpyAsync(d_probe_out, n_groups, sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, st));
+      return ORCH_OK;
+    }
+    launch(ctx, [&] {
+      k_padded_place<<<gb, kThreads, 0, st>>>(d, n, order, asc_prefix, starts, n_groups, dest_inst,
+                                              dest_slot, dst_off, bin_offset, bin_member, a_count,
+                                              a_tokens, S);
+    });
+  }
+  if (!identity_only && kind != ORCH_BINARY_PADDED) {
+    if (kind == ORCH_GREEDY_UNPADDED) {
+      rc = launch_greedy(ctx, d, n, nullptr, xs, order, nullptr, nullptr, dest_inst, dest_slot,
+                         dst_off, a_count, a_tokens, S, st);
+      if (rc) return rc;
+    } else if (kind == ORCH_QUADRATIC_TOLERANCE) {
+      const size_t sm = (2 * sizeof(int64_t) + sizeof(int32_t)) * d;
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_quadtol, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm));
+      launch(ctx, [&] {
+        k_quadtol<<<1, 32, sm, st>>>(d, n, pol->tolerance_v, xs, order, dest_inst, dest_slot,
+                                     dst_off, a_count, a_tokens, S);
+      });
+    } else {  // ConvTransformer
+      rc = launch_greedy(ctx, d, n, nullptr, xs, order, nullptr, nullptr, g_di, g_ds, g_doff,
+                         a_count, a_tokens, S, st);
+      if (rc) return rc;
+      launch(ctx, [&] {
+        k_conv_seed<<<1, 32, 0, st>>>(d, n, xs, order, a_tokens, dest_inst, dest_slot, dst_off,
+                                      seed_load, seed_count, consumed, S);
+      });
+      rc = launch_greedy(ctx, d, n, consumed, xs, order, seed_load, seed_count, dest_inst,
+                         dest_slot, dst_off, a_count, a_tokens, S, st);
+      if (rc) return rc;
+    }
+    size_t tb = cub_bytes;
+    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, a_count, bin_offset, d + 1, st));
+    if (n > 0)
+      launch(ctx, [&] {
+        k_scatter_members<<<gb, kThreads, 0, st>>>(n, dest_inst, dest_slot, bin_offset,
+                                                   bin_member, S);
+      });
+  }
+  if (!identity_only)
+    launch(ctx, [&] {
+      k_bin_cost<<<cb, kThreads, 0, st>>>(model, d, bin_offset, bin_member, len, bin_count,
+                                          bin_len, bin_tokens, bin_cost, S);
+    });
+  launch(ctx, [&] {
+    k_decide<<<1, 1024, 0, st>>>(d, identity_only, i_cost, identity_only ? i_cost : bin_cost, S);
+  });
+  const int fb = blocks_for(std::max<int64_t>(n, d + 1), kThreads);
+  launch(ctx, [&] {
+    k_apply_identity<<<fb, kThreads, 0, st>>>(
+        d, n, origin, src_slot, src_off, ident_offset, ident_order, i_count, i_len, i_tokens,
+        i_cost, dest_inst, dest_slot, dst_off, bin_offset, bin_member, bin_count, bin_len,
+        bin_tokens, bin_cost, S);
+  });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+}  // namespace orchb
+
+namespace {
+
+int device_error_message(int code, int64_t idx, int d, const int64_t* h_len,
+                         const int32_t* h_origin) {
+  if (code == ORCH_INVALID_ARGUMENT && h_len && h_origin) {
+    if (h_origin[idx] < 0 || h_origin[idx] >= d)
+      return orchb::fail(code, "item origin instance outside [0, d)");
+    return orchb::fail(code, "item length must be >= 1");
+  }
+  if (code == ORCH_INVALID_ARGUMENT) return orchb::fail(code, "invalid item at input position " + std::to_string(idx));
+  return orchb::fail(code, "input exceeds the device limits (length < 2^32, total tokens < 2^50)");
+}
+
+struct HostStage {
+  int64_t* len;
+  int32_t* origin;
+  orch_balance_out out;
+  orch_summary* summary;
+};
+
+}  // namespace
+
+extern "C" {
+
+int orch_balance(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                 const int64_t* d_len, const int32_t* d_origin, int32_t identity_only,
+                 const orch_balance_out* out, void* stream) {
+  if (!ctx) return orchb::fail(ORCH_INVALID_ARGUMENT, "null context");
+  int rc = orchb::check_policy_args(policy, d, n, identity_only);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
+  return orchb::run_balance(ctx, policy, d, n, d_len, d_origin, identity_only ? 1 : 0, 0, out,
+                            nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// Host-buffer variants keep their staging buffers in a second allocation so
+// the pipeline arena can be reserved independently.
+namespace {
+
+struct Staging {
+  void* base = nullptr;
+  size_t cap = 0;
+};
+thread_local Staging g_stage;
+
+int stage_reserve(size_t bytes) {
+  if (bytes <= g_stage.cap) return ORCH_OK;
+  if (g_stage.base) cudaFree(g_stage.base);
+  g_stage.base = nullptr;
+  size_t cap = 1 << 20;
+  while (cap < bytes) cap *= 2;
+  ORCH_CUDA_TRY(cudaMalloc(&g_stage.base, cap));
+  g_stage.cap = cap;
+  return ORCH_OK;
+}
+
+int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                  const int64_t* h_len, const int32_t* h_origin, int mode, int64_t probe,
+                  int32_t* h_dest_inst, int32_t* h_dest_slot, int64_t* h_dst_off,
+                  int32_t* h_bin_count, double* h_bin_cost, orch_summary* h_summary,
+                  int64_t* h_bound, int32_t* h_probe, cudaStream_t st) {
+  if (!ctx) return orchb::fail(ORCH_INVALID_ARGUMENT, "null context");
+  ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+  auto al = [](size_t b) { return (b + 255) & ~size_t{255}; };
+  const size_t need = al(nn * 8) + al(nn * 4) + 2 * al(nn * 4) + al(nn * 8) + al(d * 4) +
+                      al(d * 8) + al(sizeof(orch_summary)) + 2 * al(8);
+  int rc = stage_reserve(need);
+  if (rc) return rc;
+  char* p = static_cast<char*>(g_stage.base);
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += al(b);
+    return r;
+  };
+  int64_t* len = reinterpret_cast<int64_t*>(take(nn * 8));
+  int32_t* origin = reinterpret_cast<int32_t*>(take(nn * 4));
+  orch_balance_out out{};
+  out.dest_inst = reinterpret_cast<int32_t*>(take(nn * 4));
+  out.dest_slot = reinterpret_cast<int32_t*>(take(nn * 4));
+  out.dst_off = reinterpret_cast<int64_t*>(take(nn * 8));
+  out.bin_count = reinterpret_cast<int32_t*>(take(d * 4));
+  out.bin_cost = reinterpret_cast<double*>(take(d * 8));
+  out.summary = reinterpret_cast<orch_summary*>(take(sizeof(orch_summary)));
+  int64_t* d_bound = reinterpret_cast<int64_t*>(take(8));
+  int32_t* d_probe = reinterpret_cast<int32_t*>(take(8));
+  if (n > 0) {
+    ORCH_CUDA_TRY(cudaMemcpyAsync(len, h_len, n * 8, cudaMemcpyHostToDevice, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(origin, h_origin, n * 4, cudaMemcpyHostToDevice, st));
+  }
+  rc = orchb::run_balance(ctx, policy, d, n, len, origin, mode, probe, &out, d_bound, d_probe, st);
+  if (rc) return rc;
+  orch_summary sum;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(&sum, out.summary, sizeof sum, cudaMemcpyDeviceToHost, st));
+  if (n > 0 && mode < 2) {
+    if (h_dest_inst)
+      ORCH_CUDA_TRY(cudaMemcpyAsync(h_dest_inst, out.dest_inst, n * 4, cudaMemcpyDeviceToHost, st));
+    if (h_dest_slot)
+      ORCH_CUDA_TRY(cudaMemcpyAsync(h_dest_slot, out.dest_slot, n * 4, cudaMemcpyDeviceToHost, st));
+    if (h_dst_off)
+      ORCH_CUDA_TRY(cudaMemcpyAsync(h_dst_off, out.dst_off, n * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (mode < 2) {
+    if (h_bin_count)
+      ORCH_CUDA_TRY(cudaMemcpyAsync(h_bin_count, out.bin_count, d * 4, cudaMemcpyDeviceToHost, st));
+    if (h_bin_cost)
+      ORCH_CUDA_TRY(cudaMemcpyAsync(h_bin_cost, out.bin_cost, d * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (mode == 2 && h_bound)
+    ORCH_CUDA_TRY(cudaMemcpyAsync(h_bound, d_bound, 8, cudaMemcpyDeviceToHost, st));
+  if (mode == 3 && h_probe)
+    ORCH_CUDA_TRY(cudaMemcpyAsync(h_probe, d_probe, 4, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_summary) *h_summary = sum;
+  if (sum.error) return device_error_message(sum.error, sum.error_index, d, h_len, h_origin);
+  return ORCH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int orch_balance_host(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                      const int64_t* h_len, const int32_t* h_origin, int32_t identity_only,
+                      int32_t* h_dest_inst, int32_t* h_dest_slot, int64_t* h_dst_off,
+                      int32_t* h_bin_count, double* h_bin_cost, orch_summary* h_summary,
+                      void* stream) {
+  int rc = orchb::check_policy_args(policy, d, n, identity_only);
+  if (rc) return rc;
+  return host_pipeline(ctx, policy, d, n, h_len, h_origin, identity_only ? 1 : 0, 0, h_dest_inst,
+                       h_dest_slot, h_dst_off, h_bin_count, h_bin_cost, h_summary, nullptr,
+                       nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int orch_min_feasible_padded_bound_host(orch_ctx* ctx, int32_t d, int64_t n,
+                                        const int64_t* h_len, const int32_t* h_origin,
+                                        int64_t* h_bound, void* stream) {
+  orch_policy p{ORCH_BINARY_PADDED, 0, 0, 0.0};
+  int rc = orchb::check_policy_args(&p, d, n, 0);
+  if (rc) return rc;
+  return host_pipeline(ctx, &p, d, n, h_len, h_origin, 2, 0, nullptr, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, h_bound, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int orch_padded_bound_feasible_host(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* h_len,
+                                    const int32_t* h_origin, int64_t bound, int32_t* h_feasible,
+                                    void* stream) {
+  orch_policy p{ORCH_BINARY_PADDED, 0, 0, 0.0};
+  int rc = orchb::check_policy_args(&p, d, n, 0);
+  if (rc) return rc;
+  return host_pipeline(ctx, &p, d, n, h_len, h_origin, 3, bound, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, nullptr, nullptr, h_feasible,
+                       static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// Shared plumbing of the sm_100a dispatcher library: context/workspace,
+// error reporting, launch accounting, exact double arithmetic helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "orchsim_capi.h"
+
+namespace orchb {
+
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+// Thread-local message for orch_last_error().
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define ORCH_CUDA_TRY(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return ::orchb::fail(ORCH_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Device workspace: one growable arena per context; carve() hands out
+// 256-byte aligned slices that stay valid until the next reset().
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  size_t high = 0;  // high-water mark of the current pass
+};
+
+}  // namespace orchb
+
+struct orch_ctx {
+  int device = 0;
+  orchb::Arena arena;
+  // Pinned host staging for small device->host reads.
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
+  int64_t launches = 0;
+};
+
+namespace orchb {
+
+// Reserve `bytes` in the arena, growing it (synchronously, outside timed
+// steady state) when needed. Returns nullptr on allocation failure.
+void* carve(orch_ctx* ctx, size_t bytes);
+void arena_reset(orch_ctx* ctx);
+// Make sure the arena can hold `bytes` without reallocation.
+int arena_reserve(orch_ctx* ctx, size_t bytes, cudaStream_t stream);
+void* pinned(orch_ctx* ctx, size_t bytes);
+
+inline unsigned ceil_log2(unsigned long long x) {
+  unsigned b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+
+inline int blocks_for(int64_t n, int threads, int cap = kSMs * 8) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<int>(b);
+}
+
+}  // namespace orchb
+
+// ---- exact IEEE double helpers: the reference compiles cost() without FMA
+// (SURVEY.md section 0.6); every product/sum is an explicitly rounded op.
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_div(double a, double b) { return __ddiv_rn(a, b); }
+
+// cost() of one batch (core.cpp:91-118) from its reductions. count = items,
+// tokens = sum of lengths, longest = max length, sq = sum of l*l as the
+// reference's sequential double accumulation (exact integer when < 2^53).
+__device__ __forceinline__ double batch_cost(const orch_cost_model& m, int64_t count,
+                                             int64_t tokens, int64_t longest, double sq) {
+  if (count == 0) return 0.0;
+  const int64_t blen = m.padded ? count * longest : tokens;  // core.cpp:70-89
+  const double linear = rn_mul(m.alpha, static_cast<double>(blen));
+  switch (m.variant) {
+    case ORCH_LINEAR_ONLY:
+      return linear;
+    case ORCH_TRANSFORMER_QUADRATIC:
+      if (!m.padded) return rn_add(linear, rn_mul(m.beta, sq));
+      {
+        const double p = static_cast<double>(blen);
+        return rn_add(linear, rn_mul(rn_mul(rn_div(m.beta, static_cast<double>(count)), p), p));
+      }
+    default: {
+      const double lo = static_cast<double>(longest);
+      return rn_add(linear, rn_mul(rn_mul(rn_mul(m.beta, static_cast<double>(count)), lo), lo));
+    }
+  }
+}

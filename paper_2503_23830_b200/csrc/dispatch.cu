@@ -1,0 +1,795 @@
+// Send/recv layout and token-row movement of the exchange (C-ABI
+// orch_volume_matrix / orch_layout / orch_dispatch), cost model entry points
+// and the NCCL communicator. Row movement realises apply() (core.cpp:120-161)
+// on bf16 token rows: every item is a contiguous run of len rows in its origin
+// rank's input buffer and lands as a contiguous run in its destination rank's
+// output buffer; off-rank runs travel through one grouped NCCL send/recv.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <nccl.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "balance_kernels.cuh"
+#include "plan.cuh"
+
+struct orch_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0;
+  int size = 1;
+  int device = 0;
+};
+
+namespace orchb {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMoveThreads = 256;
+constexpr int kUnitRows = 8;  // rows per work unit of the movement kernels
+
+template <class F>
+void launch(orch_ctx* ctx, F&& f) {
+  f();
+  ++ctx->launches;
+}
+
+#define ORCH_NCCL_TRY(expr)                                                          \
+  do {                                                                              \
+    ncclResult_t r_ = (expr);                                                       \
+    if (r_ != ncclSuccess)                                                          \
+      return ::orchb::fail(ORCH_NCCL_ERROR, std::string(#expr ": ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ------------------------------------------------------------ volume matrix
+// topology.cpp:40-53: V[src][dst] += length. Integer atomics: exact and
+// order-independent.
+__global__ void k_volume(int d, int64_t n, const int64_t* __restrict__ len,
+                         const int32_t* __restrict__ origin, const int32_t* __restrict__ dest,
+                         unsigned long long* __restrict__ V) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&V[static_cast<size_t>(origin[i]) * d + dest[i]],
+              static_cast<unsigned long long>(len[i]));
+}
+
+// ------------------------------------------------------------------ layout
+// Per-instance token totals of the origin and destination batches.
+__global__ void k_inst_rows(int64_t n, const int64_t* __restrict__ len,
+                            const int32_t* __restrict__ origin, const int32_t* __restrict__ dest,
+                            unsigned long long* __restrict__ inst_in,
+                            unsigned long long* __restrict__ inst_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(&inst_in[origin[i]], static_cast<unsigned long long>(len[i]));
+    atomicAdd(&inst_out[dest[i]], static_cast<unsigned long long>(len[i]));
+  }
+}
+
+// Instance bases inside their rank buffers (instances of a rank are
+// consecutive): one thread per rank.
+__global__ void k_inst_bases(int d, int P, const unsigned long long* __restrict__ inst_in,
+                             const unsigned long long* __restrict__ inst_out,
+                             int64_t* __restrict__ base_in, int64_t* __restrict__ base_out,
+                             int64_t* __restrict__ in_rows, int64_t* __restrict__ out_rows) {
+  const int c = d / P;
+  for (int r = threadIdx.x; r < P; r += blockDim.x) {
+    int64_t a = 0, b = 0;
+    for (int i = r * c; i < (r + 1) * c; ++i) {
+      base_in[i] = a;
+      base_out[i] = b;
+      a += static_cast<int64_t>(inst_in[i]);
+      b += static_cast<int64_t>(inst_out[i]);
+    }
+    in_rows[r] = a;
+    out_rows[r] = b;
+  }
+}
+
+__global__ void k_rank_offsets(int64_t n, const int32_t* __restrict__ origin,
+                               const int32_t* __restrict__ dest, const int64_t* __restrict__ src_off,
+                               const int64_t* __restrict__ dst_off,
+                               const int64_t* __restrict__ base_in,
+                               const int64_t* __restrict__ base_out,
+                               int64_t* __restrict__ rank_src_off,
+                               int64_t* __restrict__ rank_dst_off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    rank_src_off[i] = base_in[origin[i]] + src_off[i];
+    rank_dst_off[i] = base_out[dest[i]] + dst_off[i];
+  }
+}
+
+// Within each destination batch (slot order), the running row offset of the
+// item among items from the same ORIGIN RANK (warp per batch, P <= 8 lanes of
+// warp scans per 32 items), plus per-(batch, origin rank) totals W.
+__global__ void k_pair_within(int d, int P, const int32_t* __restrict__ bin_offset,
+                              const int32_t* __restrict__ bin_member,
+                              const int64_t* __restrict__ len, const int32_t* __restrict__ origin,
+                              int64_t* __restrict__ pair_off, int64_t* __restrict__ W) {
+  const int lane = threadIdx.x & 31;
+  const int c = d / P;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < d; j += warps) {
+    int64_t run[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int beg = bin_offset[j], end = bin_offset[j + 1];
+    for (int base = beg; base < end; base += 32) {
+      const int k = base + lane;
+      int32_t pos = 0, r = -1;
+      int64_t l = 0;
+      if (k < end) {
+        pos = bin_member[k];
+        l = len[pos];
+        r = origin[pos] / c;
+      }
+      int64_t mine = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q >= P) break;
+        int64_t v = r == q ? l : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int64_t o = __shfl_up_sync(~0u, incl, off);
+          if (lane >= off) incl += o;
+        }
+        if (r == q) mine = run[q] + incl - v;
+        run[q] += __shfl_sync(~0u, incl, 31);
+      }
+      if (k < end) pair_off[pos] = mine;
+    }
+    if (lane < P) {
+      int64_t v = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q == lane) v = run[q];
+      W[j * P + lane] = v;
+    }
+  }
+}
+
+// Segment bases: for dest rank q and origin rank r, the rows from r into the
+// batches of q before batch j; per-pair send counts and NCCL displacements.
+__global__ void k_pair_bases(int d, int P, const int64_t* __restrict__ W,
+                             int64_t* __restrict__ Wbase, int64_t* __restrict__ send_rows,
+                             int64_t* __restrict__ send_displ, int64_t* __restrict__ recv_displ) {
+  const int c = d / P;
+  const int t = threadIdx.x;
+  if (t < P * P) {
+    const int q = t / P, r = t % P;
+    int64_t acc = 0;
+    for (int j = q * c; j < (q + 1) * c; ++j) {
+      Wbase[j * P + r] = acc;
+      acc += W[j * P + r];
+    }
+    send_rows[r * P + q] = acc;
+  }
+  __syncthreads();
+  if (t < P) {  // rank t's send buffer: segments q != t in q order
+    int64_t a = 0;
+    for (int q = 0; q < P; ++q) {
+      send_displ[t * P + q] = q == t ? 0 : a;
+      if (q != t) a += send_rows[t * P + q];
+    }
+    int64_t b = 0;  // rank t's recv buffer: segments r != t in r order
+    for (int r = 0; r < P; ++r) {
+      recv_displ[t * P + r] = r == t ? 0 : b;
+      if (r != t) b += send_rows[r * P + t];
+    }
+  }
+}
+
+__global__ void k_pair_apply(int64_t n, int d, int P, const int32_t* __restrict__ origin,
+                             const int32_t* __restrict__ dest, const int64_t* __restrict__ Wbase,
+                             int64_t* __restrict__ pair_off) {
+  const int c = d / P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pair_off[i] += Wbase[static_cast<int64_t>(dest[i]) * P + origin[i] / c];
+}
+
+// ---------------------------------------------------------------- movement
+// Work units of kUnitRows rows along an iteration buffer (a rank's input or
+// output buffer). unit_first[u] = slice index of the item holding row
+// u*kUnitRows. Items are >= 1 row, so a unit touches at most kUnitRows items.
+// The slice [offs[lo], offs[hi]) of a CSR is read on the device.
+__global__ void k_unit_map(const int32_t* __restrict__ offs, int lo_idx, int hi_idx,
+                           const int32_t* __restrict__ members,
+                           const int64_t* __restrict__ iter_off, const int64_t* __restrict__ len,
+                           int32_t* __restrict__ unit_first, int64_t cap_units) {
+  const int64_t beg = offs[lo_idx], end = offs[hi_idx];
+  for (int64_t k = beg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < end;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t pos = members[k];
+    const int64_t a = iter_off[pos], b = a + len[pos];
+    for (int64_t u = (a + kUnitRows - 1) / kUnitRows; u * kUnitRows < b && u < cap_units; ++u)
+      unit_first[u] = static_cast<int32_t>(k - beg);
+  }
+}
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// Block-wide copy of nvec 16-byte vectors, 4 loads in flight per thread.
+__device__ __forceinline__ void block_copy(int4* __restrict__ dst, const int4* __restrict__ src,
+                                           int64_t nvec) {
+  constexpr int U = 4;
+  int64_t v = threadIdx.x;
+  for (; v + (U - 1) * kMoveThreads < nvec; v += U * kMoveThreads) {
+    int4 t[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) t[j] = ld_stream(src + v + j * kMoveThreads);
+#pragma unroll
+    for (int j = 0; j < U; ++j) st_stream(dst + v + j * kMoveThreads, t[j]);
+  }
+  for (; v < nvec; v += kMoveThreads) st_stream(dst + v, ld_stream(src + v));
+}
+
+enum MoveMode { kLocal = 0, kPack = 1, kUnpack = 2 };
+
+struct MoveArgs {
+  int me, P, c;
+  const int32_t* offs;  // CSR offsets of the iteration order
+  int lo_idx, hi_idx;
+  const int32_t* members;
+  const int64_t* iter_rows;  // [P] rows of the iterated buffer per rank
+  int64_t iter_cap;          // capacity of the iterated buffer (rows)
+  int64_t out_cap;           // capacity of the output buffer (rows)
+  const int64_t* out_rows;   // [P]
+  const int64_t* in_rows;    // [P]
+  int64_t in_cap;            // capacity of the input buffer (rows)
+  const int64_t* send_rows;  // [P*P]
+  int64_t send_cap;
+  const int64_t* len;
+  const int32_t* origin;
+  const int32_t* dest;
+  const int64_t* rank_src_off;
+  const int64_t* rank_dst_off;
+  const int64_t* pair_off;
+  const int64_t* displ;  // send_displ row of me (pack) / recv_displ row of me (unpack)
+  const int32_t* unit_first;
+  int32_t* status;
+  size_t R;
+  const char* in;
+  char* out;
+  char* send;
+  const char* recv;
+};
+
+// Persistent movement kernel. Iterates the units of one rank buffer:
+//   kLocal : output buffer order, in -> out                     (one rank)
+//   kPack  : input buffer order, in -> out (item stays on rank) or -> send
+//   kUnpack: output buffer order, recv -> out (off-rank items only)
+template <int MODE>
+__global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
+  const int64_t total = a.iter_rows[a.me];
+  bool over = total > a.iter_cap || a.out_rows[a.me] > a.out_cap;
+  if (MODE != kUnpack) over = over || a.in_rows[a.me] > a.in_cap;
+  if (MODE == kPack) {
+    int64_t st = 0;
+    for (int q = 0; q < a.P; ++q)
+      if (q != a.me) st += a.send_rows[a.me * a.P + q];
+    over = over || st > a.send_cap;
+  }
+  if (over) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.status = ORCH_INVALID_ARGUMENT;
+    return;
+  }
+  const int64_t beg = a.offs[a.lo_idx], end = a.offs[a.hi_idx];
+  const int64_t units = (total + kUnitRows - 1) / kUnitRows;
+  const int64_t vrow = static_cast<int64_t>(a.R / 16);
+  const size_t R = a.R;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t row0 = u * kUnitRows;
+    const int64_t row1 = row0 + kUnitRows < total ? row0 + kUnitRows : total;
+    for (int64_t k = beg + a.unit_first[u]; k < end; ++k) {
+      const int32_t pos = a.members[k];
+      const int64_t off = MODE == kPack ? a.rank_src_off[pos] : a.rank_dst_off[pos];
+      if (off >= row1) break;
+      const int64_t l = a.len[pos];
+      const int64_t lo = off > row0 ? off : row0;
+      const int64_t hi = off + l < row1 ? off + l : row1;
+      const int64_t skip = lo - off;
+      const char* s;
+      char* t;
+      if (MODE == kLocal) {
+        s = a.in + (a.rank_src_off[pos] + skip) * R;
+        t = a.out + lo * R;
+      } else if (MODE == kPack) {
+        s = a.in + lo * R;
+        const int q = a.dest[pos] / a.c;
+        t = q == a.me ? a.out + (a.rank_dst_off[pos] + skip) * R
+                      : a.send + (a.displ[q] + a.pair_off[pos] + skip) * R;
+      } else {
+        const int r = a.origin[pos] / a.c;
+        if (r == a.me) continue;  // moved by the pack kernel
+        s = a.recv + (a.displ[r] + a.pair_off[pos] + skip) * R;
+        t = a.out + lo * R;
+      }
+      block_copy(reinterpret_cast<int4*>(t), reinterpret_cast<const int4*>(s), (hi - lo) * vrow);
+    }
+  }
+}
+
+// ----------------------------------------------------- all-gather scatter
+__global__ void k_pack_records(int64_t local_n, int64_t max_local, const int64_t* __restrict__ pos,
+                               const int64_t* __restrict__ len, const int32_t* __restrict__ org,
+                               int64_t* __restrict__ rec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < max_local;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    rec[3 * i] = i < local_n ? pos[i] : -1;
+    rec[3 * i + 1] = i < local_n ? len[i] : 0;
+    rec[3 * i + 2] = i < local_n ? org[i] : 0;
+  }
+}
+
+__global__ void k_scatter_records(int64_t total, int64_t n, const int64_t* __restrict__ rec,
+                                  int64_t* __restrict__ len, int32_t* __restrict__ org,
+                                  unsigned int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = rec[3 * i];
+    if (p < 0) continue;
+    if (p >= n) {
+      atomicOr(bad, 1u);
+      continue;
+    }
+    len[p] = rec[3 * i + 1];
+    org[p] = static_cast<int32_t>(rec[3 * i + 2]);
+  }
+}
+
+// ------------------------------------------------------- encode_lengths
+__global__ void k_encode(int64_t E, const int32_t* __restrict__ part_offset,
+                         const int32_t* __restrict__ modality, const int64_t* __restrict__ meta,
+                         int32_t M, const int64_t* __restrict__ rates,
+                         int64_t* __restrict__ encoded, int64_t* __restrict__ inter) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t sum = 0;
+    for (int p = part_offset[e]; p < part_offset[e + 1]; ++p) {
+      const int32_t m = modality[p];
+      const int64_t rate = (m >= 0 && m < M) ? rates[m] : 1;  // unknown modality: rate 1
+      const int64_t enc = (meta[p] + rate - 1) / rate;         // core.cpp:176-179
+      if (encoded) encoded[p] = enc;
+      sum += enc;
+    }
+    if (inter) inter[e] = sum;  // interleaved_length, core.cpp:163-169
+  }
+}
+
+}  // namespace
+
+}  // namespace orchb
+
+using namespace orchb;
+
+extern "C" {
+
+int orch_volume_matrix(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
+                       const int32_t* d_origin, const int32_t* d_dest_inst, int64_t* d_V,
+                       void* stream) {
+  if (!ctx) return fail(ORCH_INVALID_ARGUMENT, "null context");
+  if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
+  auto st = static_cast<cudaStream_t>(stream);
+  ORCH_CUDA_TRY(cudaMemsetAsync(d_V, 0, sizeof(int64_t) * static_cast<size_t>(d) * d, st));
+  if (n > 0)
+    launch(ctx, [&] {
+      k_volume<<<blocks_for(n, kThreads), kThreads, 0, st>>>(
+          d, n, d_len, d_origin, d_dest_inst, reinterpret_cast<unsigned long long*>(d_V));
+    });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+int orch_layout(orch_ctx* ctx, int32_t d, int32_t P, int64_t n, const int64_t* d_len,
+                const int32_t* d_origin, const orch_balance_out* bal,
+                const orch_layout_out* L, void* stream) {
+  if (!ctx || !bal || !L) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (P < 1 || P > 8 || d % P != 0)
+    return fail(ORCH_INVALID_ARGUMENT, "rank count must be in [1, 8] and divide the instance count");
+  if (!bal->dest_inst || !bal->src_off || !bal->dst_off || !bal->bin_offset || !bal->bin_member)
+    return fail(ORCH_INVALID_ARGUMENT, "orch_layout needs dest_inst, src_off, dst_off, bin_offset, bin_member");
+  auto st = static_cast<cudaStream_t>(stream);
+  Plan plan;
+  unsigned long long *inst_in, *inst_out;
+  int64_t *base_in, *base_out, *W, *Wbase;
+  plan.add(&inst_in, d);
+  plan.add(&inst_out, d);
+  plan.add(&base_in, d);
+  plan.add(&base_out, d);
+  plan.add(&W, static_cast<size_t>(d) * P);
+  plan.add(&Wbase, static_cast<size_t>(d) * P);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  if (!L->status) return fail(ORCH_INVALID_ARGUMENT, "layout->status is required");
+  ORCH_CUDA_TRY(cudaMemsetAsync(L->status, 0, sizeof(int32_t), st));
+  ORCH_CUDA_TRY(cudaMemsetAsync(inst_in, 0, sizeof(uint64_t) * d, st));
+  ORCH_CUDA_TRY(cudaMemsetAsync(inst_out, 0, sizeof(uint64_t) * d, st));
+  const int gb = blocks_for(n, kThreads);
+  if (n > 0)
+    launch(ctx, [&] {
+      k_inst_rows<<<gb, kThreads, 0, st>>>(n, d_len, d_origin, bal->dest_inst, inst_in, inst_out);
+    });
+  launch(ctx, [&] {
+    k_inst_bases<<<1, 32, 0, st>>>(d, P, inst_in, inst_out, base_in, base_out, L->in_rows,
+                                   L->out_rows);
+  });
+  if (n > 0)
+    launch(ctx, [&] {
+      k_rank_offsets<<<gb, kThreads, 0, st>>>(n, d_origin, bal->dest_inst, bal->src_off,
+                                              bal->dst_off, base_in, base_out, L->rank_src_off,
+                                              L->rank_dst_off);
+    });
+  launch(ctx, [&] {
+    k_pair_within<<<blocks_for(static_cast<int64_t>(d) * 32, kThreads), kThreads, 0, st>>>(
+        d, P, bal->bin_offset, bal->bin_member, d_len, d_origin, L->pair_off, W);
+  });
+  launch(ctx, [&] {
+    k_pair_bases<<<1, 64, 0, st>>>(d, P, W, Wbase, L->send_rows, L->send_displ, L->recv_displ);
+  });
+  if (n > 0)
+    launch(ctx, [&] {
+      k_pair_apply<<<gb, kThreads, 0, st>>>(n, d, P, d_origin, bal->dest_inst, Wbase, L->pair_off);
+    });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_move_args(orch_ctx* ctx, int P, int me, int d, const orch_balance_out* bal,
+                    const orch_layout_out* L, size_t R) {
+  if (!ctx || !bal || !L) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (R == 0 || R % 16 != 0)
+    return fail(ORCH_INVALID_ARGUMENT, "row_bytes must be a positive multiple of 16");
+  if (P < 1 || P > 8 || me < 0 || me >= P || d % P != 0)
+    return fail(ORCH_INVALID_ARGUMENT, "bad rank / rank count (must divide the instance count, <= 8)");
+  if (!bal->src_offset || !bal->src_member || !bal->bin_offset || !bal->bin_member ||
+      !bal->dest_inst || !L->status)
+    return fail(ORCH_INVALID_ARGUMENT, "movement needs the CSR outputs of orch_balance and layout->status");
+  return ORCH_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+MoveArgs make_args(int P, int me, int d, const int64_t* len, const int32_t* origin,
+                   const orch_balance_out* bal, const orch_layout_out* L, size_t R) {
+  MoveArgs a{};
+  a.me = me;
+  a.P = P;
+  a.c = d / P;
+  a.lo_idx = me * a.c;
+  a.hi_idx = (me + 1) * a.c;
+  a.out_rows = L->out_rows;
+  a.in_rows = L->in_rows;
+  a.send_rows = L->send_rows;
+  a.len = len;
+  a.origin = origin;
+  a.dest = bal->dest_inst;
+  a.rank_src_off = L->rank_src_off;
+  a.rank_dst_off = L->rank_dst_off;
+  a.pair_off = L->pair_off;
+  a.status = L->status;
+  a.R = R;
+  return a;
+}
+
+constexpr int kMoveGrid = kSMs * 8;
+
+int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter_off,
+             cudaStream_t st) {
+  Plan plan;
+  int32_t* unit_first;
+  const int64_t cap_units = a.iter_cap / kUnitRows + 2;
+  plan.add(&unit_first, static_cast<size_t>(cap_units));
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  a.unit_first = unit_first;
+  launch(ctx, [&] {
+    k_unit_map<<<blocks_for(n, kThreads), kThreads, 0, st>>>(a.offs, a.lo_idx, a.hi_idx,
+                                                             a.members, iter_off, a.len,
+                                                             unit_first, cap_units);
+  });
+  launch(ctx, [&] {
+    if (mode == kLocal)
+      k_move<kLocal><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+    else if (mode == kPack)
+      k_move<kPack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+    else
+      k_move<kUnpack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+  });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int orch_pack(orch_ctx* ctx, int32_t rank, int32_t nranks, int32_t d, int64_t n,
+              const int64_t* d_len, const int32_t* d_origin, const orch_balance_out* bal,
+              const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap, void* d_out,
+              int64_t out_cap, void* d_send, int64_t send_cap, void* stream) {
+  int rc = check_move_args(ctx, nranks, rank, d, bal, L, R);
+  if (rc) return rc;
+  if (!aligned16(d_in) || !aligned16(d_out) || !aligned16(d_send))
+    return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
+  if (n == 0) return ORCH_OK;
+  MoveArgs a = make_args(nranks, rank, d, d_len, d_origin, bal, L, R);
+  a.offs = bal->src_offset;
+  a.members = bal->src_member;
+  a.iter_rows = L->in_rows;
+  a.iter_cap = in_cap;
+  a.in_cap = in_cap;
+  a.out_cap = out_cap;
+  a.send_cap = send_cap;
+  a.displ = L->send_displ + rank * nranks;
+  a.in = static_cast<const char*>(d_in);
+  a.out = static_cast<char*>(d_out);
+  a.send = static_cast<char*>(d_send);
+  return run_move(ctx, kPack, a, n, L->rank_src_off, static_cast<cudaStream_t>(stream));
+}
+
+int orch_unpack(orch_ctx* ctx, int32_t rank, int32_t nranks, int32_t d, int64_t n,
+                const int64_t* d_len, const int32_t* d_origin, const orch_balance_out* bal,
+                const orch_layout_out* L, size_t R, const void* d_recv, void* d_out,
+                int64_t out_cap, void* stream) {
+  int rc = check_move_args(ctx, nranks, rank, d, bal, L, R);
+  if (rc) return rc;
+  if (!aligned16(d_recv) || !aligned16(d_out))
+    return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
+  if (n == 0) return ORCH_OK;
+  MoveArgs a = make_args(nranks, rank, d, d_len, d_origin, bal, L, R);
+  a.offs = bal->bin_offset;
+  a.members = bal->bin_member;
+  a.iter_rows = L->out_rows;
+  a.iter_cap = out_cap;
+  a.out_cap = out_cap;
+  a.displ = L->recv_displ + rank * nranks;
+  a.recv = static_cast<const char*>(d_recv);
+  a.out = static_cast<char*>(d_out);
+  return run_move(ctx, kUnpack, a, n, L->rank_dst_off, static_cast<cudaStream_t>(stream));
+}
+
+int orch_exchange(orch_ctx* ctx, orch_comm* comm, const orch_layout_out* L, size_t R,
+                  const void* d_send, void* d_recv, int64_t recv_cap, void* stream) {
+  if (!ctx || !comm || !L) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  const int P = comm->size, me = comm->rank;
+  auto st = static_cast<cudaStream_t>(stream);
+  int64_t* h = static_cast<int64_t*>(pinned(ctx, sizeof(int64_t) * 3 * P * P));
+  if (!h) return fail(ORCH_CUDA_ERROR, "pinned staging allocation failed");
+  int64_t *h_send = h, *h_sdis = h + P * P, *h_rdis = h + 2 * P * P;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(h_send, L->send_rows, sizeof(int64_t) * P * P,
+                                cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(h_sdis, L->send_displ, sizeof(int64_t) * P * P,
+                                cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(h_rdis, L->recv_displ, sizeof(int64_t) * P * P,
+                                cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));  // NCCL takes host-side counts
+  int64_t recv_total = 0;
+  for (int r = 0; r < P; ++r)
+    if (r != me) recv_total += h_send[r * P + me];
+  if (recv_total > recv_cap)
+    return fail(ORCH_INVALID_ARGUMENT, "receive buffer smaller than the incoming rows");
+  const char* send = static_cast<const char*>(d_send);
+  char* recv = static_cast<char*>(d_recv);
+  ORCH_NCCL_TRY(ncclGroupStart());
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const int64_t s_rows = h_send[me * P + q];
+    const int64_t r_rows = h_send[q * P + me];
+    if (s_rows > 0)
+      ORCH_NCCL_TRY(ncclSend(send + h_sdis[me * P + q] * R, static_cast<size_t>(s_rows) * R,
+                             ncclInt8, q, comm->comm, st));
+    if (r_rows > 0)
+      ORCH_NCCL_TRY(ncclRecv(recv + h_rdis[me * P + q] * R, static_cast<size_t>(r_rows) * R,
+                             ncclInt8, q, comm->comm, st));
+  }
+  ORCH_NCCL_TRY(ncclGroupEnd());
+  return ORCH_OK;
+}
+
+int orch_dispatch(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                  const int32_t* d_origin, const orch_balance_out* bal,
+                  const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap,
+                  void* d_out, int64_t out_cap, void* d_send, int64_t send_cap, void* d_recv,
+                  int64_t recv_cap, void* stream) {
+  const int P = comm ? comm->size : 1;
+  const int me = comm ? comm->rank : 0;
+  int rc = check_move_args(ctx, P, me, d, bal, L, R);
+  if (rc) return rc;
+  auto st = static_cast<cudaStream_t>(stream);
+  if (P == 1) {
+    if (!aligned16(d_in) || !aligned16(d_out))
+      return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
+    if (n == 0) return ORCH_OK;
+    MoveArgs a = make_args(1, 0, d, d_len, d_origin, bal, L, R);
+    a.offs = bal->bin_offset;
+    a.members = bal->bin_member;
+    a.iter_rows = L->out_rows;
+    a.iter_cap = out_cap;
+    a.out_cap = out_cap;
+    a.in_cap = in_cap;
+    a.in = static_cast<const char*>(d_in);
+    a.out = static_cast<char*>(d_out);
+    return run_move(ctx, kLocal, a, n, L->rank_dst_off, st);
+  }
+  rc = orch_pack(ctx, me, P, d, n, d_len, d_origin, bal, L, R, d_in, in_cap, d_out, out_cap,
+                 d_send, send_cap, stream);
+  if (rc) return rc;
+  rc = orch_exchange(ctx, comm, L, R, d_send, d_recv, recv_cap, stream);
+  if (rc) return rc;
+  return orch_unpack(ctx, me, P, d, n, d_len, d_origin, bal, L, R, d_recv, d_out, out_cap,
+                     stream);
+}
+
+// ------------------------------------------------------------- cost model
+int orch_batch_costs(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded, int32_t d,
+                     int64_t n, const int64_t* d_len, const int32_t* d_bin_offset,
+                     const int32_t* d_bin_member, double* d_cost, double* d_stats, void* stream) {
+  (void)n;
+  if (!ctx || !model) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if ((model->padded != 0) != (batch_padded != 0))
+    return fail(ORCH_INVALID_ARGUMENT, "cost model padding mode does not match batch padding mode");
+  if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
+  auto st = static_cast<cudaStream_t>(stream);
+  launch(ctx, [&] {
+    k_bin_cost<<<blocks_for(static_cast<int64_t>(d) * 32, kThreads), kThreads, 0, st>>>(
+        *model, d, d_bin_offset, d_bin_member, d_len, nullptr, nullptr, nullptr, d_cost, nullptr);
+  });
+  if (d_stats) {
+    launch(ctx, [&] { k_stats_only<<<1, 1024, 0, st>>>(d, d_cost, d_stats); });
+  }
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+int orch_group_by_origin(orch_ctx* ctx, int32_t d, int64_t n, const int32_t* d_origin,
+                         int32_t* d_bin_offset, int32_t* d_bin_member, void* stream) {
+  if (!ctx) return fail(ORCH_INVALID_ARGUMENT, "null context");
+  if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+  const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
+  Plan plan;
+  uint32_t *k_in, *k_out;
+  int32_t *iota, *cnt;
+  void* tmp;
+  plan.add(&k_in, nn);
+  plan.add(&k_out, nn);
+  plan.add(&iota, nn);
+  plan.add(&cnt, d + 1);
+  size_t tb = 0, b2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, iota, d_bin_member, (int)nn, 0, obits, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, b2, cnt, d_bin_offset, d + 1, st);
+  tb = std::max(tb, b2);
+  plan.add(reinterpret_cast<char**>(&tmp), tb);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (d + 1), st));
+  if (n > 0) {
+    launch(ctx, [&] {
+      k_origin_keys<<<blocks_for(n, kThreads), kThreads, 0, st>>>(d, n, d_origin, k_in, iota, cnt);
+    });
+    size_t t = tb;
+    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, t, k_in, k_out, iota, d_bin_member, (int)n,
+                                                  0, obits, st));
+  }
+  size_t t = tb;
+  ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t, cnt, d_bin_offset, d + 1, st));
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+int orch_encode_lengths(orch_ctx* ctx, int64_t E, const int32_t* d_part_offset,
+                        const int32_t* d_modality, const int64_t* d_meta_len, int32_t M,
+                        const int64_t* h_rates, int64_t* d_encoded, int64_t* d_interleaved,
+                        void* stream) {
+  if (!ctx) return fail(ORCH_INVALID_ARGUMENT, "null context");
+  if (M < 0 || M > 64) return fail(ORCH_INVALID_ARGUMENT, "modality count must be in [0, 64]");
+  for (int m = 0; m < M; ++m)
+    if (h_rates[m] < 1) return fail(ORCH_CONFIG_ERROR, "downsample rate must be >= 1");
+  auto st = static_cast<cudaStream_t>(stream);
+  Plan plan;
+  int64_t* rates;
+  plan.add(&rates, M > 0 ? M : 1);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  if (M > 0)
+    ORCH_CUDA_TRY(cudaMemcpyAsync(rates, h_rates, sizeof(int64_t) * M, cudaMemcpyHostToDevice, st));
+  if (E > 0)
+    launch(ctx, [&] {
+      k_encode<<<blocks_for(E, kThreads), kThreads, 0, st>>>(E, d_part_offset, d_modality,
+                                                             d_meta_len, M, rates, d_encoded,
+                                                             d_interleaved);
+    });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+// ---------------------------------------------------------------- NCCL
+int orch_comm_unique_id(unsigned char* h_id128) {
+  ncclUniqueId id;
+  ORCH_NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(h_id128, &id, sizeof id);
+  return ORCH_OK;
+}
+
+int orch_comm_create(int32_t nranks, int32_t rank, const unsigned char* h_id128,
+                     orch_comm** out) {
+  if (!out || !h_id128) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ORCH_INVALID_ARGUMENT, "bad rank");
+  ncclUniqueId id;
+  memcpy(&id, h_id128, sizeof id);
+  auto* c = new orch_comm();
+  ORCH_CUDA_TRY(cudaGetDevice(&c->device));
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(ORCH_NCCL_ERROR, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  c->rank = rank;
+  c->size = nranks;
+  *out = c;
+  return ORCH_OK;
+}
+
+void orch_comm_destroy(orch_comm* comm) {
+  if (!comm) return;
+  if (comm->comm) ncclCommDestroy(comm->comm);
+  delete comm;
+}
+
+int32_t orch_comm_rank(const orch_comm* comm) { return comm ? comm->rank : 0; }
+int32_t orch_comm_size(const orch_comm* comm) { return comm ? comm->size : 1; }
+
+int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_t max_local,
+                         const int64_t* d_local_pos, const int64_t* d_local_len,
+                         const int32_t* d_local_origin, int64_t n, int64_t* d_len,
+                         int32_t* d_origin, void* stream) {
+  if (!ctx || !comm) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (local_n > max_local || max_local < 0) return fail(ORCH_INVALID_ARGUMENT, "local_n > max_local");
+  auto st = static_cast<cudaStream_t>(stream);
+  const int P = comm->size;
+  Plan plan;
+  int64_t *sendrec, *recvrec;
+  unsigned int* bad;
+  plan.add(&sendrec, static_cast<size_t>(3 * (max_local > 0 ? max_local : 1)));
+  plan.add(&recvrec, static_cast<size_t>(3 * (max_local > 0 ? max_local : 1) * P));
+  plan.add(&bad, 1);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned int), st));
+  if (max_local > 0) {
+    launch(ctx, [&] {
+      k_pack_records<<<blocks_for(max_local, kThreads), kThreads, 0, st>>>(
+          local_n, max_local, d_local_pos, d_local_len, d_local_origin, sendrec);
+    });
+    ORCH_NCCL_TRY(ncclAllGather(sendrec, recvrec, static_cast<size_t>(3 * max_local), ncclInt64,
+                                comm->comm, st));
+    launch(ctx, [&] {
+      k_scatter_records<<<blocks_for(max_local * P, kThreads), kThreads, 0, st>>>(
+          max_local * P, n, recvrec, d_len, d_origin, bad);
+    });
+  }
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+"""GPU parity of the balance pipeline against the oracle (bit-exact).
+
+Every comparison is exact: assignment vectors, slots, token offsets, per-batch
+counts/lengths/tokens, per-batch costs and the objective compared as IEEE
+bits, the identity fallback flag, the CSR outputs. Cases follow the
+reference's own test generators (proj/tests/helpers.hpp:15-60,
+test_balancers.cpp) plus config-shaped and adversarial inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_instance
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [0, 1, 2, 3]
+
+
+def gpu_balance(ctx, kind, d, length, origin, lam=0.0, v=0, identity_only=False):
+    L = torch.from_numpy(np.ascontiguousarray(length, np.int64)).cuda()
+    O = torch.from_numpy(np.ascontiguousarray(origin, np.int32)).cuda()
+    b = ctx.balance(kind, d, L, O, lam=lam, v=v, identity_only=identity_only)
+    torch.cuda.synchronize()
+    return b
+
+
+def check_same(b, o, n, d):
+    s = b.summary()
+    assert s.error == 0, s.error
+    np.testing.assert_array_equal(b.dest_inst[:n].cpu().numpy(), o.dest_inst)
+    np.testing.assert_array_equal(b.dest_slot[:n].cpu().numpy(), o.dest_slot)
+    np.testing.assert_array_equal(b.src_slot[:n].cpu().numpy(), o.src_slot)
+    np.testing.assert_array_equal(b.src_off[:n].cpu().numpy(), o.src_off)
+    np.testing.assert_array_equal(b.dst_off[:n].cpu().numpy(), o.dst_off)
+    np.testing.assert_array_equal(b.bin_count.cpu().numpy(), o.bin_count)
+    np.testing.assert_array_equal(b.bin_len.cpu().numpy(), o.bin_len)
+    np.testing.assert_array_equal(b.bin_tokens.cpu().numpy(), o.bin_tokens)
+    assert b.bin_cost.cpu().numpy().tobytes() == o.bin_cost.tobytes()
+    assert np.float64(s.objective).tobytes() == np.float64(o.objective).tobytes()
+    assert s.used_identity == o.used_identity
+    # CSR consistency: members in (dest, slot) order
+    off = b.bin_offset.cpu().numpy()
+    mem = b.bin_member[:n].cpu().numpy()
+    assert off[0] == 0 and off[-1] == n
+    np.testing.assert_array_equal(np.diff(off), o.bin_count)
+    if n:
+        di, ds = o.dest_inst[mem], o.dest_slot[mem]
+        np.testing.assert_array_equal(di, np.repeat(np.arange(d), o.bin_count))
+        np.testing.assert_array_equal(ds, np.concatenate([np.arange(c) for c in o.bin_count]))
+    soff = b.src_offset.cpu().numpy()
+    assert soff[0] == 0 and soff[-1] == n
+
+
+def run_case(ctx, oracle, kind, d, length, origin, lam=0.0, v=0):
+    n = len(length)
+    o = oracle.balance(kind, d, length, origin, lam=lam, v=v)
+    b = gpu_balance(ctx, kind, d, length, origin, lam=lam, v=v)
+    check_same(b, o, n, d)
+    # source CSR = origin batches in input order
+    if n:
+        smem = b.src_member[:n].cpu().numpy()
+        np.testing.assert_array_equal(smem, np.argsort(np.asarray(origin), kind="stable"))
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_random_small(ctx, oracle, kind):
+    rng = np.random.default_rng(1000 + kind)
+    for trial in range(150):
+        d = int(rng.integers(1, 9))
+        n = int(rng.integers(1 if kind in (1, 3) else 0, 40))
+        hi = int(rng.choice([3, 10, 50, 5000]))
+        length, origin = random_instance(rng, d, n, 1, hi,
+                                         rng.choice(["random", "zero", "rr"]))
+        lam = float(rng.choice([0.0, 0.01, 0.05, 0.3]))
+        v = int(rng.choice([0, 1, 3, 20]))
+        run_case(ctx, oracle, kind, d, length, origin, lam, v)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_random_medium_large_d(ctx, oracle, kind):
+    """d > 32 exercises the round-batched block greedy."""
+    rng = np.random.default_rng(2000 + kind)
+    for trial in range(25):
+        d = int(rng.choice([33, 64, 100, 256, 511, 600, 1024]))
+        n = int(rng.integers(1, 6000))
+        hi = int(rng.choice([2, 8, 100, 4096, 100000]))
+        length, origin = random_instance(rng, d, n, 1, hi, rng.choice(["random", "zero", "rr"]))
+        run_case(ctx, oracle, kind, d, length, origin, lam=1e-4, v=int(rng.choice([0, 64, 2048])))
+
+
+def test_heavy_ties(ctx, oracle):
+    """All-equal lengths: every argmin is a tie broken by the lowest index."""
+    for d in (2, 7, 31, 32, 33, 64, 257):
+        for n in (1, d - 1, d, d + 1, 5 * d + 3):
+            if n < 1:
+                continue
+            length = np.full(n, 7, np.int64)
+            origin = (np.arange(n) % d).astype(np.int32)
+            for kind in KINDS:
+                run_case(ctx, oracle, kind, d, length, origin, lam=0.01, v=2)
+
+
+@pytest.mark.parametrize("shape", [(8, 512), (64, 4096), (2560, 76800), (4096, 40000)])
+def test_config_shapes_greedy(ctx, oracle, shape):
+    """C1 (DP=8x64), DP=64x64, C4 (DP=2560x30), and the d limit."""
+    d, n = shape
+    rng = np.random.default_rng(0xC1 + d)
+    length = rng.integers(128, 4097, n).astype(np.int64)
+    origin = (np.arange(n) % d).astype(np.int32)
+    run_case(ctx, oracle, 0, d, length, origin)
+
+
+@pytest.mark.parametrize("kind", [1, 2, 3])
+def test_config_shapes_other_policies(ctx, oracle, kind):
+    rng = np.random.default_rng(77 + kind)
+    for d, n in [(8, 512), (64, 4096), (256, 20000)]:
+        length = np.ceil(np.exp(rng.normal(6.5, 0.8, n))).clip(64, 4096).astype(np.int64)
+        origin = (np.arange(n) % d).astype(np.int32)
+        run_case(ctx, oracle, kind, d, length, origin, lam=1.0 / (6 * 8192), v=2048)
+
+
+def test_long_context_quadratic(ctx, oracle):
+    """C5: 32k-token sequences, quadratic cost, tolerance v=2048."""
+    rng = np.random.default_rng(5)
+    for P in (2, 4, 8):
+        n = 8 * P
+        length = rng.integers(8192, 32769, n).astype(np.int64)
+        origin = (np.arange(n) % P).astype(np.int32)
+        for kind in (0, 2):
+            run_case(ctx, oracle, kind, P, length, origin, lam=1.0 / (6 * 8192), v=2048)
+        run_case(ctx, oracle, 2, P, np.full(n, 32768, np.int64), origin, lam=2.03e-5, v=2048)
+
+
+def test_identity_arrangement(ctx, oracle):
+    rng = np.random.default_rng(9)
+    for kind in KINDS:
+        for _ in range(20):
+            d = int(rng.integers(1, 40))
+            n = int(rng.integers(0, 200))
+            length, origin = random_instance(rng, d, n, 1, 300)
+            o = oracle.identity(kind, d, length, origin, lam=0.02, v=3)
+            b = gpu_balance(ctx, kind, d, length, origin, lam=0.02, v=3, identity_only=True)
+            o.used_identity = 1
+            check_same(b, o, n, d)
+
+
+def test_reference_known_answers(ctx):
+    """Golden values of proj/tests/test_balancers.cpp."""
+    def items_on_zero(ls):
+        return np.asarray(ls, np.int64), np.zeros(len(ls), np.int32)
+
+    L, O = items_on_zero([5, 4, 3, 3, 2, 1])
+    r = ctx.balance_host(0, 2, L, O)
+    assert r["summary"].objective == 9.0                      # :40-46
+    L, O = items_on_zero([3, 3, 2, 2, 2])
+    assert ctx.balance_host(0, 2, L, O)["summary"].objective == 7.0  # :48-55
+    L, O = items_on_zero([7, 5, 3, 2])
+    r = ctx.balance_host(1, 2, L, O)
+    assert r["summary"].objective == 14.0                     # :71-81
+    assert ctx.min_feasible_padded_bound(2, L, O) == 14
+    L, O = items_on_zero([8, 8, 4, 4])
+    assert abs(ctx.balance_host(2, 2, L, O, lam=0.1, v=1)["summary"].objective - 20.0) < 1e-12
+    L, O = items_on_zero([6, 5, 4, 3])
+    assert abs(ctx.balance_host(3, 2, L, O, lam=0.05)["summary"].objective - 15.75) < 1e-12
+    L, O = items_on_zero([7])
+    assert abs(ctx.balance_host(2, 3, L, O, lam=0.2, v=2)["summary"].objective - (7 + 0.2 * 49)) < 1e-12
+    L, O = items_on_zero([9])
+    assert abs(ctx.balance_host(3, 2, L, O, lam=0.1)["summary"].objective - (9 + 0.1 * 81)) < 1e-12
+
+
+def test_errors_match_reference_classes(ctx, oracle):
+    from oracle import OracleError
+    from paper_2503_23830_b200.capi import OrchError
+    cases = [
+        (0, 0, [1], [0], 0.0, 0),     # d = 0
+        (0, 2, [1, 2], [0, 2], 0.0, 0),  # origin outside [0, d)
+        (0, 2, [1, 0], [0, 1], 0.0, 0),  # length 0
+        (1, 2, [], [], 0.0, 0),       # padded, empty
+        (3, 2, [], [], 0.1, 0),       # conv, empty
+        (2, 2, [1], [0], -1.0, 0),    # negative lambda
+        (2, 2, [1], [0], 0.0, -1),    # negative v
+        (3, 2, [1], [0], -0.5, 0),
+        (0, 3, [5, -1, 2], [0, 5, 1], 0.0, 0),  # first bad item decides the message
+    ]
+    for kind, d, L, O, lam, v in cases:
+        with pytest.raises(OracleError) as eo:
+            oracle.balance(kind, d, L, O, lam=lam, v=v)
+        with pytest.raises(OrchError) as eg:
+            ctx.balance_host(kind, d, L, O, lam=lam, v=v)
+        assert eg.value.code == eo.value.code
+        assert eg.value.msg == eo.value.msg
+
+
+def test_padded_bound_functions(ctx, oracle):
+    """test_balancers.cpp:96-110 (minimal feasible bound property), seed 47."""
+    rng = np.random.default_rng(47)
+    for _ in range(100):
+        d = int(rng.integers(1, 4))
+        n = int(rng.integers(1, 11))
+        L = rng.integers(1, 31, n).astype(np.int64)
+        O = (np.arange(n) % d).astype(np.int32)
+        b = ctx.min_feasible_padded_bound(d, L, O)
+        assert b == oracle.min_feasible_padded_bound(d, L, O)
+        assert ctx.padded_bound_feasible(d, L, O, b)
+        assert not ctx.padded_bound_feasible(d, L, O, b - 1)
+        assert ctx.padded_bound_feasible(d, L, O, int(L.max()) * (n // d + 1))
+
+
+def test_pre_post_stats(ctx, oracle):
+    rng = np.random.default_rng(13)
+    for kind in KINDS:
+        d, n = 16, 400
+        length, origin = random_instance(rng, d, n, 1, 3000)
+        o = oracle.balance(kind, d, length, origin, lam=0.001, v=10)
+        oi = oracle.identity(kind, d, length, origin, lam=0.001, v=10)
+        s = gpu_balance(ctx, kind, d, length, origin, lam=0.001, v=10).summary()
+        assert (s.pre_max, s.pre_mean, s.pre_ratio) == oracle.stats(oi.bin_cost)
+        assert (s.post_max, s.post_mean, s.post_ratio) == oracle.stats(o.bin_cost)
+
+
+def test_reference_library_agrees(ctx, reflib):
+    """Direct differential against the unmodified reference (oracle/_ref)."""
+    rng = np.random.default_rng(31)
+    for kind in KINDS:
+        for _ in range(40):
+            d = int(rng.integers(1, 70))
+            n = int(rng.integers(1, 500))
+            length, origin = random_instance(rng, d, n, 1, int(rng.choice([5, 500, 5000])))
+            di, ds, obj, _ = reflib.balance(kind, d, length, origin, lam=0.003, v=17)
+            b = gpu_balance(ctx, kind, d, length, origin, lam=0.003, v=17)
+            np.testing.assert_array_equal(b.dest_inst[:n].cpu().numpy(), di)
+            np.testing.assert_array_equal(b.dest_slot[:n].cpu().numpy(), ds)
+            assert np.float64(b.summary().objective).tobytes() == np.float64(obj).tobytes()
