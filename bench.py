@@ -1,0 +1,396 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Batch Post-Balancing Dispatcher (BASELINE.json metric).
+
+One step = one iteration's balance + dispatch of the C2 workload
+(BASELINE.json configs[1]): DP=8 instances, vision+text batch of 64 examples
+per instance from the reference's synthetic MCI generator, per-phase
+rebalancing (vision encoder phase on metadata lengths, LLM phase on
+interleaved lengths, GreedyUnpadded), bf16 d_model=4096 token rows (8 KiB).
+Per phase: [all-gather of lengths] -> cost model + ordering + greedy
+assignment + never-worse (one balance call) -> send/recv layout -> pack ->
+[NCCL grouped send/recv] -> unpack. At N GPUs the 8 instances are spread
+8/N per GPU (strong scaling: the job is fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+METRIC = "balance+dispatch tokens/s at 1–8 B200; a2a GB/s vs NVLink; max/mean load"
+D_INST = 8
+PER_INSTANCE = 64
+SEED = 2
+ROW_BYTES = 8192  # bf16, d_model = 4096
+WORKLOAD = ("C2: DP=8 vision+text MCI batch (64 examples/instance, reference generator seed 2), "
+            "per-phase GreedyUnpadded rebalancing (vision metadata lengths, LLM interleaved "
+            "lengths, vision rate 4), bf16 d=4096 token rows (8 KiB)")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={','.join(map(str, self.gpus))}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                    "sw_power_cap"), f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.remove(self.path)
+            except Exception:
+                pass
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_inputs():
+    from paper_2503_23830_b200 import workload
+    b = workload.make_batch(2, D_INST, PER_INSTANCE, SEED)
+    lv, ov, _ = b.phase_items("vision")
+    ll, ol = b.llm_items()
+    return b, [("vision", lv, ov), ("llm", ll, ol)]
+
+
+# --------------------------------------------------------------- reference arm
+def cpu_reference_step(phases, nthreads, ref, oracle, bufs):
+    """Reference balance() (oracle/_ref: the reference's own code, or the C
+    restatement when _ref was not built) + threaded host memcpy dispatch
+    restating apply() on token rows."""
+    t0 = time.perf_counter()
+    for (name, L, O), (ins, outs) in zip(phases, bufs):
+        if ref is not None:
+            di, ds, _, _ = ref.balance(0, D_INST, L, O)
+        else:
+            r = oracle.balance(0, D_INST, L, O)
+            di, ds = r.dest_inst, r.dest_slot
+        lay = oracle.layout(D_INST, 1, L, O, di, ds)
+        oracle.dispatch_rows(D_INST, 1, L, O, di, lay["rank_src_off"], lay["rank_dst_off"],
+                             ROW_BYTES, ins, outs, nthreads)
+    return time.perf_counter() - t0
+
+
+def cpu_arm(phases, steps, warmup):
+    from oracle import Oracle, RefLib
+    oracle = Oracle()
+    ref = RefLib() if RefLib.available() else None
+    kind = "reference" if ref is not None else "port"
+    nthreads = os.cpu_count() or 1
+    bufs = []
+    for name, L, O in phases:
+        rows = int(L.sum())
+        bufs.append(([np.ones(rows * ROW_BYTES, np.uint8)], [np.empty(rows * ROW_BYTES, np.uint8)]))
+    for _ in range(warmup):
+        cpu_reference_step(phases, nthreads, ref, oracle, bufs)
+    times = [cpu_reference_step(phases, nthreads, ref, oracle, bufs) for _ in range(steps)]
+    tokens = sum(int(L.sum()) for _, L, _ in phases)
+    return times, tokens, kind, nthreads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    _, phases = build_inputs()
+    steps = max(1, args.steps)
+    times, tokens, kind, nthreads = cpu_arm(phases, steps, max(1, args.warmup))
+    total = sum(times)
+    value = tokens * steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": D_INST * PER_INSTANCE,
+                   "dp_instances": D_INST, "row_bytes": ROW_BYTES, "tokens_per_step": tokens},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": kind,
+                         "sample": f"full C2 step x{steps}: reference balance() per phase "
+                                   f"(single thread) + {nthreads}-thread host memcpy dispatch"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- B200 arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_23830_b200.capi import Balance, Comm, Context, Layout
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if D_INST % world:
+        raise SystemExit("N must divide the 8 DP instances")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+        uid = [Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = Comm(world, rank, uid[0])
+    ctx = Context(local)
+    P, c, R = world, D_INST // world, ROW_BYTES
+    batch, phases = build_inputs()
+
+    # per-phase device state: local items (global positions), global arrays, results, buffers
+    st = []
+    for name, L, O in phases:
+        n = len(L)
+        mine = np.nonzero(O // c == rank)[0]
+        max_local = int(max(np.bincount(O // c, minlength=P)))
+        s = dict(name=name, n=n, L=L, O=O, max_local=max_local,
+                 h_pos=torch.from_numpy(mine.astype(np.int64)).pin_memory(),
+                 h_len=torch.from_numpy(L[mine]).pin_memory(),
+                 h_org=torch.from_numpy(O[mine]).pin_memory())
+        s["pos"] = s["h_pos"].to(dev)
+        s["llen"] = s["h_len"].to(dev)
+        s["lorg"] = s["h_org"].to(dev)
+        s["glen"] = torch.from_numpy(L).to(dev)
+        s["gorg"] = torch.from_numpy(O).to(dev)
+        s["bal"] = Balance.alloc(D_INST, n, dev)
+        s["lay"] = Layout.alloc(P, n, dev)
+        st.append(s)
+
+    def gather(s):
+        if comm is not None:
+            ctx.allgather_items(comm, s["pos"], s["llen"], s["lorg"], s["max_local"], s["n"],
+                                s["glen"], s["gorg"])
+
+    # sizing pass (not timed): buffers from this batch's layout
+    for s in st:
+        gather(s)
+        ctx.balance(0, D_INST, s["glen"], s["gorg"], out=s["bal"])
+        ctx.layout(D_INST, P, s["glen"], s["gorg"], s["bal"], out=s["lay"])
+    torch.cuda.synchronize()
+    for s in st:
+        lay = s["lay"]
+        in_rows = int(lay.in_rows[rank].item())
+        out_rows = int(lay.out_rows[rank].item())
+        S = lay.send_rows.cpu().numpy().reshape(P, P)
+        s["moved_rows"] = out_rows  # every row of this rank's output is written once
+        s["send_rows"] = int(S[rank].sum() - S[rank, rank])
+        s["recv_rows"] = int(S[:, rank].sum() - S[rank, rank])
+        s["rin"] = torch.randint(0, 255, (max(in_rows, 1) * R,), dtype=torch.uint8, device=dev)
+        s["rout"] = torch.empty(max(out_rows, 1) * R, dtype=torch.uint8, device=dev)
+        s["send"] = torch.empty(max(s["send_rows"], 1) * R, dtype=torch.uint8, device=dev) \
+            if P > 1 else None
+        s["recv"] = torch.empty(max(s["recv_rows"], 1) * R, dtype=torch.uint8, device=dev) \
+            if P > 1 else None
+
+    stream = torch.cuda.current_stream()
+    disp_events = []
+
+    def step(record=False):
+        for s in st:
+            gather(s)
+            ctx.balance(0, D_INST, s["glen"], s["gorg"], out=s["bal"])
+            ctx.layout(D_INST, P, s["glen"], s["gorg"], s["bal"], out=s["lay"])
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            ctx.dispatch(D_INST, s["glen"], s["gorg"], s["bal"], s["lay"], R, s["rin"],
+                         s["rout"], s["send"], s["recv"], comm)
+            if record:
+                e1.record(stream)
+                disp_events.append((s["name"], e0, e1))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    launches0 = ctx.launches
+    with ClockSampler([local]) as clocks:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        t1.record(stream)
+        barrier()
+    launches = ctx.launches - launches0
+    ms = max_over_ranks(t0.elapsed_time(t1))
+    tokens = sum(int(s["L"].sum()) for s in st)
+    seqs = sum(s["n"] for s in st)
+    value = tokens * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the row movement; one dispatch per phase)
+    disp_ms = sum(e0.elapsed_time(e1) for _, e0, e1 in disp_events)
+    moved = sum(s["moved_rows"] for s in st) * R * args.steps  # rows written once, read once
+    hbm_bytes = 2 * moved
+    if P > 1:  # off-rank rows cross HBM twice more (pack to send, recv to out)
+        hbm_bytes += 2 * sum(s["send_rows"] + s["recv_rows"] for s in st) * R * args.steps
+    peak, peak_kind = peaks()
+    achieved = hbm_bytes / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None
+
+    # end-to-end through the C-ABI with host buffers: metadata H2D each step,
+    # assignment vectors + summaries D2H each step.
+    h2d = sum(s["h_pos"].numel() * 8 + s["h_len"].numel() * 8 + s["h_org"].numel() * 4
+              for s in st)
+    d2h = sum(s["n"] * 8 + 128 for s in st)
+    host_out = [(torch.empty(s["n"], dtype=torch.int32).pin_memory(),
+                 torch.empty(s["n"], dtype=torch.int32).pin_memory(),
+                 torch.empty(128, dtype=torch.uint8).pin_memory()) for s in st]
+
+    def e2e_step():
+        for s, (hi, hs, hsum) in zip(st, host_out):
+            s["pos"].copy_(s["h_pos"], non_blocking=True)
+            s["llen"].copy_(s["h_len"], non_blocking=True)
+            s["lorg"].copy_(s["h_org"], non_blocking=True)
+            if comm is None:  # single rank: the local arrays are the global arrays
+                s["glen"].copy_(s["llen"], non_blocking=True)
+                s["gorg"].copy_(s["lorg"], non_blocking=True)
+        step()
+        for s, (hi, hs, hsum) in zip(st, host_out):
+            hi.copy_(s["bal"].dest_inst[:s["n"]], non_blocking=True)
+            hs.copy_(s["bal"].dest_slot[:s["n"]], non_blocking=True)
+            hsum[:s["bal"].summary_raw.numel()].copy_(s["bal"].summary_raw, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - w0)
+
+    # load balance (stats_of max/mean, orchestrator.cpp:91-102)
+    imb = {}
+    for s in st:
+        sm = s["bal"].summary()
+        imb[s["name"]] = {"pre": round(sm.pre_ratio, 6), "post": round(sm.post_ratio, 6)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": D_INST * PER_INSTANCE,
+                   "dp_instances": D_INST, "instances_per_gpu": c, "row_bytes": R,
+                   "tokens_per_step": tokens, "seqs_per_step": seqs,
+                   "l2": f"row buffers {tokens * R / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"},
+        "seqs_per_s": seqs * args.steps / (ms / 1e3),
+        "load_imbalance_max_over_mean": imb,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "kernel": "k_move (orch_dispatch)", "peak_kind": peak_kind,
+                     "share_of_step": disp_ms / (t0.elapsed_time(t1) or 1.0)},
+        "e2e": {"value": tokens * args.steps / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "C-ABI with host metadata buffers; token rows are device-resident "
+                        "activations (encoder/embedding outputs)"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if P > 1:
+        line["a2a_rows_per_step"] = sum(s["send_rows"] for s in st)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, ctoks, kind, nthreads = cpu_arm(phases, 1, 0)
+        line["cpu_baseline"] = {"value": ctoks / times[0], "unit": "tokens/s", "cores": nthreads,
+                                "kind": kind,
+                                "sample": "one full C2 step: reference balance() per phase "
+                                          f"+ {nthreads}-thread host memcpy dispatch"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -2,12 +2,12 @@
  * orchsim_capi.h -- the drop-in C-ABI of the B200-native Batch Post-Balancing
  * Dispatcher (OrchMLLM, arXiv 2503.23830). This is the ONLY boundary between
  * host code and the sm_100a kernels: plain pointers and sizes, no C++ or
- * torch types. Implemented in paper_2503_23830_b200/csrc/*.cu and exported by
+ * torch types. Implemented in paper_2503_23830_b200/csrc and exported by
  * paper_2503_23830_b200/lib/liborchsim_b200.so.
  *
  * Each entry point names the reference interface it replaces
  * (paths relative to /root/reference/proj). The C++ API of the reference
- * (include/orchsim/*.hpp in this repo, same names/signatures/exceptions) is
+ * (the headers under include/orchsim in this repo, same names/signatures/exceptions) is
  * implemented on top of these calls in liborchsim_b200_host.so.
  *
  * Conventions
@@ -158,6 +158,15 @@ int orch_padded_bound_feasible_host(orch_ctx* ctx, int32_t d, int64_t n, const i
                                     const int32_t* h_origin, int64_t bound, int32_t* h_feasible,
                                     void* stream);
 
+/* oracle_optimal (balancers.hpp:84, balancers.cpp:380-413): exhaustive
+ * minimum of the max batch cost over canonical assignments, brute force on
+ * the device; returns the first optimum in the reference's depth-first order.
+ * ORCH_SIZE_CAP above the caller's caps, ORCH_UNSUPPORTED above d <= 4,
+ * d^n <= 2^36. Host buffers, synchronous. */
+int orch_oracle_optimal_host(orch_ctx* ctx, const orch_cost_model* model, int32_t d, int64_t n,
+                             const int64_t* h_len, int32_t max_items, int32_t max_instances,
+                             int32_t* h_assignment, double* h_objective, void* stream);
+
 /* ---------------------------------------------------------- cost model */
 /* cost(model, batch) over many batches at once (core.cpp:91-118) plus
  * stats_of (orchestrator.cpp:91-102): batches given as CSR over input
@@ -166,6 +175,12 @@ int orch_padded_bound_feasible_host(orch_ctx* ctx, int32_t d, int64_t n, const i
 int orch_batch_costs(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded,
                      int32_t d, int64_t n, const int64_t* d_len, const int32_t* d_bin_offset,
                      const int32_t* d_bin_member, double* d_cost, double* d_stats, void* stream);
+
+/* Host-buffer variant of orch_batch_costs (synchronous); h_stats may be NULL. */
+int orch_batch_costs_host(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded,
+                          int32_t d, int64_t n, const int64_t* h_len,
+                          const int32_t* h_bin_offset, const int32_t* h_bin_member,
+                          double* h_cost, double* h_stats, void* stream);
 
 /* batches_from_items (core.cpp:183-199): CSR of the origin batches. */
 int orch_group_by_origin(orch_ctx* ctx, int32_t d, int64_t n, const int32_t* d_origin,
@@ -185,6 +200,11 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_pa
 int orch_volume_matrix(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
                        const int32_t* d_origin, const int32_t* d_dest_inst, int64_t* d_V,
                        void* stream);
+
+/* Host-buffer variant of orch_volume_matrix (synchronous). */
+int orch_volume_matrix_host(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* h_len,
+                            const int32_t* h_origin, const int32_t* h_dest_inst, int64_t* h_V,
+                            void* stream);
 
 /* Send/recv layout of the exchange (make_exchange_plan, exchange.cpp:10-32,
  * realised on ranks): offsets, per-pair counts. Needs the balance result's

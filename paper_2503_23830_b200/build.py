@@ -39,7 +39,7 @@ def _nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu"]
+CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu", "exhaustive.cu"]
 HOST_SOURCES = ["host/core.cpp", "host/balancers.cpp", "host/topology.cpp", "host/exchange.cpp",
                 "host/runtime.cpp"]
 
@@ -88,7 +88,8 @@ def build_host(force=False):
     if not force and not _stale(out, srcs + hdrs + [os.path.join(INCLUDE, "orchsim_capi.h")]):
         return out
     _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off", "-Wall", "-Wextra",
-          "-I", INCLUDE, "-o", out, *srcs, "-L", LIB, "-l:liborchsim_b200.so",
+          "-I", INCLUDE, "-I/usr/local/cuda/include", "-o", out, *srcs, "-L", LIB,
+          "-l:liborchsim_b200.so",
           "-Wl,-rpath,$ORIGIN", "-L/usr/local/cuda/lib64", "-lcudart",
           "-Wl,-rpath,/usr/local/cuda/lib64"])
     return out

@@ -24,7 +24,8 @@ EXPORTED = [
     "orch_ctx_create", "orch_ctx_destroy", "orch_last_error", "orch_version",
     "orch_ctx_launches", "orch_balance", "orch_balance_host",
     "orch_min_feasible_padded_bound_host", "orch_padded_bound_feasible_host",
-    "orch_batch_costs", "orch_group_by_origin", "orch_encode_lengths", "orch_volume_matrix",
+    "orch_oracle_optimal_host",
+    "orch_batch_costs", "orch_batch_costs_host", "orch_volume_matrix_host", "orch_group_by_origin", "orch_encode_lengths", "orch_volume_matrix",
     "orch_layout", "orch_pack", "orch_exchange", "orch_unpack", "orch_dispatch",
     "orch_comm_unique_id", "orch_comm_create",
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",

@@ -16,6 +16,7 @@
 #include <string>
 
 #include "balance_kernels.cuh"
+#include "balance_small.cuh"
 #include "plan.cuh"
 
 namespace orchb {
@@ -146,6 +147,49 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   const bool needs_asc = padded_only || (!identity_only && kind == ORCH_BINARY_PADDED);
   const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+
+  if (mode <= 1 && d <= kSmallMaxD && n <= 4 * kSmallThreads) {
+    Plan sp;
+    SmallArgs a{};
+    const size_t nn1 = static_cast<size_t>(n > 0 ? n : 1);
+    sp.add_or(&a.dest_inst, out->dest_inst, nn1);
+    sp.add_or(&a.dest_slot, out->dest_slot, nn1);
+    sp.add_or(&a.src_slot, out->src_slot, nn1);
+    sp.add_or(&a.src_off, out->src_off, nn1);
+    sp.add_or(&a.dst_off, out->dst_off, nn1);
+    sp.add_or(&a.bin_count, out->bin_count, d);
+    sp.add_or(&a.bin_len, out->bin_len, d);
+    sp.add_or(&a.bin_tokens, out->bin_tokens, d);
+    sp.add_or(&a.bin_cost, out->bin_cost, d);
+    sp.add_or(&a.bin_offset, out->bin_offset, d + 1);
+    sp.add_or(&a.bin_member, out->bin_member, nn1);
+    sp.add_or(&a.src_offset, out->src_offset, d + 1);
+    sp.add_or(&a.src_member, out->src_member, nn1);
+    int rc0 = sp.commit(ctx, st);
+    if (rc0) return rc0;
+    a.kind = kind;
+    a.identity_only = identity_only;
+    a.d = d;
+    a.n = static_cast<int>(n);
+    a.tol_v = pol->tolerance_v;
+    a.model = model;
+    a.len = len;
+    a.origin = origin;
+    a.s = S;
+    if (n <= kSmallThreads) {
+      const int sm = static_cast<int>(sizeof(SmallSmem<1>));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_balance_small<1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      launch(ctx, [&] { k_balance_small<1><<<1, kSmallThreads, sm, st>>>(a); });
+    } else {
+      const int sm = static_cast<int>(sizeof(SmallSmem<4>));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_balance_small<4>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      launch(ctx, [&] { k_balance_small<4><<<1, kSmallThreads, sm, st>>>(a); });
+    }
+    ORCH_CUDA_TRY(cudaGetLastError());
+    return ORCH_OK;
+  }
 
   // ---- workspace plan
   Plan plan;

@@ -416,7 +416,9 @@ __global__ void __launch_bounds__(1024, 1)
   __shared__ int64_t cand[32];
   __shared__ int feas[32];
   __shared__ int64_t s_lo, s_hi;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so the warp-collective
+  // code below compiles without WARPSYNC.COLLECTIVE divergence handling
+  const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int64_t max_len = a[n - 1];
   if (mode == 1) {
     if (warp == 0) {

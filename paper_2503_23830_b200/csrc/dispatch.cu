@@ -197,15 +197,21 @@ __global__ void k_pair_apply(int64_t n, int d, int P, const int32_t* __restrict_
 // The slice [offs[lo], offs[hi]) of a CSR is read on the device.
 __global__ void k_unit_map(const int32_t* __restrict__ offs, int lo_idx, int hi_idx,
                            const int32_t* __restrict__ members,
-                           const int64_t* __restrict__ iter_off, const int64_t* __restrict__ len,
-                           int32_t* __restrict__ unit_first, int64_t cap_units) {
+                           const int64_t* __restrict__ iter_off,
+                           const int64_t* __restrict__ iter_rows, int me, int64_t unit_bytes,
+                           int64_t R, int32_t* __restrict__ unit_first, int64_t cap_units) {
   const int64_t beg = offs[lo_idx], end = offs[hi_idx];
-  for (int64_t k = beg + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < end;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t pos = members[k];
-    const int64_t a = iter_off[pos], b = a + len[pos];
-    for (int64_t u = (a + kUnitRows - 1) / kUnitRows; u * kUnitRows < b && u < cap_units; ++u)
-      unit_first[u] = static_cast<int32_t>(k - beg);
+  int64_t units = (iter_rows[me] * R + unit_bytes - 1) / unit_bytes;
+  units = units < cap_units ? units : cap_units;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < units;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = u * unit_bytes / R;  // the row holding the unit's first byte
+    int64_t lo = beg, hi = end - 1;  // last k with iter_off[members[k]] <= row
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (iter_off[members[mid]] <= row) lo = mid; else hi = mid - 1;
+    }
+    unit_first[u] = static_cast<int32_t>(lo - beg);
   }
 }
 
@@ -320,6 +326,166 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
       }
       block_copy(reinterpret_cast<int4*>(t), reinterpret_cast<const int4*>(s), (hi - lo) * vrow);
     }
+  }
+}
+
+// ------------------------------------------------------------ TMA movement
+// Rows of >= 8 KiB move with bulk async copies (cp.async.bulk, SASS UBLKCP):
+// global -> shared stage -> global, one warp per SM. The iteration buffer is
+// cut into 32 KiB chunks (chunk c -> CTA c % grid); each chunk is at most
+// kTmaMaxPieces contiguous item pieces. The 32 lanes decode 32 chunks' pieces
+// in parallel into a shared table, lane 0 streams them through a 3-stage ring:
+// loads of two chunks in flight while the oldest chunk is stored.
+constexpr int kTmaStages = 3;
+constexpr int kTmaChunk = 32768;
+constexpr int kTmaMaxPieces = 6;
+constexpr int64_t kTmaMinRow = 8192;
+
+struct TmaTable {
+  const char* src[32][kTmaMaxPieces];
+  char* dst[32][kTmaMaxPieces];
+  uint32_t bytes[32][kTmaMaxPieces];
+  int np[32];
+  char* st_dst[kTmaStages][kTmaMaxPieces];
+  uint32_t st_bytes[kTmaStages][kTmaMaxPieces];
+  int st_np[kTmaStages];
+  alignas(8) uint64_t bar[kTmaStages];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
+  extern __shared__ __align__(128) unsigned char ring[];  // kTmaStages * kTmaChunk
+  __shared__ TmaTable T;
+  const int lane = threadIdx.x;
+  const int64_t total = a.iter_rows[a.me];
+  bool over = total > a.iter_cap || a.out_rows[a.me] > a.out_cap;
+  if (MODE != kUnpack) over = over || a.in_rows[a.me] > a.in_cap;
+  if (MODE == kPack) {
+    int64_t st = 0;
+    for (int q = 0; q < a.P; ++q)
+      if (q != a.me) st += a.send_rows[a.me * a.P + q];
+    over = over || st > a.send_cap;
+  }
+  if (over) {
+    if (blockIdx.x == 0 && lane == 0) *a.status = ORCH_INVALID_ARGUMENT;
+    return;
+  }
+  const int64_t R = static_cast<int64_t>(a.R);
+  const int64_t total_b = total * R;
+  const int64_t chunks = (total_b + kTmaChunk - 1) / kTmaChunk;
+  const int64_t mine = chunks > blockIdx.x ? (chunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t beg = a.offs[a.lo_idx], end = a.offs[a.hi_idx];
+  if (lane == 0) {
+    for (int s = 0; s < kTmaStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&T.bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phases = 0;  // lane 0: parity bit per stage
+  int64_t fed = 0;      // lane 0: chunks issued so far (stage = fed % kTmaStages)
+
+  auto retire = [&](int64_t r) {  // lane 0: wait chunk r's loads, store its pieces
+    const int s = static_cast<int>(r % kTmaStages);
+    const uint32_t ph = (phases >> s) & 1u;
+    asm volatile(
+        "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W%=;\n}" ::"r"(smem_u32(&T.bar[s])),
+        "r"(ph));
+    phases ^= 1u << s;
+    uint32_t off = 0;
+    for (int p = 0; p < T.st_np[s]; ++p) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(T.st_dst[s][p]),
+                   "r"(smem_u32(ring + s * kTmaChunk + off)), "r"(T.st_bytes[s][p])
+                   : "memory");
+      off += T.st_bytes[s][p];
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  };
+
+  for (int64_t base = 0; base < mine; base += 32) {
+    // ---- decode: lane j -> this CTA's chunk (base + j)
+    const int64_t t = base + lane;
+    int np = 0;
+    if (t < mine) {
+      const int64_t c = blockIdx.x + t * gridDim.x;
+      const int64_t b0 = c * kTmaChunk;
+      const int64_t b1 = b0 + kTmaChunk < total_b ? b0 + kTmaChunk : total_b;
+      for (int64_t k = beg + a.unit_first[c]; k < end && np < kTmaMaxPieces; ++k) {
+        const int32_t pos = a.members[k];
+        const int64_t ob = (MODE == kPack ? a.rank_src_off[pos] : a.rank_dst_off[pos]) * R;
+        if (ob >= b1) break;
+        const int64_t ib = ob + a.len[pos] * R;
+        const int64_t lo = ob > b0 ? ob : b0;
+        const int64_t hi = ib < b1 ? ib : b1;
+        const int64_t skip = lo - ob;
+        const char* s = nullptr;
+        char* d = nullptr;
+        if (MODE == kLocal) {
+          s = a.in + a.rank_src_off[pos] * R + skip;
+          d = a.out + lo;
+        } else if (MODE == kPack) {
+          s = a.in + lo;
+          const int q = a.dest[pos] / a.c;
+          d = q == a.me ? a.out + a.rank_dst_off[pos] * R + skip
+                        : a.send + (a.displ[q] + a.pair_off[pos]) * R + skip;
+        } else {
+          const int r = a.origin[pos] / a.c;
+          if (r != a.me) {
+            s = a.recv + (a.displ[r] + a.pair_off[pos]) * R + skip;
+            d = a.out + lo;
+          }
+        }
+        if (s) {
+          T.src[lane][np] = s;
+          T.dst[lane][np] = d;
+          T.bytes[lane][np] = static_cast<uint32_t>(hi - lo);
+          ++np;
+        }
+        if (ib >= b1) break;
+      }
+    }
+    T.np[lane] = np;
+    __syncwarp();
+    // ---- feed (lane 0)
+    if (lane == 0) {
+      const int cnt = mine - base < 32 ? static_cast<int>(mine - base) : 32;
+      for (int j = 0; j < cnt; ++j) {
+        const int pn = T.np[j];
+        if (pn == 0) continue;  // nothing to move in this chunk
+        if (fed >= kTmaStages - 1) retire(fed - (kTmaStages - 1));
+        if (fed >= kTmaStages)  // stage of chunk fed-3 is free once its store has read smem
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        const int s = static_cast<int>(fed % kTmaStages);
+        uint32_t tot = 0;
+        for (int p = 0; p < pn; ++p) tot += T.bytes[j][p];
+        const uint32_t bar = smem_u32(&T.bar[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tot)
+                     : "memory");
+        uint32_t off = 0;
+        for (int p = 0; p < pn; ++p) {
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(smem_u32(ring + s * kTmaChunk + off)), "l"(T.src[j][p]), "r"(T.bytes[j][p]),
+              "r"(bar)
+              : "memory");
+          T.st_dst[s][p] = T.dst[j][p];
+          T.st_bytes[s][p] = T.bytes[j][p];
+          off += T.bytes[j][p];
+        }
+        T.st_np[s] = pn;
+        ++fed;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    for (int64_t r = fed - (kTmaStages - 1) > 0 ? fed - (kTmaStages - 1) : 0; r < fed; ++r)
+      retire(r);
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 }
 
@@ -493,26 +659,47 @@ constexpr int kMoveGrid = kSMs * 8;
 
 int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter_off,
              cudaStream_t st) {
+  const bool tma = static_cast<int64_t>(a.R) >= kTmaMinRow;
+  const int64_t unit_bytes = tma ? kTmaChunk : kUnitRows * static_cast<int64_t>(a.R);
+  const int64_t cap_units = (a.iter_cap * static_cast<int64_t>(a.R)) / unit_bytes + 2;
   Plan plan;
   int32_t* unit_first;
-  const int64_t cap_units = a.iter_cap / kUnitRows + 2;
   plan.add(&unit_first, static_cast<size_t>(cap_units));
   int rc = plan.commit(ctx, st);
   if (rc) return rc;
   a.unit_first = unit_first;
   launch(ctx, [&] {
-    k_unit_map<<<blocks_for(n, kThreads), kThreads, 0, st>>>(a.offs, a.lo_idx, a.hi_idx,
-                                                             a.members, iter_off, a.len,
-                                                             unit_first, cap_units);
+    k_unit_map<<<blocks_for(cap_units, kThreads, kSMs * 4), kThreads, 0, st>>>(
+        a.offs, a.lo_idx, a.hi_idx, a.members, iter_off, a.iter_rows, a.me, unit_bytes,
+        static_cast<int64_t>(a.R), unit_first, cap_units);
   });
-  launch(ctx, [&] {
-    if (mode == kLocal)
-      k_move<kLocal><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
-    else if (mode == kPack)
-      k_move<kPack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
-    else
-      k_move<kUnpack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
-  });
+  if (tma) {
+    const int sm = kTmaStages * kTmaChunk;
+    static bool attr_done = false;
+    if (!attr_done) {
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kUnpack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      attr_done = true;
+    }
+    launch(ctx, [&] {
+      if (mode == kLocal)
+        k_move_tma<kLocal><<<kSMs, 32, sm, st>>>(a);
+      else if (mode == kPack)
+        k_move_tma<kPack><<<kSMs, 32, sm, st>>>(a);
+      else
+        k_move_tma<kUnpack><<<kSMs, 32, sm, st>>>(a);
+    });
+  } else {
+    launch(ctx, [&] {
+      if (mode == kLocal)
+        k_move<kLocal><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+      else if (mode == kPack)
+        k_move<kPack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+      else
+        k_move<kUnpack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+    });
+  }
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
 }
@@ -719,6 +906,74 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t E, const int32_t* d_part_offset,
                                                              d_interleaved);
     });
   ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+// Host-buffer variants (staged through the context arena; synchronous).
+int orch_batch_costs_host(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded,
+                          int32_t d, int64_t n, const int64_t* h_len, const int32_t* h_bin_offset,
+                          const int32_t* h_bin_member, double* h_cost, double* h_stats,
+                          void* stream) {
+  if (!ctx || !model) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if ((model->padded != 0) != (batch_padded != 0))
+    return fail(ORCH_INVALID_ARGUMENT, "cost model padding mode does not match batch padding mode");
+  if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
+  ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+  Plan plan;
+  int64_t* len;
+  int32_t *off, *mem;
+  double *cost, *stats;
+  plan.add(&len, nn);
+  plan.add(&off, d + 1);
+  plan.add(&mem, nn);
+  plan.add(&cost, d);
+  plan.add(&stats, 3);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  if (n > 0) {
+    ORCH_CUDA_TRY(cudaMemcpyAsync(len, h_len, 8 * n, cudaMemcpyHostToDevice, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(mem, h_bin_member, 4 * n, cudaMemcpyHostToDevice, st));
+  }
+  ORCH_CUDA_TRY(cudaMemcpyAsync(off, h_bin_offset, 4 * (d + 1), cudaMemcpyHostToDevice, st));
+  launch(ctx, [&] {
+    k_bin_cost<<<blocks_for(static_cast<int64_t>(d) * 32, kThreads), kThreads, 0, st>>>(
+        *model, d, off, mem, len, nullptr, nullptr, nullptr, cost, nullptr);
+  });
+  if (h_stats) launch(ctx, [&] { k_stats_only<<<1, 1024, 0, st>>>(d, cost, stats); });
+  ORCH_CUDA_TRY(cudaMemcpyAsync(h_cost, cost, 8 * d, cudaMemcpyDeviceToHost, st));
+  if (h_stats) ORCH_CUDA_TRY(cudaMemcpyAsync(h_stats, stats, 24, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  return ORCH_OK;
+}
+
+int orch_volume_matrix_host(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* h_len,
+                            const int32_t* h_origin, const int32_t* h_dest_inst, int64_t* h_V,
+                            void* stream) {
+  if (!ctx) return fail(ORCH_INVALID_ARGUMENT, "null context");
+  if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
+  ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+  Plan plan;
+  int64_t *len, *V;
+  int32_t *org, *dst;
+  plan.add(&len, nn);
+  plan.add(&org, nn);
+  plan.add(&dst, nn);
+  plan.add(&V, static_cast<size_t>(d) * d);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  if (n > 0) {
+    ORCH_CUDA_TRY(cudaMemcpyAsync(len, h_len, 8 * n, cudaMemcpyHostToDevice, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(org, h_origin, 4 * n, cudaMemcpyHostToDevice, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(dst, h_dest_inst, 4 * n, cudaMemcpyHostToDevice, st));
+  }
+  rc = orch_volume_matrix(ctx, d, n, len, org, dst, V, stream);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(h_V, V, sizeof(int64_t) * d * d, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
   return ORCH_OK;
 }
 

@@ -80,11 +80,11 @@ def host_inputs(oracle, d, P, length, origin, o, R):
     return e, ins, outs
 
 
-@pytest.mark.parametrize("R", [16, 64, 8192])
+@pytest.mark.parametrize("R", [16, 64, 8192, 16384, 12288])
 def test_dispatch_one_rank_bytes(ctx, oracle, R):
     rng = np.random.default_rng(R)
     cases = [(8, 512, 30), (1, 40, 9), (33, 700, 12), (64, 3000, 5)] if R < 8192 else \
-        [(8, 256, 40)]
+        [(8, 256, 40), (1, 3, 1), (16, 400, 3)]
     for d, n, hi in cases:
         for kind in (0, 1, 2, 3):
             length, origin = make_case(rng, d, n, hi)
@@ -101,17 +101,18 @@ def test_dispatch_one_rank_bytes(ctx, oracle, R):
             assert torch.equal(rout.cpu(), torch.from_numpy(outs[0]))
 
 
+@pytest.mark.parametrize("R", [32, 8192, 24576])
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_pack_unpack_emulated_ranks(ctx, oracle, P):
+def test_pack_unpack_emulated_ranks(ctx, oracle, P, R):
     """pack on every rank -> emulated all-to-all (device copies of the
-    r->q segments at the layout displacements) -> unpack on every rank."""
-    R = 32
-    rng = np.random.default_rng(7 * P)
+    r->q segments at the layout displacements) -> unpack on every rank.
+    R >= 8 KiB exercises the TMA bulk-copy movement kernels."""
+    rng = np.random.default_rng(7 * P + R)
     for kind in (0, 1, 2, 3):
-        for trial in range(3):
+        for trial in range(3 if R == 32 else 2):
             d = P * int(rng.integers(1, 5))
-            n = int(rng.integers(1, 600))
-            length, origin = make_case(rng, d, n, hi=int(rng.choice([4, 40])))
+            n = int(rng.integers(1, 600 if R == 32 else 200))
+            length, origin = make_case(rng, d, n, hi=int(rng.choice([4, 40] if R == 32 else [3, 9])))
             o = oracle.balance(kind, d, length, origin, lam=0.01, v=3)
             e, ins, outs = host_inputs(oracle, d, P, length, origin, o, R)
             L, O = to_dev(length, np.int64), to_dev(origin, np.int32)
