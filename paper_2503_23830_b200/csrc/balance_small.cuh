@@ -19,6 +19,13 @@
 namespace orchb {
 namespace {
 
+#ifdef ORCH_SMALL_PROFILE
+__device__ long long g_small_prof[16];
+#define SMALL_MARK(i) do { __syncthreads(); if (threadIdx.x == 0) g_small_prof[i] = clock64(); } while (0)
+#else
+#define SMALL_MARK(i) do { } while (0)
+#endif
+
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallMaxD = 32;
 
@@ -167,6 +174,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   const int n = a.n, d = a.d;
   orch_summary* sum = a.s;
 
+  SMALL_MARK(0);
   // ---- S1: load, validate (index_sources, balancers.cpp:25-37)
   if (tid == 0) {
     S.bad = INT_MAX;
@@ -214,6 +222,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     return;
   }
 
+  SMALL_MARK(1);
   // ---- S2: identity grouping: stable sort by origin
   const int obits = 32 - __clz(d);  // covers the padding key d
   {
@@ -263,6 +272,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   }
   if (tid <= d) a.src_offset[tid] = S.off_id[tid];
 
+  SMALL_MARK(2);
   // ---- S3..S5: the policy's own packing
   if (!a.identity_only) {
     const bool asc = a.kind == ORCH_BINARY_PADDED;
@@ -291,6 +301,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       }
     }
     __syncthreads();
+    SMALL_MARK(3);
     if (a.kind == ORCH_GREEDY_UNPADDED) {
       if (warp == 0) warp_greedy<true>(S, d, 0, n, nullptr, nullptr, a.dst_off, &S.rounds);
     } else if (a.kind == ORCH_QUADRATIC_TOLERANCE) {
@@ -471,6 +482,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       if (tid < d) S.cnt_a[tid] = tid < G ? static_cast<int32_t>(S.starts[tid + 1] - S.starts[tid]) : 0;
     }
     __syncthreads();
+    SMALL_MARK(4);
     // ---- algorithm CSR (balancers.cpp:43-60 assemble: slot = position in bin)
     if (warp == 0) {
       const int c = lane < d ? S.cnt_a[lane] : 0;
@@ -494,6 +506,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     __syncthreads();  // bin_member (global) visible to the block
   }
 
+  SMALL_MARK(5);
   // ---- S6: batch costs (core.cpp:91-118): warp w -> algorithm batch w, identity batch w
   for (int task = warp; task < 2 * d; task += 32) {
     const int side = task < d ? 0 : 1;  // 0 algorithm, 1 identity
@@ -541,6 +554,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     }
   }
   __syncthreads();
+  SMALL_MARK(6);
   // ---- never_worse (balancers.cpp:71-76) + stats_of (orchestrator.cpp:91-102)
   if (tid == 0) {
     double stat[2][3];
@@ -596,6 +610,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     }
     if (tid <= d) a.bin_offset[tid] = S.off_id[tid];
   }
+  SMALL_MARK(7);
 }
 
 }  // namespace
