@@ -301,6 +301,14 @@ def run_b200(args):
         hbm_bytes += 2 * sum(s["send_rows"] + s["recv_rows"] for s in st) * R * args.steps
     peak, peak_kind = peaks()
     achieved = hbm_bytes / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None
+    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)["per_launch"]
+        traffic = sum(x["dram_read_plus_write"] for x in tj) / len(tj)
+        traffic_alg = sum(x["algorithmic_bytes"] for x in tj) / len(tj)
+    except Exception:
+        traffic_alg = None
 
     # end-to-end through the C-ABI with host buffers: metadata H2D each step,
     # assignment vectors + summaries D2H each step.
@@ -353,7 +361,8 @@ def run_b200(args):
         "seqs_per_s": seqs * args.steps / (ms / 1e3),
         "load_imbalance_max_over_mean": imb,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "traffic_algorithmic_per_launch": traffic_alg,
                      "kernel": "k_move (orch_dispatch)", "peak_kind": peak_kind,
                      "share_of_step": disp_ms / (t0.elapsed_time(t1) or 1.0)},
         "e2e": {"value": tokens * args.steps / e2e_s, "unit": "tokens/s",
@@ -366,11 +375,12 @@ def run_b200(args):
     if P > 1:
         line["a2a_rows_per_step"] = sum(s["send_rows"] for s in st)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, ctoks, kind, nthreads = cpu_arm(phases, 1, 0)
+        times, ctoks, kind, nthreads = cpu_arm(phases, 1, 1)
         line["cpu_baseline"] = {"value": ctoks / times[0], "unit": "tokens/s", "cores": nthreads,
                                 "kind": kind,
-                                "sample": "one full C2 step: reference balance() per phase "
-                                          f"+ {nthreads}-thread host memcpy dispatch"}
+                                "sample": "one full C2 step after one warm-up step: reference "
+                                          f"balance() per phase + {nthreads}-thread host "
+                                          "memcpy dispatch"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
