@@ -178,7 +178,7 @@ def run_reference(args):
 def run_b200(args):
     import torch
     import torch.distributed as dist
-    from paper_2503_23830_b200.capi import Balance, Comm, Context, Layout
+    from paper_2503_23830_b200.capi import Balance, Comm, Context, Layout, Window
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -238,7 +238,13 @@ def run_b200(args):
         s["send_rows"] = int(S[rank].sum() - S[rank, rank])
         s["recv_rows"] = int(S[:, rank].sum() - S[rank, rank])
         s["rin"] = torch.randint(0, 255, (max(in_rows, 1) * R,), dtype=torch.uint8, device=dev)
-        s["rout"] = torch.empty(max(out_rows, 1) * R, dtype=torch.uint8, device=dev)
+        s["win"] = None
+        if P > 1 and args.exchange == "put":
+            wrows = int(lay.out_rows.max().item())
+            s["win"] = Window(ctx, comm, max(wrows, 1) * R)
+            s["rout"] = s["win"].tensor_view(dev)
+        else:
+            s["rout"] = torch.empty(max(out_rows, 1) * R, dtype=torch.uint8, device=dev)
         s["send"] = torch.empty(max(s["send_rows"], 1) * R, dtype=torch.uint8, device=dev) \
             if P > 1 else None
         s["recv"] = torch.empty(max(s["recv_rows"], 1) * R, dtype=torch.uint8, device=dev) \
@@ -256,8 +262,12 @@ def run_b200(args):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-            ctx.dispatch(D_INST, s["glen"], s["gorg"], s["bal"], s["lay"], R, s["rin"],
-                         s["rout"], s["send"], s["recv"], comm)
+            if s["win"] is not None:
+                ctx.dispatch_put(D_INST, s["glen"], s["gorg"], s["bal"], s["lay"], R, s["rin"],
+                                 s["win"], comm)
+            else:
+                ctx.dispatch(D_INST, s["glen"], s["gorg"], s["bal"], s["lay"], R, s["rin"],
+                             s["rout"], s["send"], s["recv"], comm)
             if record:
                 e1.record(stream)
                 disp_events.append((s["name"], e0, e1))
@@ -297,7 +307,7 @@ def run_b200(args):
     disp_ms = sum(e0.elapsed_time(e1) for _, e0, e1 in disp_events)
     moved = sum(s["moved_rows"] for s in st) * R * args.steps  # rows written once, read once
     hbm_bytes = 2 * moved
-    if P > 1:  # off-rank rows cross HBM twice more (pack to send, recv to out)
+    if P > 1 and args.exchange == "nccl":  # staging: pack to send, recv to out
         hbm_bytes += 2 * sum(s["send_rows"] + s["recv_rows"] for s in st) * R * args.steps
     peak, peak_kind = peaks()
     achieved = hbm_bytes / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None
@@ -373,7 +383,12 @@ def run_b200(args):
         "clocks": clocks.summary(),
     }
     if P > 1:
-        line["a2a_rows_per_step"] = sum(s["send_rows"] for s in st)
+        a2a_bytes = sum(s["send_rows"] for s in st) * R
+        line["exchange"] = args.exchange
+        line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes,
+                       "busbw_gbs_rank": a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9,
+                       "nvlink_peak_gbs": 900.0, "nvlink_measured_gbs": 770.0,
+                       "note": "off-rank bytes of this rank / device time of its dispatch calls"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         times, ctoks, kind, nthreads = cpu_arm(phases, 1, 1)
         line["cpu_baseline"] = {"value": ctoks / times[0], "unit": "tokens/s", "cores": nthreads,
@@ -383,6 +398,10 @@ def run_b200(args):
                                           "memcpy dispatch"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    for s in st:
+        if s.get("win") is not None:
+            s["rout"] = None
+            s["win"].close()
     if comm is not None:
         comm.close()
         dist.destroy_process_group()
@@ -396,6 +415,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="put", choices=["put", "nccl"],
+                    help="N>1: fused pack+put over NVLink (default) or NCCL send/recv")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -254,6 +254,28 @@ void orch_comm_destroy(orch_comm* comm);
 int32_t orch_comm_rank(const orch_comm* comm);
 int32_t orch_comm_size(const orch_comm* comm);
 
+/* Barrier over the communicator on a stream (a 1-int ncclAllReduce). */
+int orch_barrier(orch_comm* comm, void* stream);
+
+/* A row buffer every rank can store into over NVLink (cudaMalloc + CUDA IPC
+ * handles exchanged over the communicator). Collective: every rank calls it
+ * with the same size. */
+typedef struct orch_window orch_window;
+int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out);
+void* orch_window_ptr(const orch_window* w);
+size_t orch_window_bytes(const orch_window* w);
+int orch_window_destroy(orch_window* w); /* collective */
+
+/* Fused pack + put exchange: every item's rows are
+ * read once from this rank's d_in and stored directly at their final
+ * destination-slot offset in the destination rank's window (TMA bulk stores
+ * over NVLink to peer memory); a communicator barrier on the stream then
+ * publishes the windows. Same result bytes as orch_dispatch. */
+int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                      const int32_t* d_origin, const orch_balance_out* bal,
+                      const orch_layout_out* layout, size_t row_bytes, const void* d_in,
+                      int64_t in_cap, orch_window* out_win, void* stream);
+
 /* gather_lengths (exchange.cpp:34-47) realised as ncclAllGather: every rank
  * contributes its local items (global input position, length, origin) and
  * receives the global arrays scattered into input order. Local counts are

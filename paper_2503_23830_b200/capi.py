@@ -29,6 +29,8 @@ EXPORTED = [
     "orch_layout", "orch_pack", "orch_exchange", "orch_unpack", "orch_dispatch",
     "orch_comm_unique_id", "orch_comm_create",
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
+    "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
+    "orch_window_destroy", "orch_dispatch_put",
 ]
 
 
@@ -87,6 +89,8 @@ def lib():
         L.orch_ctx_launches.restype = C.c_int64
         L.orch_ctx_destroy.restype = None
         L.orch_comm_destroy.restype = None
+        L.orch_window_ptr.restype = C.c_void_p
+        L.orch_window_bytes.restype = C.c_size_t
         _lib = L
     return _lib
 
@@ -192,6 +196,35 @@ class Comm:
         if self.h:
             lib().orch_comm_destroy(self.h)
             self.h = C.c_void_p()
+
+
+class Window:
+    """orch_window: an IPC-shared row buffer of one rank (collective create)."""
+
+    def __init__(self, ctx: "Context", comm: Comm, nbytes: int):
+        self.h = C.c_void_p()
+        _check(lib().orch_window_create(ctx.h, comm.h, C.c_size_t(nbytes), C.byref(self.h)))
+        self.nbytes = nbytes
+        self.ptr = lib().orch_window_ptr(self.h)
+
+    def tensor_view(self, device):
+        """A uint8 torch view of this rank's window (no copy)."""
+        import torch
+        return _view_u8(self.ptr, self.nbytes, device)
+
+    def close(self):
+        if self.h:
+            _check(lib().orch_window_destroy(self.h))
+            self.h = C.c_void_p()
+
+
+def _view_u8(ptr, nbytes, device):
+    class _Holder:
+        pass
+    h = _Holder()
+    h.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                  "version": 3, "strides": None}
+    return torch.as_tensor(h, device=device)
 
 
 class Context:
@@ -354,6 +387,16 @@ class Context:
                                  C.c_int64(length.numel()), _ptr(length), _ptr(origin), C.byref(b),
                                  C.byref(lo), C.c_size_t(R), _ptr(recv), _ptr(rows_out),
                                  C.c_int64(self._rows(rows_out, R)), _stream(stream)))
+
+    def dispatch_put(self, d, length, origin, bal: Balance, lay: Layout, row_bytes, rows_in,
+                     window: "Window", comm: Comm, stream=None):
+        b, lo = bal.struct(), lay.struct()
+        R = row_bytes
+        _check(lib().orch_dispatch_put(self.h, comm.h, C.c_int32(d), C.c_int64(length.numel()),
+                                       _ptr(length), _ptr(origin), C.byref(b), C.byref(lo),
+                                       C.c_size_t(R), _ptr(rows_in),
+                                       C.c_int64(self._rows(rows_in, R)), window.h,
+                                       _stream(stream)))
 
     def allgather_items(self, comm: Comm, local_pos, local_len, local_origin, max_local, n,
                         out_len, out_origin, stream=None):

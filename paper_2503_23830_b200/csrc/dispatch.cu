@@ -20,6 +20,18 @@ struct orch_comm {
   int rank = 0;
   int size = 1;
   int device = 0;
+  int32_t* barrier_buf = nullptr;  // 1 int on the device (ncclAllReduce barrier)
+};
+
+// A row buffer every rank of the communicator can store into (CUDA IPC over
+// NVLink): the fused pack+put exchange writes rows straight into the
+// destination rank's output, one pass, no staging buffers.
+struct orch_window {
+  orch_comm* comm = nullptr;
+  char* base = nullptr;
+  size_t bytes = 0;
+  std::vector<char*> peers;       // host copy, peers[rank] == base
+  char** peers_dev = nullptr;     // device copy [P]
 };
 
 namespace orchb {
@@ -243,7 +255,7 @@ __device__ __forceinline__ void block_copy(int4* __restrict__ dst, const int4* _
   for (; v < nvec; v += kMoveThreads) st_stream(dst + v, ld_stream(src + v));
 }
 
-enum MoveMode { kLocal = 0, kPack = 1, kUnpack = 2 };
+enum MoveMode { kLocal = 0, kPack = 1, kUnpack = 2, kPut = 3 };
 
 struct MoveArgs {
   int me, P, c;
@@ -266,6 +278,7 @@ struct MoveArgs {
   const int64_t* pair_off;
   const int64_t* displ;  // send_displ row of me (pack) / recv_displ row of me (unpack)
   const int32_t* unit_first;
+  char* const* peer_out;  // kPut: output buffer of every rank (IPC-mapped), [P]
   int32_t* status;
   size_t R;
   const char* in;
@@ -283,6 +296,8 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
   const int64_t total = a.iter_rows[a.me];
   bool over = total > a.iter_cap || a.out_rows[a.me] > a.out_cap;
   if (MODE != kUnpack) over = over || a.in_rows[a.me] > a.in_cap;
+  if (MODE == kPut)  // every rank's window has the same capacity
+    for (int q = 0; q < a.P; ++q) over = over || a.out_rows[q] > a.out_cap;
   if (MODE == kPack) {
     int64_t st = 0;
     for (int q = 0; q < a.P; ++q)
@@ -302,7 +317,8 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
     const int64_t row1 = row0 + kUnitRows < total ? row0 + kUnitRows : total;
     for (int64_t k = beg + a.unit_first[u]; k < end; ++k) {
       const int32_t pos = a.members[k];
-      const int64_t off = MODE == kPack ? a.rank_src_off[pos] : a.rank_dst_off[pos];
+      const int64_t off =
+          (MODE == kPack || MODE == kPut) ? a.rank_src_off[pos] : a.rank_dst_off[pos];
       if (off >= row1) break;
       const int64_t l = a.len[pos];
       const int64_t lo = off > row0 ? off : row0;
@@ -318,6 +334,9 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
         const int q = a.dest[pos] / a.c;
         t = q == a.me ? a.out + (a.rank_dst_off[pos] + skip) * R
                       : a.send + (a.displ[q] + a.pair_off[pos] + skip) * R;
+      } else if (MODE == kPut) {  // straight into the destination rank's output (NVLink)
+        s = a.in + lo * R;
+        t = a.peer_out[a.dest[pos] / a.c] + (a.rank_dst_off[pos] + skip) * R;
       } else {
         const int r = a.origin[pos] / a.c;
         if (r == a.me) continue;  // moved by the pack kernel
@@ -327,6 +346,7 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
       block_copy(reinterpret_cast<int4*>(t), reinterpret_cast<const int4*>(s), (hi - lo) * vrow);
     }
   }
+  if (MODE == kPut) __threadfence_system();
 }
 
 // ------------------------------------------------------------ TMA movement
@@ -364,6 +384,8 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
   const int64_t total = a.iter_rows[a.me];
   bool over = total > a.iter_cap || a.out_rows[a.me] > a.out_cap;
   if (MODE != kUnpack) over = over || a.in_rows[a.me] > a.in_cap;
+  if (MODE == kPut)  // every rank's window has the same capacity
+    for (int q = 0; q < a.P; ++q) over = over || a.out_rows[q] > a.out_cap;
   if (MODE == kPack) {
     int64_t st = 0;
     for (int q = 0; q < a.P; ++q)
@@ -416,7 +438,8 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
       const int64_t b1 = b0 + kTmaChunk < total_b ? b0 + kTmaChunk : total_b;
       for (int64_t k = beg + a.unit_first[c]; k < end && np < kTmaMaxPieces; ++k) {
         const int32_t pos = a.members[k];
-        const int64_t ob = (MODE == kPack ? a.rank_src_off[pos] : a.rank_dst_off[pos]) * R;
+        const int64_t ob =
+            ((MODE == kPack || MODE == kPut) ? a.rank_src_off[pos] : a.rank_dst_off[pos]) * R;
         if (ob >= b1) break;
         const int64_t ib = ob + a.len[pos] * R;
         const int64_t lo = ob > b0 ? ob : b0;
@@ -432,6 +455,9 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
           const int q = a.dest[pos] / a.c;
           d = q == a.me ? a.out + a.rank_dst_off[pos] * R + skip
                         : a.send + (a.displ[q] + a.pair_off[pos]) * R + skip;
+        } else if (MODE == kPut) {
+          s = a.in + lo;
+          d = a.peer_out[a.dest[pos] / a.c] + a.rank_dst_off[pos] * R + skip;
         } else {
           const int r = a.origin[pos] / a.c;
           if (r != a.me) {
@@ -486,6 +512,10 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
     for (int64_t r = fed - (kTmaStages - 1) > 0 ? fed - (kTmaStages - 1) : 0; r < fed; ++r)
       retire(r);
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (MODE == kPut) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence_system();
+    }
   }
 }
 
@@ -680,6 +710,7 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kUnpack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPut>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       attr_done = true;
     }
     launch(ctx, [&] {
@@ -687,6 +718,8 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
         k_move_tma<kLocal><<<kSMs, 32, sm, st>>>(a);
       else if (mode == kPack)
         k_move_tma<kPack><<<kSMs, 32, sm, st>>>(a);
+      else if (mode == kPut)
+        k_move_tma<kPut><<<kSMs, 32, sm, st>>>(a);
       else
         k_move_tma<kUnpack><<<kSMs, 32, sm, st>>>(a);
     });
@@ -696,6 +729,8 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
         k_move<kLocal><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
       else if (mode == kPack)
         k_move<kPack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+      else if (mode == kPut)
+        k_move<kPut><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
       else
         k_move<kUnpack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
     });
@@ -1001,6 +1036,12 @@ int orch_comm_create(int32_t nranks, int32_t rank, const unsigned char* h_id128,
   }
   c->rank = rank;
   c->size = nranks;
+  if (cudaMalloc(&c->barrier_buf, sizeof(int32_t)) != cudaSuccess) {
+    ncclCommDestroy(c->comm);
+    delete c;
+    return fail(ORCH_CUDA_ERROR, "barrier buffer allocation failed");
+  }
+  cudaMemset(c->barrier_buf, 0, sizeof(int32_t));
   *out = c;
   return ORCH_OK;
 }
@@ -1008,6 +1049,7 @@ int orch_comm_create(int32_t nranks, int32_t rank, const unsigned char* h_id128,
 void orch_comm_destroy(orch_comm* comm) {
   if (!comm) return;
   if (comm->comm) ncclCommDestroy(comm->comm);
+  if (comm->barrier_buf) cudaFree(comm->barrier_buf);
   delete comm;
 }
 
@@ -1045,6 +1087,99 @@ int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_
   }
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
+}
+
+
+// ------------------------------------------------------------ windows / put
+int orch_barrier(orch_comm* comm, void* stream) {
+  if (!comm) return fail(ORCH_INVALID_ARGUMENT, "null communicator");
+  ORCH_NCCL_TRY(ncclAllReduce(comm->barrier_buf, comm->barrier_buf, 1, ncclInt32, ncclSum,
+                              comm->comm, static_cast<cudaStream_t>(stream)));
+  return ORCH_OK;
+}
+
+int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out) {
+  if (!ctx || !comm || !out || bytes == 0) return fail(ORCH_INVALID_ARGUMENT, "bad window arguments");
+  const int P = comm->size;
+  auto* w = new orch_window();
+  w->comm = comm;
+  w->bytes = bytes;
+  w->peers.assign(P, nullptr);
+  cudaError_t e = cudaMalloc(&w->base, bytes);
+  if (e != cudaSuccess) {
+    delete w;
+    return fail(ORCH_CUDA_ERROR, std::string("window allocation: ") + cudaGetErrorString(e));
+  }
+  cudaIpcMemHandle_t mine;
+  ORCH_CUDA_TRY(cudaIpcGetMemHandle(&mine, w->base));
+  char* dev = nullptr;
+  ORCH_CUDA_TRY(cudaMalloc(&dev, sizeof(cudaIpcMemHandle_t) * (P + 1)));
+  ORCH_CUDA_TRY(cudaMemcpy(dev, &mine, sizeof mine, cudaMemcpyHostToDevice));
+  ORCH_NCCL_TRY(ncclAllGather(dev, dev + sizeof(cudaIpcMemHandle_t), sizeof(cudaIpcMemHandle_t),
+                              ncclChar, comm->comm, 0));
+  std::vector<cudaIpcMemHandle_t> all(P);
+  ORCH_CUDA_TRY(cudaMemcpy(all.data(), dev + sizeof(cudaIpcMemHandle_t),
+                           sizeof(cudaIpcMemHandle_t) * P, cudaMemcpyDeviceToHost));
+  cudaFree(dev);
+  for (int q = 0; q < P; ++q) {
+    if (q == comm->rank) {
+      w->peers[q] = w->base;
+      continue;
+    }
+    void* p = nullptr;
+    e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(ORCH_CUDA_ERROR, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    w->peers[q] = static_cast<char*>(p);
+  }
+  ORCH_CUDA_TRY(cudaMalloc(&w->peers_dev, sizeof(char*) * P));
+  ORCH_CUDA_TRY(cudaMemcpy(w->peers_dev, w->peers.data(), sizeof(char*) * P,
+                           cudaMemcpyHostToDevice));
+  *out = w;
+  return ORCH_OK;
+}
+
+void* orch_window_ptr(const orch_window* w) { return w ? w->base : nullptr; }
+size_t orch_window_bytes(const orch_window* w) { return w ? w->bytes : 0; }
+
+int orch_window_destroy(orch_window* w) {
+  if (!w) return ORCH_OK;
+  // every rank must be done writing into / reading from the windows
+  int rc = orch_barrier(w->comm, nullptr);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < static_cast<int>(w->peers.size()); ++q)
+    if (q != w->comm->rank && w->peers[q]) cudaIpcCloseMemHandle(w->peers[q]);
+  cudaFree(w->peers_dev);
+  cudaFree(w->base);
+  delete w;
+  return rc;
+}
+
+int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                      const int32_t* d_origin, const orch_balance_out* bal,
+                      const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap,
+                      orch_window* out_win, void* stream) {
+  if (!comm || !out_win) return fail(ORCH_INVALID_ARGUMENT, "put needs a communicator and a window");
+  const int P = comm->size, me = comm->rank;
+  int rc = check_move_args(ctx, P, me, d, bal, L, R);
+  if (rc) return rc;
+  if (!aligned16(d_in)) return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
+  if (n > 0) {
+    MoveArgs a = make_args(P, me, d, d_len, d_origin, bal, L, R);
+    a.offs = bal->src_offset;
+    a.members = bal->src_member;
+    a.iter_rows = L->in_rows;
+    a.iter_cap = in_cap;
+    a.in_cap = in_cap;
+    a.out_cap = static_cast<int64_t>(out_win->bytes / R);
+    a.in = static_cast<const char*>(d_in);
+    a.out = out_win->base;
+    a.peer_out = out_win->peers_dev;
+    rc = run_move(ctx, kPut, a, n, L->rank_src_off, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+  }
+  // rows from every peer have landed once every rank passed its put kernel
+  return orch_barrier(comm, stream);
 }
 
 }  // extern "C"

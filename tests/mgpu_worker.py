@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 from oracle import Oracle  # noqa: E402
-from paper_2503_23830_b200.capi import Comm, Context  # noqa: E402
+from paper_2503_23830_b200.capi import Comm, Context, Window  # noqa: E402
 
 
 def main():
@@ -76,6 +76,19 @@ def main():
                 torch.cuda.synchronize()
                 ok = ok and int(lay.status.item()) == 0
                 ok = ok and torch.equal(rout.cpu(), torch.from_numpy(outs[rank]))
+                # fused pack + put into IPC windows (one pass over NVLink)
+                wbytes = max(int(e["out_tokens"].max()), 1) * R
+                win = Window(ctx, comm, wbytes)
+                wv = win.tensor_view(torch.device("cuda", local))
+                wv.zero_()
+                torch.cuda.synchronize()
+                dist.barrier()
+                ctx.dispatch_put(d, gl, go, bal, lay, R, rin, win, comm)
+                torch.cuda.synchronize()
+                ok = ok and int(lay.status.item()) == 0
+                k = len(outs[rank])
+                ok = ok and torch.equal(wv[:k].cpu(), torch.from_numpy(outs[rank]))
+                win.close()
                 cases += 1
                 if not ok:
                     failures += 1
