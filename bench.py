@@ -189,17 +189,26 @@ def run_b200(args):
         raise SystemExit("N must divide the 8 DP instances")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    comm = None
+    comm_meta = comm_data = None
     if world > 1:
         dist.init_process_group("gloo", init_method="env://")
-        uid = [Comm.unique_id() if rank == 0 else None]
+        uid = [(Comm.unique_id(), Comm.unique_id()) if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        comm = Comm(world, rank, uid[0])
-    ctx = Context(local)
+        # two communicators: lengths all-gather (metadata stream) and row
+        # exchange (data stream) run concurrently, so they must not share one
+        comm_meta = Comm(world, rank, uid[0][0])
+        comm_data = Comm(world, rank, uid[0][1])
+    # one context (workspace arena) per stream
+    ctx_meta, ctx_data = Context(local), Context(local)
     P, c, R = world, D_INST // world, ROW_BYTES
     batch, phases = build_inputs()
+    meta_stream = torch.cuda.Stream(device=dev)
+    data_stream = torch.cuda.Stream(device=dev)
 
-    # per-phase device state: local items (global positions), global arrays, results, buffers
+    # Per phase: local items (global input positions), and two buffer sets of
+    # the metadata (global arrays, balance, layout) so step i+1's balance runs
+    # on the metadata stream while step i's rows move on the data stream (the
+    # paper overlaps the solver with the forward pass).
     st = []
     for name, L, O in phases:
         n = len(L)
@@ -208,29 +217,32 @@ def run_b200(args):
         s = dict(name=name, n=n, L=L, O=O, max_local=max_local,
                  h_pos=torch.from_numpy(mine.astype(np.int64)).pin_memory(),
                  h_len=torch.from_numpy(L[mine]).pin_memory(),
-                 h_org=torch.from_numpy(O[mine]).pin_memory())
+                 h_org=torch.from_numpy(O[mine]).pin_memory(),
+                 h_glen=torch.from_numpy(L).pin_memory(),
+                 h_gorg=torch.from_numpy(O).pin_memory())
         s["pos"] = s["h_pos"].to(dev)
         s["llen"] = s["h_len"].to(dev)
         s["lorg"] = s["h_org"].to(dev)
-        s["glen"] = torch.from_numpy(L).to(dev)
-        s["gorg"] = torch.from_numpy(O).to(dev)
-        s["bal"] = Balance.alloc(D_INST, n, dev)
-        s["lay"] = Layout.alloc(P, n, dev)
+        s["buf"] = [dict(glen=torch.from_numpy(L).to(dev), gorg=torch.from_numpy(O).to(dev),
+                         bal=Balance.alloc(D_INST, n, dev), lay=Layout.alloc(P, n, dev),
+                         meta_done=torch.cuda.Event(), data_done=torch.cuda.Event())
+                    for _ in range(2)]
         st.append(s)
 
-    def gather(s):
-        if comm is not None:
-            ctx.allgather_items(comm, s["pos"], s["llen"], s["lorg"], s["max_local"], s["n"],
-                                s["glen"], s["gorg"])
+    def meta(s, B, stream):
+        if comm_meta is not None:
+            ctx_meta.allgather_items(comm_meta, s["pos"], s["llen"], s["lorg"], s["max_local"],
+                                     s["n"], B["glen"], B["gorg"], stream=stream)
+        ctx_meta.balance(0, D_INST, B["glen"], B["gorg"], out=B["bal"], stream=stream)
+        ctx_meta.layout(D_INST, P, B["glen"], B["gorg"], B["bal"], out=B["lay"], stream=stream)
 
     # sizing pass (not timed): buffers from this batch's layout
     for s in st:
-        gather(s)
-        ctx.balance(0, D_INST, s["glen"], s["gorg"], out=s["bal"])
-        ctx.layout(D_INST, P, s["glen"], s["gorg"], s["bal"], out=s["lay"])
+        for B in s["buf"]:
+            meta(s, B, torch.cuda.current_stream())
     torch.cuda.synchronize()
     for s in st:
-        lay = s["lay"]
+        lay = s["buf"][0]["lay"]
         in_rows = int(lay.in_rows[rank].item())
         out_rows = int(lay.out_rows[rank].item())
         S = lay.send_rows.cpu().numpy().reshape(P, P)
@@ -241,7 +253,7 @@ def run_b200(args):
         s["win"] = None
         if P > 1 and args.exchange == "put":
             wrows = int(lay.out_rows.max().item())
-            s["win"] = Window(ctx, comm, max(wrows, 1) * R)
+            s["win"] = Window(ctx_data, comm_data, max(wrows, 1) * R)
             s["rout"] = s["win"].tensor_view(dev)
         else:
             s["rout"] = torch.empty(max(out_rows, 1) * R, dtype=torch.uint8, device=dev)
@@ -250,27 +262,42 @@ def run_b200(args):
         s["recv"] = torch.empty(max(s["recv_rows"], 1) * R, dtype=torch.uint8, device=dev) \
             if P > 1 else None
 
-    stream = torch.cuda.current_stream()
     disp_events = []
+    counter = [0]
 
-    def step(record=False):
+    def step(record=False, h2d=False):
+        b = counter[0] % 2
+        counter[0] += 1
         for s in st:
-            gather(s)
-            ctx.balance(0, D_INST, s["glen"], s["gorg"], out=s["bal"])
-            ctx.layout(D_INST, P, s["glen"], s["gorg"], s["bal"], out=s["lay"])
+            B = s["buf"][b]
+            meta_stream.wait_event(B["data_done"])  # rows of step i-2 moved: buffers free
+            with torch.cuda.stream(meta_stream):
+                if h2d:  # e2e: this step's metadata comes from pinned host memory
+                    if comm_meta is None:
+                        B["glen"].copy_(s["h_glen"], non_blocking=True)
+                        B["gorg"].copy_(s["h_gorg"], non_blocking=True)
+                    else:
+                        s["pos"].copy_(s["h_pos"], non_blocking=True)
+                        s["llen"].copy_(s["h_len"], non_blocking=True)
+                        s["lorg"].copy_(s["h_org"], non_blocking=True)
+            meta(s, B, meta_stream)
+            B["meta_done"].record(meta_stream)
+            data_stream.wait_event(B["meta_done"])
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+                e0.record(data_stream)
             if s["win"] is not None:
-                ctx.dispatch_put(D_INST, s["glen"], s["gorg"], s["bal"], s["lay"], R, s["rin"],
-                                 s["win"], comm)
+                ctx_data.dispatch_put(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R,
+                                      s["rin"], s["win"], comm_data, stream=data_stream)
             else:
-                ctx.dispatch(D_INST, s["glen"], s["gorg"], s["bal"], s["lay"], R, s["rin"],
-                             s["rout"], s["send"], s["recv"], comm)
+                ctx_data.dispatch(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
+                                  s["rout"], s["send"], s["recv"], comm_data, stream=data_stream)
             if record:
-                e1.record(stream)
+                e1.record(data_stream)
                 disp_events.append((s["name"], e0, e1))
+            B["data_done"].record(data_stream)
+        return b
 
     def barrier():
         torch.cuda.synchronize()
@@ -287,17 +314,18 @@ def run_b200(args):
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
-    launches0 = ctx.launches
+    launches0 = ctx_meta.launches + ctx_data.launches
     with ClockSampler([local]) as clocks:
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
+        t0.record(data_stream)
+        meta_stream.wait_event(t0)
         for _ in range(args.steps):
             step(record=True)
-        t1.record(stream)
+        t1.record(data_stream)
         barrier()
-    launches = ctx.launches - launches0
+    launches = ctx_meta.launches + ctx_data.launches - launches0
     ms = max_over_ranks(t0.elapsed_time(t1))
     tokens = sum(int(s["L"].sum()) for s in st)
     seqs = sum(s["n"] for s in st)
@@ -320,29 +348,29 @@ def run_b200(args):
     except Exception:
         traffic_alg = None
 
-    # end-to-end through the C-ABI with host buffers: metadata H2D each step,
-    # assignment vectors + summaries D2H each step.
-    h2d = sum(s["h_pos"].numel() * 8 + s["h_len"].numel() * 8 + s["h_org"].numel() * 4
-              for s in st)
+    # end-to-end through the C-ABI with host buffers: each step copies its
+    # metadata from pinned host memory and reads back its assignment vectors
+    # and summaries, and completes before the next one starts (no overlap).
+    if comm_meta is None:
+        h2d = sum(s["h_glen"].numel() * 8 + s["h_gorg"].numel() * 4 for s in st)
+    else:
+        h2d = sum(s["h_pos"].numel() * 8 + s["h_len"].numel() * 8 + s["h_org"].numel() * 4
+                  for s in st)
     d2h = sum(s["n"] * 8 + 128 for s in st)
     host_out = [(torch.empty(s["n"], dtype=torch.int32).pin_memory(),
                  torch.empty(s["n"], dtype=torch.int32).pin_memory(),
                  torch.empty(128, dtype=torch.uint8).pin_memory()) for s in st]
 
     def e2e_step():
-        for s, (hi, hs, hsum) in zip(st, host_out):
-            s["pos"].copy_(s["h_pos"], non_blocking=True)
-            s["llen"].copy_(s["h_len"], non_blocking=True)
-            s["lorg"].copy_(s["h_org"], non_blocking=True)
-            if comm is None:  # single rank: the local arrays are the global arrays
-                s["glen"].copy_(s["llen"], non_blocking=True)
-                s["gorg"].copy_(s["lorg"], non_blocking=True)
-        step()
-        for s, (hi, hs, hsum) in zip(st, host_out):
-            hi.copy_(s["bal"].dest_inst[:s["n"]], non_blocking=True)
-            hs.copy_(s["bal"].dest_slot[:s["n"]], non_blocking=True)
-            hsum[:s["bal"].summary_raw.numel()].copy_(s["bal"].summary_raw, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        b = step(h2d=True)
+        with torch.cuda.stream(meta_stream):
+            for s, (hi, hs, hsum) in zip(st, host_out):
+                bal = s["buf"][b]["bal"]
+                hi.copy_(bal.dest_inst[:s["n"]], non_blocking=True)
+                hs.copy_(bal.dest_slot[:s["n"]], non_blocking=True)
+                hsum[:bal.summary_raw.numel()].copy_(bal.summary_raw, non_blocking=True)
+        meta_stream.synchronize()
+        data_stream.synchronize()
 
     for _ in range(2):
         e2e_step()
@@ -356,7 +384,7 @@ def run_b200(args):
     # load balance (stats_of max/mean, orchestrator.cpp:91-102)
     imb = {}
     for s in st:
-        sm = s["bal"].summary()
+        sm = s["buf"][0]["bal"].summary()
         imb[s["name"]] = {"pre": round(sm.pre_ratio, 6), "post": round(sm.post_ratio, 6)}
 
     line = {
@@ -377,8 +405,9 @@ def run_b200(args):
                      "share_of_step": disp_ms / (t0.elapsed_time(t1) or 1.0)},
         "e2e": {"value": tokens * args.steps / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "note": "C-ABI with host metadata buffers; token rows are device-resident "
-                        "activations (encoder/embedding outputs)"},
+                "note": "C-ABI with host metadata buffers, one synchronous step at a time; "
+                        "token rows are device-resident activations (encoder/embedding "
+                        "outputs)"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
@@ -402,8 +431,9 @@ def run_b200(args):
         if s.get("win") is not None:
             s["rout"] = None
             s["win"].close()
-    if comm is not None:
-        comm.close()
+    if comm_meta is not None:
+        comm_meta.close()
+        comm_data.close()
         dist.destroy_process_group()
     return 0
 

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -211,7 +212,9 @@ __global__ void k_unit_map(const int32_t* __restrict__ offs, int lo_idx, int hi_
                            const int32_t* __restrict__ members,
                            const int64_t* __restrict__ iter_off,
                            const int64_t* __restrict__ iter_rows, int me, int64_t unit_bytes,
-                           int64_t R, int32_t* __restrict__ unit_first, int64_t cap_units) {
+                           int64_t R, int32_t* __restrict__ unit_first, int64_t cap_units,
+                           unsigned long long* __restrict__ chunk_counter) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && chunk_counter) *chunk_counter = 0;
   const int64_t beg = offs[lo_idx], end = offs[hi_idx];
   int64_t units = (iter_rows[me] * R + unit_bytes - 1) / unit_bytes;
   units = units < cap_units ? units : cap_units;
@@ -279,6 +282,7 @@ struct MoveArgs {
   const int64_t* displ;  // send_displ row of me (pack) / recv_displ row of me (unpack)
   const int32_t* unit_first;
   char* const* peer_out;  // kPut: output buffer of every rank (IPC-mapped), [P]
+  unsigned long long* chunk_counter;  // TMA path: next unclaimed chunk (zeroed by k_unit_map)
   int32_t* status;
   size_t R;
   const char* in;
@@ -399,7 +403,9 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
   const int64_t R = static_cast<int64_t>(a.R);
   const int64_t total_b = total * R;
   const int64_t chunks = (total_b + kTmaChunk - 1) / kTmaChunk;
-  const int64_t mine = chunks > blockIdx.x ? (chunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // dynamic scheduling: CTAs claim 32 consecutive chunks at a time, so a CTA
+  // sharing its SM with other work (the next step's balance) is no straggler
+  unsigned long long* claim = a.chunk_counter;
   const int64_t beg = a.offs[a.lo_idx], end = a.offs[a.hi_idx];
   if (lane == 0) {
     for (int s = 0; s < kTmaStages; ++s)
@@ -428,12 +434,15 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   };
 
-  for (int64_t base = 0; base < mine; base += 32) {
+  for (;;) {
+    int64_t base = 0;
+    if (lane == 0) base = static_cast<int64_t>(atomicAdd(claim, 32ull));
+    base = __shfl_sync(~0u, base, 0);
+    if (base >= chunks) break;
     // ---- decode: lane j -> this CTA's chunk (base + j)
-    const int64_t t = base + lane;
+    const int64_t c = base + lane;
     int np = 0;
-    if (t < mine) {
-      const int64_t c = blockIdx.x + t * gridDim.x;
+    if (c < chunks) {
       const int64_t b0 = c * kTmaChunk;
       const int64_t b1 = b0 + kTmaChunk < total_b ? b0 + kTmaChunk : total_b;
       for (int64_t k = beg + a.unit_first[c]; k < end && np < kTmaMaxPieces; ++k) {
@@ -478,7 +487,7 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
     __syncwarp();
     // ---- feed (lane 0)
     if (lane == 0) {
-      const int cnt = mine - base < 32 ? static_cast<int>(mine - base) : 32;
+      const int cnt = chunks - base < 32 ? static_cast<int>(chunks - base) : 32;
       for (int j = 0; j < cnt; ++j) {
         const int pn = T.np[j];
         if (pn == 0) continue;  // nothing to move in this chunk
@@ -694,17 +703,26 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
   const int64_t cap_units = (a.iter_cap * static_cast<int64_t>(a.R)) / unit_bytes + 2;
   Plan plan;
   int32_t* unit_first;
+  unsigned long long* counter;
   plan.add(&unit_first, static_cast<size_t>(cap_units));
+  plan.add(&counter, 1);
   int rc = plan.commit(ctx, st);
   if (rc) return rc;
   a.unit_first = unit_first;
+  a.chunk_counter = counter;
   launch(ctx, [&] {
     k_unit_map<<<blocks_for(cap_units, kThreads, kSMs * 4), kThreads, 0, st>>>(
         a.offs, a.lo_idx, a.hi_idx, a.members, iter_off, a.iter_rows, a.me, unit_bytes,
-        static_cast<int64_t>(a.R), unit_first, cap_units);
+        static_cast<int64_t>(a.R), unit_first, cap_units, counter);
   });
   if (tma) {
     const int sm = kTmaStages * kTmaChunk;
+    static const int ctas_per_sm = [] {
+      const char* e = getenv("ORCH_TMA_CTAS_PER_SM");
+      const int v = e ? atoi(e) : 1;
+      return v >= 1 && v <= 2 ? v : 1;
+    }();
+    const int tma_grid = kSMs * ctas_per_sm;
     static bool attr_done = false;
     if (!attr_done) {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -715,13 +733,13 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
     }
     launch(ctx, [&] {
       if (mode == kLocal)
-        k_move_tma<kLocal><<<kSMs, 32, sm, st>>>(a);
+        k_move_tma<kLocal><<<tma_grid, 32, sm, st>>>(a);
       else if (mode == kPack)
-        k_move_tma<kPack><<<kSMs, 32, sm, st>>>(a);
+        k_move_tma<kPack><<<tma_grid, 32, sm, st>>>(a);
       else if (mode == kPut)
-        k_move_tma<kPut><<<kSMs, 32, sm, st>>>(a);
+        k_move_tma<kPut><<<tma_grid, 32, sm, st>>>(a);
       else
-        k_move_tma<kUnpack><<<kSMs, 32, sm, st>>>(a);
+        k_move_tma<kUnpack><<<tma_grid, 32, sm, st>>>(a);
     });
   } else {
     launch(ctx, [&] {
