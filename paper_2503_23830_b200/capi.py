@@ -143,10 +143,14 @@ class Balance:
                        torch.empty(SUMMARY_BYTES, dtype=torch.uint8, device=device))
 
     def struct(self) -> BalanceOutS:
-        return BalanceOutS(*[_ptr(getattr(self, k)) for k in (
-            "dest_inst", "dest_slot", "src_slot", "src_off", "dst_off", "bin_count", "bin_len",
-            "bin_tokens", "bin_cost", "bin_offset", "bin_member", "src_offset", "src_member",
-            "summary_raw")])
+        st = self.__dict__.get("_struct")
+        if st is None:  # device pointers are fixed for the life of the tensors
+            st = BalanceOutS(*[_ptr(getattr(self, k)) for k in (
+                "dest_inst", "dest_slot", "src_slot", "src_off", "dst_off", "bin_count",
+                "bin_len", "bin_tokens", "bin_cost", "bin_offset", "bin_member", "src_offset",
+                "src_member", "summary_raw")])
+            self.__dict__["_struct"] = st
+        return st
 
     def summary(self) -> Summary:
         raw = self.summary_raw.cpu().numpy().tobytes()
@@ -174,9 +178,13 @@ class Layout:
                       torch.zeros(1, dtype=torch.int32, device=device))
 
     def struct(self) -> LayoutOutS:
-        return LayoutOutS(*[_ptr(getattr(self, k)) for k in (
-            "rank_src_off", "rank_dst_off", "pair_off", "send_rows", "send_displ", "recv_displ",
-            "in_rows", "out_rows", "status")])
+        st = self.__dict__.get("_struct")
+        if st is None:
+            st = LayoutOutS(*[_ptr(getattr(self, k)) for k in (
+                "rank_src_off", "rank_dst_off", "pair_off", "send_rows", "send_displ",
+                "recv_displ", "in_rows", "out_rows", "status")])
+            self.__dict__["_struct"] = st
+        return st
 
 
 class Comm:

@@ -68,6 +68,7 @@ orch_cost_model policy_model(const orch_policy& p) {  // balancers.cpp:162-176
 size_t greedy_rounds_smem(int d) {
   int p2 = 1;
   while (p2 < d) p2 <<= 1;
+  if (p2 < 32) p2 = 32;
   return 3 * sizeof(uint64_t) * p2 + sizeof(int32_t) * d;
 }
 
@@ -148,7 +149,7 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
 
-  if (mode <= 1 && d <= kSmallMaxD && n <= 4 * kSmallThreads) {
+  if (mode <= 1 && d <= kSmallMaxD && n <= kSmallMaxItems) {
     Plan sp;
     SmallArgs a{};
     const size_t nn1 = static_cast<size_t>(n > 0 ? n : 1);
@@ -176,17 +177,25 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
     a.len = len;
     a.origin = origin;
     a.s = S;
-    if (n <= kSmallThreads) {
-      const int sm = static_cast<int>(sizeof(SmallSmem<1>));
-      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_balance_small<1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      launch(ctx, [&] { k_balance_small<1><<<1, kSmallThreads, sm, st>>>(a); });
-    } else {
-      const int sm = static_cast<int>(sizeof(SmallSmem<4>));
-      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_balance_small<4>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      launch(ctx, [&] { k_balance_small<4><<<1, kSmallThreads, sm, st>>>(a); });
-    }
+    auto run_small = [&](auto kern, int sm) -> int {
+      static int configured[3] = {0, 0, 0};  // per instantiation, once per process
+      const int slot = sm == static_cast<int>(sizeof(SmallSmem<2>)) ? 0
+                       : sm == static_cast<int>(sizeof(SmallSmem<4>)) ? 1 : 2;
+      if (!configured[slot]) {
+        ORCH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        configured[slot] = 1;
+      }
+      launch(ctx, [&] { kern<<<1, kSmallThreads, sm, st>>>(a); });
+      return ORCH_OK;
+    };
+    int rc1;
+    if (n <= 2 * kSmallThreads)
+      rc1 = run_small(k_balance_small<2>, static_cast<int>(sizeof(SmallSmem<2>)));
+    else if (n <= 4 * kSmallThreads)
+      rc1 = run_small(k_balance_small<4>, static_cast<int>(sizeof(SmallSmem<4>)));
+    else
+      rc1 = run_small(k_balance_small<16>, static_cast<int>(sizeof(SmallSmem<16>)));
+    if (rc1) return rc1;
     ORCH_CUDA_TRY(cudaGetLastError());
     return ORCH_OK;
   }
@@ -318,9 +327,15 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
     ORCH_CUDA_TRY(cudaMemsetAsync(asc_len + n, 0, sizeof(int64_t), st));
     tb = cub_bytes;
     ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, asc_len, asc_prefix, (int)n + 1, st));
+    constexpr int kPadSmemItems = 200 * 1024 / 4;
+    const int pad_items = n <= kPadSmemItems ? static_cast<int>(n) : 0;
+    const int pad_smem = pad_items * 4;
+    if (pad_smem > 48 * 1024)
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_padded_search,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, pad_smem));
     launch(ctx, [&] {
-      k_padded_search<<<1, 1024, 0, st>>>(d, n, xs, mode == 3 ? 1 : 0, probe, starts, n_groups,
-                                          bound, S);
+      k_padded_search<<<1, 1024, pad_smem, st>>>(d, n, xs, mode == 3 ? 1 : 0, probe, starts,
+                                                 n_groups, bound, S, pad_items);
     });
     if (padded_only) {
       if (mode == 2 && d_bound_out)

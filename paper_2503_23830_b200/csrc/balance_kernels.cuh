@@ -149,6 +149,70 @@ __global__ void k_greedy_warp(int d, int64_t n, const int64_t* __restrict__ d_fi
   if (lane == 0) s->rounds = n - first;
 }
 
+// Block-wide ascending bitonic sort of p (power of two) 64-bit keys in shared
+// memory. Stages with stride >= 32 exchange through shared memory (one
+// barrier each); the strides 16..1 of every size run in registers with warp
+// shuffles, so a 4096-key sort takes 36 barriers instead of 78.
+template <int kThreads>
+__device__ void block_bitonic(uint64_t* U, int p) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = kThreads / 32;
+  auto reg_stages = [&](int size_lo, int size_hi) {  // sizes size_lo..size_hi, strides < 32
+    for (int blk = warp; blk * 32 < p; blk += kWarps) {
+      const int i = blk * 32 + lane;
+      uint64_t key = U[i];
+      for (int size = size_lo; size <= size_hi; size <<= 1)
+        for (int stride = (size > 32 ? 16 : size >> 1); stride > 0; stride >>= 1) {
+          const uint64_t other = __shfl_xor_sync(~0u, key, stride);
+          const bool up = (i & size) == 0;
+          const bool lower = (i & stride) == 0;
+          const uint64_t lo = other < key ? other : key;
+          const uint64_t hi = other < key ? key : other;
+          key = (lower == up) ? lo : hi;
+        }
+      U[i] = key;
+    }
+  };
+  if (p <= 1) return;
+  if (p < 32) {  // tiny: plain shared-memory network
+    for (int size = 2; size <= p; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < (p >> 1); i += kThreads) {
+          const int lo = 2 * stride * (i / stride) + (i % stride);
+          const int hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const uint64_t a = U[lo], b = U[hi];
+          if ((a > b) == up) {
+            U[lo] = b;
+            U[hi] = a;
+          }
+        }
+        __syncthreads();
+      }
+    return;
+  }
+  reg_stages(2, 32);
+  __syncthreads();
+  for (int size = 64; size <= p; size <<= 1) {
+    for (int stride = size >> 1; stride >= 32; stride >>= 1) {
+      for (int i = threadIdx.x; i < (p >> 1); i += kThreads) {
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = U[lo], b = U[hi];
+        if ((a > b) == up) {
+          U[lo] = b;
+          U[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+    reg_stages(size, size);
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- K4b
 // distribute_min_sum for any d <= ORCH_MAX_INSTANCES: exact round-batched
 // LPT. Bins are kept sorted by the packed key
@@ -169,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int p2 = 1;
   while (p2 < d) p2 <<= 1;
+  if (p2 < 32) p2 = 32;
   uint64_t* S = reinterpret_cast<uint64_t*>(smem_raw);  // [p2] sorted bins
   uint64_t* T = S + p2;                                  // [p2] merge output
   uint64_t* U = T + p2;                                  // [p2] updated keys
@@ -190,22 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
-  if (init_load) {  // pre-seeded bins: sort them once
-    for (int size = 2; size <= p2; size <<= 1)
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = tid; i < (p2 >> 1); i += kThreads) {
-          const int lo = 2 * stride * (i / stride) + (i % stride);
-          const int hi = lo + stride;
-          const bool up = (lo & size) == 0;
-          const uint64_t a = S[lo], b = S[hi];
-          if ((a > b) == up) {
-            S[lo] = b;
-            S[hi] = a;
-          }
-        }
-        __syncthreads();
-      }
-  }
+  if (init_load) block_bitonic<kThreads>(S, p2);  // pre-seeded bins: sort them once
 
   int64_t next = d_first ? *d_first : 0;
   int64_t rounds = 0;
@@ -238,21 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
-    // bitonic sort of the k updated keys
-    for (int size = 2; size <= pk; size <<= 1)
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = tid; i < (pk >> 1); i += kThreads) {
-          const int lo = 2 * stride * (i / stride) + (i % stride);
-          const int hi = lo + stride;
-          const bool up = (lo & size) == 0;
-          const uint64_t a = U[lo], b = U[hi];
-          if ((a > b) == up) {
-            U[lo] = b;
-            U[hi] = a;
-          }
-        }
-        __syncthreads();
-      }
+    block_bitonic<kThreads>(U, pk);
     // merge U[0,k) with S[k,d) into T (keys are unique: distinct bin index)
     const int rest = d - k;
     for (int i = tid; i < d; i += kThreads) {
@@ -278,10 +314,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       T[pos] = key;
     }
     __syncthreads();
-    for (int i = tid; i < d; i += kThreads) S[i] = T[i];
+    uint64_t* tmp = S;  // T becomes the sorted bins (S[d..p2) and T[d..p2) stay MAX)
+    S = T;
+    T = tmp;
     next += k;
     ++rounds;
-    __syncthreads();
   }
   for (int i = tid; i < d; i += kThreads) {
     const uint64_t key = S[i];
@@ -409,13 +446,22 @@ __device__ __forceinline__ bool warp_feasible(const uint32_t* __restrict__ a, in
 // [max, max * (n/d + 1)] (feasibility is monotone in b), then the
 // group starts at that bound. mode 0: search; mode 1: feasibility of `bound`.
 __global__ void __launch_bounds__(1024, 1)
-    k_padded_search(int d, int64_t n, const uint32_t* __restrict__ a, int mode, int64_t probe,
+    k_padded_search(int d, int64_t n, const uint32_t* __restrict__ a_global, int mode, int64_t probe,
                     int64_t* __restrict__ starts, int32_t* __restrict__ n_groups,
-                    int64_t* __restrict__ out_bound, orch_summary* s) {
+                    int64_t* __restrict__ out_bound, orch_summary* s, int smem_items) {
   if (pipeline_failed(s)) return;
   __shared__ int64_t cand[32];
   __shared__ int feas[32];
   __shared__ int64_t s_lo, s_hi;
+  extern __shared__ __align__(16) uint32_t a_smem[];
+  // The galloping group scans probe a[] ~d times per candidate: keep the
+  // ascending lengths in shared memory when they fit (L2 latency -> ~30 cycles).
+  const uint32_t* a = a_global;
+  if (n <= smem_items) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a_smem[i] = a_global[i];
+    __syncthreads();
+    a = a_smem;
+  }
   // warp index through a shuffle: provably warp-uniform, so the warp-collective
   // code below compiles without WARPSYNC.COLLECTIVE divergence handling
   const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -535,11 +581,27 @@ __global__ void k_conv_seed(int d, int64_t n, const uint32_t* __restrict__ xs,
     seed_load[i] = 0;
     seed_count[i] = 0;
   }
+  // items stream through a shared-memory window so the sequential group scan
+  // never waits on L2 latency
+  constexpr int kWin = 2048;
+  __shared__ uint32_t wx[kWin];
+  __shared__ int32_t wpos[kWin];
+  int64_t wbase = 0, wend = 0;
   int g = 0;
   int64_t size = 0, load = 0, k = 0;
   while (k < n) {
+    if (k + 32 > wend && wend < n) {  // refill from k
+      __syncwarp();
+      wbase = k;
+      wend = k + kWin < n ? k + kWin : n;
+      for (int64_t j = lane; j < wend - wbase; j += 32) {
+        wx[j] = xs[wbase + j];
+        wpos[j] = order[wbase + j];
+      }
+      __syncwarp();
+    }
     const int64_t t = k + lane;
-    const int64_t x = t < n ? static_cast<int64_t>(xs[t]) : 0;
+    const int64_t x = t < n ? static_cast<int64_t>(wx[t - wbase]) : 0;
     const bool c = t < n && (size + lane + 1) * x > bound;
     const bool valid = t < n;
     const unsigned mv = __ballot_sync(~0u, valid);
@@ -552,7 +614,7 @@ __global__ void k_conv_seed(int d, int64_t n, const uint32_t* __restrict__ xs,
       if (lane >= off) incl += o;
     }
     if (lane < take) {
-      const int32_t pos = order[t];
+      const int32_t pos = wpos[t - wbase];
       dest_inst[pos] = g;
       dest_slot[pos] = static_cast<int32_t>(size + lane);
       dst_off[pos] = load + incl - x;

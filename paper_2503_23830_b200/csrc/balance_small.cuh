@@ -4,11 +4,16 @@
 // the policy's packing, costs, never_worse, all outputs -- with every array in
 // shared memory. Same outputs, bit for bit, as the multi-kernel path.
 //
-// The greedy (distribute_min_sum, balancers.cpp:92-107) runs on one warp as
-// exact round-batched LPT: lane r holds the bin of rank r (packed key
-// load << 5 | bin); per round the first k items go to ranks 0..k-1 where k is
-// the first r with load_(r) - load_(0) >= x_r, then a register bitonic sort
-// restores the order (proof in DESIGN.md).
+// Latency is the whole game here (one SM, sequential policies), so:
+//  * identity grouping ranks items with __match_any_sync per 32-item chunk
+//    instead of a radix sort;
+//  * the greedy (distribute_min_sum, balancers.cpp:92-107) runs on one warp
+//    as exact round-batched LPT with the bins held in lanes: per round every
+//    lane ranks its packed key (load << 5 | bin) against the others (d
+//    independent shuffles), k = #lanes whose rank r satisfies
+//    load_(r) - load_(0) < x_r (a prefix of ranks), and those k
+//    lanes take items next..next+k-1 -- no re-sort between rounds;
+//  * the quadratic-tolerance champion scan keeps (sum, square sum) in lanes.
 #pragma once
 
 #include <cub/block/block_radix_sort.cuh>
@@ -26,8 +31,10 @@ __device__ long long g_small_prof[16];
 #define SMALL_MARK(i) do { } while (0)
 #endif
 
-constexpr int kSmallThreads = 1024;
+constexpr int kSmallThreads = 256;
+constexpr int kSmallWarps = kSmallThreads / 32;
 constexpr int kSmallMaxD = 32;
+constexpr int kSmallMaxItems = 4096;
 
 struct SmallArgs {
   int kind;
@@ -58,6 +65,7 @@ struct SmallArgs {
 template <int ITEMS>
 struct SmallSmem {
   static constexpr int NS = kSmallThreads * ITEMS;
+  static constexpr int NCH = NS / 32;  // 32-item chunks of the identity ranking
   using Sort = cub::BlockRadixSort<uint32_t, kSmallThreads, ITEMS, int32_t>;
   using Scan = cub::BlockScan<int64_t, kSmallThreads>;
   int64_t len[NS];
@@ -67,6 +75,9 @@ struct SmallSmem {
   int32_t ord[NS];
   uint32_t xs[NS];
   uint16_t a_slot[NS];
+  uint16_t id_rank[NS];                   // rank inside its chunk among same-origin items
+  uint16_t chunk_base[NCH][kSmallMaxD];   // same-origin items in earlier chunks
+  uint8_t chunk_cnt[NCH][kSmallMaxD];
   uint8_t a_dest[NS];
   union {
     typename Sort::TempStorage sort;
@@ -76,77 +87,80 @@ struct SmallSmem {
   int32_t cnt_a[kSmallMaxD + 1], off_a[kSmallMaxD + 1];
   int64_t tok_a[kSmallMaxD], seed_load[kSmallMaxD];
   int32_t seed_cnt[kSmallMaxD];
-  int64_t qsum[kSmallMaxD], qsq[kSmallMaxD];
   // per-batch results: [0] algorithm, [1] identity
   int32_t b_cnt[2][kSmallMaxD];
   int64_t b_len[2][kSmallMaxD], b_tok[2][kSmallMaxD];
   double b_cost[2][kSmallMaxD];
   int64_t starts[kSmallMaxD + 2];
-  int64_t cand[32];
-  int feas[32];
+  int64_t cand[kSmallWarps];
+  int feas[kSmallWarps];
   unsigned long long maxlen, total;
-  int bad, unsup, k, groups, used_identity;
-  int64_t lo, hi, bound, consumed, rounds;
+  int bad, unsup, groups, used_identity;
+  int64_t lo, hi, bound, rounds;
 };
 
-__device__ __forceinline__ uint64_t warp_bitonic(uint64_t key, int width) {
+// Warp 0: round-batched LPT over xs[first, n) (descending). Lane b < d holds
+// bin b: load (optionally pre-seeded) and item count. kWrite: record each
+// item's bin / slot / token offset.
+template <bool kWrite, int W, int ITEMS>
+__device__ void warp_greedy_w(SmallSmem<ITEMS>& S, int d, int first, int n,
+                              const int64_t* init_load, const int32_t* init_cnt, int64_t* dst_off,
+                              int64_t* rounds_out) {
   const int lane = threadIdx.x & 31;
-  for (int size = 2; size <= width; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const uint64_t other = __shfl_xor_sync(~0u, key, stride);
-      const bool up = (lane & size) == 0;
-      const bool lower = (lane & stride) == 0;
-      const uint64_t lo = other < key ? other : key;
-      const uint64_t hi = other < key ? key : other;
-      key = (lower == up) ? lo : hi;
-    }
-  return key;
-}
-
-// Warp 0: round-batched LPT over xs[first, n) (descending), bins optionally
-// pre-seeded. kWrite: record each item's bin / slot / token offset.
-template <bool kWrite, int ITEMS>
-__device__ void warp_greedy(SmallSmem<ITEMS>& S, int d, int first, int n, const int64_t* init_load,
-                            const int32_t* init_cnt, int64_t* dst_off, int64_t* rounds_out) {
-  const int lane = threadIdx.x & 31;
-  int width = 1;
-  while (width < d) width <<= 1;
-  uint64_t key = kU64Max;
+  int64_t L = 0;
+  int32_t cnt = 0;
   if (lane < d) {
-    key = (static_cast<uint64_t>(init_load ? init_load[lane] : 0) << 5) | lane;
-    S.cnt_a[lane] = init_cnt ? init_cnt[lane] : 0;
+    L = init_load ? init_load[lane] : 0;
+    cnt = init_cnt ? init_cnt[lane] : 0;
   }
-  __syncwarp();
-  if (init_load) key = warp_bitonic(key, width);
   int next = first;
   int64_t rounds = 0;
   while (next < n) {
     const int m = n - next < d ? n - next : d;
-    const int64_t L = static_cast<int64_t>(key >> 5);
-    const int64_t L0 = __shfl_sync(~0u, L, 0);
-    const int64_t x = lane < m ? static_cast<int64_t>(S.xs[next + lane]) : 0;
-    const bool c = lane < m && (L - L0 < x);
-    const unsigned bal = __ballot_sync(~0u, c);
-    const int k = bal == ~0u ? 32 : __ffs(~bal) - 1;
-    if (lane < k) {
-      const int b = static_cast<int>(key & 31u);
+    const uint64_t key = lane < d ? ((static_cast<uint64_t>(L) << 5) | lane) : kU64Max;
+    int rank = 0;
+    uint64_t mn = key;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {  // W independent shuffles in flight (keys of lanes >= d are MAX)
+      const uint64_t kj = __shfl_sync(~0u, key, j);
+      rank += kj < key;
+      mn = kj < mn ? kj : mn;
+    }
+    const int64_t L0 = static_cast<int64_t>(mn >> 5);
+    const bool live = lane < d && rank < m;
+    const int64_t x = live ? static_cast<int64_t>(S.xs[next + rank]) : 0;
+    const bool c = live && (L - L0 < x);
+    const int k = __popc(__ballot_sync(~0u, c));  // c holds exactly for ranks 0..k-1
+    if (c) {
       if (kWrite) {
-        const int32_t pos = S.ord[next + lane];
-        S.a_dest[pos] = static_cast<uint8_t>(b);
-        S.a_slot[pos] = static_cast<uint16_t>(S.cnt_a[b]);
+        const int32_t pos = S.ord[next + rank];
+        S.a_dest[pos] = static_cast<uint8_t>(lane);
+        S.a_slot[pos] = static_cast<uint16_t>(cnt);
         dst_off[pos] = L;
       }
-      S.cnt_a[b] += 1;  // each bin has one rank: no race
-      key = (static_cast<uint64_t>(L + x) << 5) | static_cast<uint64_t>(b);
+      ++cnt;
+      L += x;
     }
-    __syncwarp();
-    key = warp_bitonic(key, width);
     next += k;
     ++rounds;
   }
-  if (lane < d) S.tok_a[key & 31u] = static_cast<int64_t>(key >> 5);
+  if (lane < d) {
+    S.cnt_a[lane] = cnt;
+    S.tok_a[lane] = L;
+  }
   __syncwarp();
   if (rounds_out && lane == 0) *rounds_out = rounds;
+}
+
+template <bool kWrite, int ITEMS>
+__device__ void warp_greedy(SmallSmem<ITEMS>& S, int d, int first, int n, const int64_t* init_load,
+                            const int32_t* init_cnt, int64_t* dst_off, int64_t* rounds_out) {
+  if (d <= 8)
+    warp_greedy_w<kWrite, 8>(S, d, first, n, init_load, init_cnt, dst_off, rounds_out);
+  else if (d <= 16)
+    warp_greedy_w<kWrite, 16>(S, d, first, n, init_load, init_cnt, dst_off, rounds_out);
+  else
+    warp_greedy_w<kWrite, 32>(S, d, first, n, init_load, init_cnt, dst_off, rounds_out);
 }
 
 template <int ITEMS>
@@ -169,9 +183,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   using SS = SmallSmem<ITEMS>;
   SS& S = *reinterpret_cast<SS*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
-  // provably warp-uniform (no WARPSYNC.COLLECTIVE around the warp-level greedy)
+  // provably warp-uniform (no WARPSYNC.COLLECTIVE around the warp-level code)
   const int warp = __shfl_sync(~0u, tid >> 5, 0);
   const int n = a.n, d = a.d;
+  const int nch = (n + 31) / 32;
   orch_summary* sum = a.s;
 
   SMALL_MARK(0);
@@ -182,7 +197,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     S.maxlen = 0;
     S.total = 0;
   }
-  if (tid <= kSmallMaxD) S.cnt_id[tid] = 0;
   __syncthreads();
   {
     int64_t mx = 0, tot = 0;
@@ -191,11 +205,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       const int64_t l = a.len[i];
       S.len[i] = l;
       S.org[i] = o;
-      if (o < 0 || o >= d || l < 1) {
-        atomicMin(&S.bad, i);
-      } else {
-        atomicAdd(&S.cnt_id[o], 1);
-      }
+      if (o < 0 || o >= d || l < 1) atomicMin(&S.bad, i);
       if (l > ORCH_MAX_LENGTH) S.unsup = 1;
       mx = l > mx ? l : mx;
       tot += l > 0 ? l : 0;
@@ -223,21 +233,27 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   }
 
   SMALL_MARK(1);
-  // ---- S2: identity grouping: stable sort by origin
-  const int obits = 32 - __clz(d);  // covers the padding key d
-  {
-    uint32_t keys[ITEMS];
-    int32_t vals[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const int i = tid * ITEMS + j;
-      keys[j] = i < n ? static_cast<uint32_t>(S.org[i]) : static_cast<uint32_t>(d);
-      vals[j] = i;
-    }
-    typename SS::Sort(S.tmp.sort).Sort(keys, vals, 0, obits);
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) S.ord_id[tid * ITEMS + j] = vals[j];
+  // ---- S2: identity grouping (batches_from_items, core.cpp:183-199): the
+  // source slot of an item is the number of earlier items with its origin.
+  for (int c = warp; c < nch; c += kSmallWarps) {
+    const int i = c * 32 + lane;
+    const int o = i < n ? S.org[i] : kSmallMaxD + lane;  // padding never matches
+    const unsigned peers = __match_any_sync(~0u, o);
+    if (i < n) S.id_rank[i] = static_cast<uint16_t>(__popc(peers & ((1u << lane) - 1u)));
+    if (lane < d) S.chunk_cnt[c][lane] = 0;
+    __syncwarp();
+    if (i < n && (__ffs(peers) - 1) == lane) S.chunk_cnt[c][o] = static_cast<uint8_t>(__popc(peers));
   }
+  __syncthreads();
+  if (tid < d) {  // running count of each origin over the chunks
+    int run = 0;
+    for (int c = 0; c < nch; ++c) {
+      S.chunk_base[c][tid] = static_cast<uint16_t>(run);
+      run += S.chunk_cnt[c][tid];
+    }
+    S.cnt_id[tid] = run;
+  }
+  __syncthreads();
   if (warp == 0) {  // offsets of the origin batches
     const int c = lane < d ? S.cnt_id[lane] : 0;
     int incl = c;
@@ -247,6 +263,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     }
     if (lane < d) S.off_id[lane] = incl - c;
     if (lane == 0) S.off_id[d] = n;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kSmallThreads) {
+    const int o = S.org[i];
+    const int slot = S.chunk_base[i >> 5][o] + S.id_rank[i];
+    a.src_slot[i] = slot;
+    S.ord_id[S.off_id[o] + slot] = i;
   }
   __syncthreads();
   {
@@ -266,7 +289,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   for (int k = tid; k < n; k += kSmallThreads) {
     const int32_t pos = S.ord_id[k];
     const int st = S.off_id[S.org[pos]];
-    a.src_slot[pos] = k - st;
     a.src_off[pos] = S.pfx[k] - S.pfx[st];
     a.src_member[k] = pos;
   }
@@ -285,8 +307,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
 #pragma unroll
       for (int j = 0; j < ITEMS; ++j) {
         const int i = tid * ITEMS + j;
-        keys[j] = i < n ? static_cast<uint32_t>(S.len[i])
-                        : (asc ? pad_asc : 0u);
+        keys[j] = i < n ? static_cast<uint32_t>(S.len[i]) : (asc ? pad_asc : 0u);
         vals[j] = i;
       }
       __syncthreads();  // tmp storage reuse
@@ -305,45 +326,36 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     if (a.kind == ORCH_GREEDY_UNPADDED) {
       if (warp == 0) warp_greedy<true>(S, d, 0, n, nullptr, nullptr, a.dst_off, &S.rounds);
     } else if (a.kind == ORCH_QUADRATIC_TOLERANCE) {
-      if (warp == 0) {  // champion scan (balancers.cpp:223-231), d <= 32: one ballot + restarts
-        if (lane < d) {
-          S.qsum[lane] = 0;
-          S.qsq[lane] = 0;
-          S.cnt_a[lane] = 0;
-        }
-        __syncwarp();
+      if (warp == 0) {  // champion scan (balancers.cpp:223-231) with the batches in lanes
+        int64_t qs = 0, qq = 0;
+        int32_t cnt = 0;
         for (int k = 0; k < n; ++k) {
           int best = 0;
-          int64_t bs = S.qsum[0], bq = S.qsq[0];
-          int i0 = 1;
-          while (i0 < d) {
-            const int i = i0 + lane;
-            bool c = false;
-            if (i < d) {
-              const int64_t as = S.qsum[i], aq = S.qsq[i];
-              const int64_t df = as - bs;
-              c = (df < 0 ? -df : df) < a.tol_v ? (aq < bq) : (as < bs);
-            }
+          for (;;) {
+            const int64_t bs = __shfl_sync(~0u, qs, best);
+            const int64_t bq = __shfl_sync(~0u, qq, best);
+            const int64_t df = qs - bs;
+            const bool c = lane > best && lane < d &&
+                           ((df < 0 ? -df : df) < a.tol_v ? (qq < bq) : (qs < bs));
             const unsigned m = __ballot_sync(~0u, c);
             if (!m) break;
-            best = i0 + __ffs(m) - 1;
-            bs = S.qsum[best];
-            bq = S.qsq[best];
-            i0 = best + 1;
+            best = __ffs(m) - 1;  // the first later batch that beats the champion
           }
-          if (lane == 0) {
+          if (lane == best) {
             const int64_t x = S.xs[k];
             const int32_t pos = S.ord[k];
             S.a_dest[pos] = static_cast<uint8_t>(best);
-            S.a_slot[pos] = static_cast<uint16_t>(S.cnt_a[best]);
-            a.dst_off[pos] = S.qsum[best];
-            S.cnt_a[best] += 1;
-            S.qsum[best] += x;
-            S.qsq[best] += x * x;
+            S.a_slot[pos] = static_cast<uint16_t>(cnt);
+            a.dst_off[pos] = qs;
+            ++cnt;
+            qs += x;
+            qq += x * x;
           }
-          __syncwarp();
         }
-        if (lane < d) S.tok_a[lane] = S.qsum[lane];
+        if (lane < d) {
+          S.cnt_a[lane] = cnt;
+          S.tok_a[lane] = qs;
+        }
         if (lane == 0) S.rounds = n;
       }
     } else if (a.kind == ORCH_CONVTRANSFORMER) {
@@ -426,11 +438,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         S.hi = max_len * (n / d + 1);
       }
       __syncthreads();
+      constexpr int W = kSmallWarps;
       while (true) {
         const int64_t lo = S.lo, hi = S.hi;
         if (lo >= hi) break;
         const int64_t span = hi - lo;
-        const int64_t c = span <= 32 ? lo + warp : lo + (span * warp) / 32;
+        const int64_t c = span <= W ? lo + warp : lo + (span * warp) / W;
         bool f = true;
         if (c < hi) f = warp_feasible(S.xs, n, d, c, lane);
         if (lane == 0) {
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         __syncthreads();
         if (tid == 0) {
           int64_t nhi = hi, nlo = lo;
-          for (int w = 0; w < 32; ++w) {
+          for (int w = 0; w < W; ++w) {
             if (S.cand[w] >= hi) continue;
             if (S.feas[w]) {
               if (S.cand[w] < nhi) nhi = S.cand[w];
@@ -500,15 +513,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       const int sl = S.a_slot[i];
       a.dest_inst[i] = b;
       a.dest_slot[i] = sl;
-      a.bin_member[S.off_a[b] + sl] = i;
+      S.ord[S.off_a[b] + sl] = i;  // reuse: algorithm members in (batch, slot) order
     }
+    __syncthreads();
+    for (int k = tid; k < n; k += kSmallThreads) a.bin_member[k] = S.ord[k];
     if (tid <= d) a.bin_offset[tid] = S.off_a[tid];
-    __syncthreads();  // bin_member (global) visible to the block
   }
 
   SMALL_MARK(5);
   // ---- S6: batch costs (core.cpp:91-118): warp w -> algorithm batch w, identity batch w
-  for (int task = warp; task < 2 * d; task += 32) {
+  for (int task = warp; task < 2 * d; task += kSmallWarps) {
     const int side = task < d ? 0 : 1;  // 0 algorithm, 1 identity
     const int b = side ? task - d : task;
     if (side == 0 && a.identity_only) continue;
@@ -518,7 +532,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     unsigned long long sq = 0;
     bool inexact = false;
     for (int k = beg + lane; k < end; k += 32) {
-      const int32_t pos = side ? S.ord_id[k] : a.bin_member[k];
+      const int32_t pos = side ? S.ord_id[k] : S.ord[k];
       const int64_t l = S.len[pos];
       s += l;
       mx = l > mx ? l : mx;
@@ -533,14 +547,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       sq += __shfl_xor_sync(~0u, sq, off);
     }
     inexact = __any_sync(~0u, inexact) || sq >= (1ull << 53);
-    // the identity side must score under the policy cost model too
+    // the identity side is scored under the policy cost model too
     const orch_cost_model& m = a.model;
     double sqd = static_cast<double>(sq);
     if (inexact && m.variant == ORCH_TRANSFORMER_QUADRATIC && !m.padded) {
       double acc = 0.0;
       if (lane == 0)
         for (int k = beg; k < end; ++k) {
-          const double l = static_cast<double>(S.len[side ? S.ord_id[k] : a.bin_member[k]]);
+          const double l = static_cast<double>(S.len[side ? S.ord_id[k] : S.ord[k]]);
           acc = rn_add(acc, rn_mul(l, l));
         }
       sqd = __shfl_sync(~0u, acc, 0);
@@ -590,7 +604,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     sum->used_identity = S.used_identity;
     sum->error = 0;
     sum->error_index = INT64_MAX;
-    sum->bound = a.identity_only ? 0 : ((a.kind == ORCH_BINARY_PADDED || a.kind == ORCH_CONVTRANSFORMER) ? S.bound : 0);
+    sum->bound = a.identity_only
+                     ? 0
+                     : ((a.kind == ORCH_BINARY_PADDED || a.kind == ORCH_CONVTRANSFORMER) ? S.bound
+                                                                                         : 0);
     sum->rounds = a.identity_only ? 0 : S.rounds;
   }
   __syncthreads();
