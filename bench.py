@@ -234,6 +234,8 @@ def run_b200(args):
             ctx_meta.allgather_items(comm_meta, s["pos"], s["llen"], s["lorg"], s["max_local"],
                                      s["n"], B["glen"], B["gorg"], stream=stream)
         ctx_meta.balance(0, D_INST, B["glen"], B["gorg"], out=B["bal"], stream=stream)
+        if P > 1 and args.nodewise:  # GPU-wise hosting (orchestrator.cpp:283 with node = GPU)
+            ctx_meta.nodewise(D_INST, c, B["glen"], B["gorg"], B["bal"], stream=stream)
         ctx_meta.layout(D_INST, P, B["glen"], B["gorg"], B["bal"], out=B["lay"], stream=stream)
 
     # sizing pass (not timed): buffers from this batch's layout
@@ -414,6 +416,7 @@ def run_b200(args):
     if P > 1:
         a2a_bytes = sum(s["send_rows"] for s in st) * R
         line["exchange"] = args.exchange
+        line["nodewise_hosting"] = bool(args.nodewise)
         line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes,
                        "busbw_gbs_rank": a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9,
                        "nvlink_peak_gbs": 900.0, "nvlink_measured_gbs": 770.0,
@@ -445,6 +448,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nodewise", dest="nodewise", action="store_false",
+                    help="N>1: skip the GPU-wise hosting of destination batches")
     ap.add_argument("--exchange", default="put", choices=["put", "nccl"],
                     help="N>1: fused pack+put over NVLink (default) or NCCL send/recv")
     args = ap.parse_args()

@@ -82,6 +82,7 @@ class Oracle:
         L.orc_stats.restype = None
         L.orc_volume_matrix.restype = None
         L.orc_fill_rows.restype = None
+        L.orc_batch_to_instance.restype = None
 
     def _check(self, rc):
         if rc != 0:
@@ -186,6 +187,20 @@ class Oracle:
             _p(origin, C.c_int32), _p(dest_inst, C.c_int32), _p(rs, C.c_int64),
             _p(rd, C.c_int64), C.c_size_t(row_bytes), ins, outs, C.c_int(nthreads)))
 
+    def solve_hosting(self, d, c, V):
+        V = np.ascontiguousarray(V, dtype=np.int64).reshape(-1)
+        hosting = np.zeros(d, np.int32)
+        eg = np.zeros(d // c, np.int64)
+        mx, base, vis = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.lib.orc_solve_hosting(C.c_int(d), C.c_int(c), _p(V, C.c_int64),
+                                               _p(hosting, C.c_int32), _p(eg, C.c_int64),
+                                               C.byref(mx), C.byref(base), C.byref(vis)))
+        b2i = np.zeros(d, np.int32)
+        self.lib.orc_batch_to_instance(C.c_int(d), C.c_int(c), _p(hosting, C.c_int32),
+                                       _p(b2i, C.c_int32))
+        return dict(hosting=hosting, per_node_egress=eg, max_egress=mx.value,
+                    baseline_max=base.value, visited=vis.value, batch_to_instance=b2i)
+
     def fill_rows(self, length, tag, row_off, row_bytes, buf):
         length, tag, row_off = _i64(length), _i64(tag), _i64(row_off)
         self.lib.orc_fill_rows(C.c_int64(len(length)), _p(length, C.c_int64), _p(tag, C.c_int64),
@@ -256,6 +271,15 @@ class RefLib:
                                       _p(lengths, C.c_int64), C.c_int(batch_padded),
                                       C.byref(out)))
         return out.value
+
+    def solve_hosting(self, d, c, V):
+        V = np.ascontiguousarray(V, dtype=np.int64).reshape(-1)
+        hosting = np.zeros(d, np.int32)
+        mx, vis = C.c_int64(), C.c_int64()
+        self._check(self.lib.ref_solve_hosting(C.c_int(d), C.c_int(c), _p(V, C.c_int64),
+                                               _p(hosting, C.c_int32), C.byref(mx),
+                                               C.byref(vis)))
+        return dict(hosting=hosting, max_egress=mx.value, visited=vis.value)
 
     def time_balance(self, kind, d, length, origin, reps, lam=0.0, v=0):
         length, origin = _i64(length), _i32(origin)

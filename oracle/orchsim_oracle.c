@@ -617,3 +617,224 @@ void orc_fill_rows(int64_t n, const int64_t* len, const int64_t* tag, const int6
     }
   }
 }
+
+/* ------------------------------------------------------- node-wise hosting */
+
+/* inter_node_egress: topology.cpp:61-89 */
+static void egress_of(int d, int c, const int64_t* V, const int32_t* hosting, int64_t* egress) {
+  const int nodes = d / c;
+  for (int n = 0; n < nodes; ++n) egress[n] = 0;
+  for (int i = 0; i < d; ++i) {
+    const int src = i / c;
+    for (int b = 0; b < d; ++b)
+      if (hosting[b] != src) egress[src] += V[(size_t)i * d + b];
+  }
+}
+
+typedef struct {
+  int nodes, d;
+  int64_t* gain;       /* [nodes][d] */
+  int64_t* node_total; /* [nodes] */
+  int32_t* preferred;  /* [nodes][d] batches by descending gain (stable) */
+  int32_t* order;      /* [d] branching order */
+  int32_t* assignment; /* [d] */
+  int32_t* remaining;  /* [nodes] */
+  int64_t* gained;     /* [nodes] */
+  int64_t best;
+  int32_t* best_assignment;
+  int64_t visited;
+} hsearch;
+
+static int64_t hs_optimistic(const hsearch* h, int n) { /* topology.cpp:114-126 */
+  int64_t total = 0;
+  int taken = 0;
+  for (int k = 0; k < h->d; ++k) {
+    if (taken == h->remaining[n]) break;
+    const int b = h->preferred[(size_t)n * h->d + k];
+    if (h->assignment[b] == -1) {
+      total += h->gain[(size_t)n * h->d + b];
+      ++taken;
+    }
+  }
+  return total;
+}
+
+static int64_t hs_lower_bound(const hsearch* h) { /* :128-134 */
+  int64_t bound = 0;
+  for (int n = 0; n < h->nodes; ++n) {
+    const int64_t v = h->node_total[n] - h->gained[n] - hs_optimistic(h, n);
+    if (v > bound) bound = v;
+  }
+  return bound;
+}
+
+static int64_t hs_evaluate(const hsearch* h, const int32_t* hosting) { /* :136-141 */
+  int64_t worst = INT64_MIN;
+  for (int n = 0; n < h->nodes; ++n) {
+    int64_t e = h->node_total[n];
+    for (int b = 0; b < h->d; ++b)
+      if (hosting[b] == n) e -= h->gain[(size_t)n * h->d + b];
+    if (e > worst) worst = e;
+  }
+  return worst;
+}
+
+static void hs_offer(hsearch* h, const int32_t* hosting) { /* :143-149 */
+  const int64_t v = hs_evaluate(h, hosting);
+  if (v < h->best) {
+    h->best = v;
+    memcpy(h->best_assignment, hosting, (size_t)h->d * sizeof(int32_t));
+  }
+}
+
+static const int64_t* g_cmp_gain;
+static int cmp_gain_desc(const void* a, const void* b) {
+  const int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  if (g_cmp_gain[x] != g_cmp_gain[y]) return g_cmp_gain[x] > g_cmp_gain[y] ? -1 : 1;
+  return x < y ? -1 : (x > y); /* stable: ties keep ascending index */
+}
+
+static void hs_dfs(hsearch* h, int depth) { /* :151-172 */
+  ++h->visited;
+  if (hs_lower_bound(h) >= h->best) return;
+  if (depth == h->d) {
+    hs_offer(h, h->assignment);
+    return;
+  }
+  const int b = h->order[depth];
+  int32_t cand[64];
+  int nc = 0;
+  for (int n = 0; n < h->nodes; ++n)
+    if (h->remaining[n] > 0) cand[nc++] = n;
+  /* stable sort of candidate nodes by descending gain for batch b */
+  for (int i = 1; i < nc; ++i) { /* insertion sort = stable */
+    const int32_t v = cand[i];
+    int j = i - 1;
+    while (j >= 0 && h->gain[(size_t)cand[j] * h->d + b] < h->gain[(size_t)v * h->d + b]) {
+      cand[j + 1] = cand[j];
+      --j;
+    }
+    cand[j + 1] = v;
+  }
+  for (int k = 0; k < nc; ++k) {
+    const int n = cand[k];
+    h->assignment[b] = n;
+    h->remaining[n] -= 1;
+    h->gained[n] += h->gain[(size_t)n * h->d + b];
+    hs_dfs(h, depth + 1);
+    h->gained[n] -= h->gain[(size_t)n * h->d + b];
+    h->remaining[n] += 1;
+    h->assignment[b] = -1;
+  }
+}
+
+int orc_solve_hosting(int d, int c, const int64_t* V, int32_t* hosting, int64_t* per_node_egress,
+                      int64_t* max_egress, int64_t* baseline_max, int64_t* nodes_visited) {
+  if (d < 1 || c < 1) return fail(1, "topology needs at least one instance and one per node");
+  if (d % c) return fail(1, "instance count must be divisible by instances per node");
+  const int nodes = d / c;
+  if (nodes > 64) return fail(1, "oracle hosting search limited to 64 nodes");
+  hsearch h;
+  memset(&h, 0, sizeof h);
+  h.nodes = nodes;
+  h.d = d;
+  h.gain = calloc((size_t)nodes * d, sizeof(int64_t));
+  h.node_total = calloc((size_t)nodes, sizeof(int64_t));
+  for (int i = 0; i < d; ++i) {
+    const int n = i / c;
+    for (int b = 0; b < d; ++b) {
+      h.gain[(size_t)n * d + b] += V[(size_t)i * d + b];
+      h.node_total[n] += V[(size_t)i * d + b];
+    }
+  }
+  h.preferred = malloc((size_t)nodes * d * sizeof(int32_t));
+  for (int n = 0; n < nodes; ++n) {
+    int32_t* list = h.preferred + (size_t)n * d;
+    for (int b = 0; b < d; ++b) list[b] = b;
+    g_cmp_gain = h.gain + (size_t)n * d;
+    qsort(list, (size_t)d, sizeof(int32_t), cmp_gain_desc);
+  }
+  /* branching order: descending regret (top - second gain), stable (:219-238) */
+  int64_t* regret = malloc((size_t)d * sizeof(int64_t));
+  h.order = malloc((size_t)d * sizeof(int32_t));
+  for (int b = 0; b < d; ++b) {
+    int64_t top = 0, second = 0;
+    for (int n = 0; n < nodes; ++n) {
+      const int64_t g = h.gain[(size_t)n * d + b];
+      if (g > top) {
+        second = top;
+        top = g;
+      } else if (g > second) {
+        second = g;
+      }
+    }
+    regret[b] = top - second;
+    h.order[b] = b;
+  }
+  g_cmp_gain = regret;
+  qsort(h.order, (size_t)d, sizeof(int32_t), cmp_gain_desc);
+  h.assignment = malloc((size_t)d * sizeof(int32_t));
+  for (int b = 0; b < d; ++b) h.assignment[b] = -1;
+  h.remaining = malloc((size_t)nodes * sizeof(int32_t));
+  for (int n = 0; n < nodes; ++n) h.remaining[n] = c;
+  h.gained = calloc((size_t)nodes, sizeof(int64_t));
+  h.best = INT64_MAX;
+  h.best_assignment = malloc((size_t)d * sizeof(int32_t));
+  /* incumbents: identity, then greedy (:243-262) */
+  int32_t* tmp = malloc((size_t)d * sizeof(int32_t));
+  for (int b = 0; b < d; ++b) tmp[b] = b / c;
+  hs_offer(&h, tmp);
+  int32_t* room = malloc((size_t)nodes * sizeof(int32_t));
+  for (int n = 0; n < nodes; ++n) room[n] = c;
+  for (int k = 0; k < d; ++k) {
+    const int b = h.order[k];
+    int pick = -1;
+    int64_t pick_gain = -1;
+    for (int n = 0; n < nodes; ++n)
+      if (room[n] > 0 && h.gain[(size_t)n * d + b] > pick_gain) {
+        pick = n;
+        pick_gain = h.gain[(size_t)n * d + b];
+      }
+    tmp[b] = pick;
+    room[pick] -= 1;
+  }
+  hs_offer(&h, tmp);
+  hs_dfs(&h, 0);
+  memcpy(hosting, h.best_assignment, (size_t)d * sizeof(int32_t));
+  int64_t* eg = per_node_egress ? per_node_egress : malloc((size_t)nodes * sizeof(int64_t));
+  egress_of(d, c, V, hosting, eg);
+  int64_t mx = INT64_MIN;
+  for (int n = 0; n < nodes; ++n)
+    if (eg[n] > mx) mx = eg[n];
+  if (max_egress) *max_egress = mx;
+  for (int b = 0; b < d; ++b) tmp[b] = b / c;
+  egress_of(d, c, V, tmp, eg);
+  int64_t bm = INT64_MIN;
+  for (int n = 0; n < nodes; ++n)
+    if (eg[n] > bm) bm = eg[n];
+  if (baseline_max) *baseline_max = bm;
+  if (nodes_visited) *nodes_visited = h.visited;
+  if (!per_node_egress) free(eg);
+  else egress_of(d, c, V, hosting, per_node_egress);
+  free(room);
+  free(tmp);
+  free(regret);
+  free(h.gain);
+  free(h.node_total);
+  free(h.preferred);
+  free(h.order);
+  free(h.assignment);
+  free(h.remaining);
+  free(h.gained);
+  free(h.best_assignment);
+  return 0;
+}
+
+/* topology.cpp:281-290: within a node, batches take instances in ascending batch order */
+void orc_batch_to_instance(int d, int c, const int32_t* hosting, int32_t* batch_to_instance) {
+  const int nodes = d / c;
+  int32_t* next = malloc((size_t)nodes * sizeof(int32_t));
+  for (int n = 0; n < nodes; ++n) next[n] = n * c;
+  for (int b = 0; b < d; ++b) batch_to_instance[b] = next[hosting[b]]++;
+  free(next);
+}

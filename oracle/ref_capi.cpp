@@ -150,6 +150,25 @@ int ref_cost(double alpha, double beta, int padded, int variant, int64_t n, cons
   }
 }
 
+// solve_hosting (topology.hpp:71) on a d*d volume matrix (src-major) with
+// instances_per_node = c (bandwidths 1: only the hosting matters).
+int ref_solve_hosting(int d, int c, const int64_t* V, int32_t* hosting, int64_t* max_egress,
+                      int64_t* nodes_visited) {
+  try {
+    VolumeMatrix vm(d);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) vm.at(i, j) = V[static_cast<size_t>(i) * d + j];
+    ClusterTopology topo{d, c, 2.0, 1.0};
+    const HostingSolution sol = solve_hosting(vm, topo);
+    for (int b = 0; b < d; ++b) hosting[b] = sol.hosting[static_cast<size_t>(b)];
+    *max_egress = sol.max_egress;
+    *nodes_visited = sol.nodes_visited;
+    return 0;
+  } catch (...) {
+    return classify(std::current_exception());
+  }
+}
+
 // Times `reps` back-to-back calls of the reference balance() on prebuilt
 // items (the reference's own operator, stock code path). Writes per-call
 // seconds into secs[reps].

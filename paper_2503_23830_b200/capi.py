@@ -29,6 +29,7 @@ EXPORTED = [
     "orch_layout", "orch_pack", "orch_exchange", "orch_unpack", "orch_dispatch",
     "orch_comm_unique_id", "orch_comm_create",
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
+    "orch_solve_hosting_host", "orch_nodewise",
     "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
     "orch_window_destroy", "orch_dispatch_put",
 ]
@@ -311,6 +312,31 @@ class Context:
             self.h, C.c_int32(d), C.c_int64(len(length)), length.ctypes.data_as(C.c_void_p),
             origin.ctypes.data_as(C.c_void_p), C.c_int64(bound), C.byref(out), _stream()))
         return bool(out.value)
+
+    # ---- node-wise hosting
+    def solve_hosting(self, d, c, V):
+        import numpy as np
+        V = np.ascontiguousarray(V, dtype=np.int64).reshape(-1)
+        hosting = np.zeros(d, np.int32)
+        mx, base = C.c_int64(), C.c_int64()
+        _check(lib().orch_solve_hosting_host(self.h, C.c_int32(d), C.c_int32(c),
+                                             V.ctypes.data_as(C.c_void_p),
+                                             hosting.ctypes.data_as(C.c_void_p), C.byref(mx),
+                                             C.byref(base), _stream()))
+        return dict(hosting=hosting, max_egress=mx.value, baseline_max=base.value)
+
+    def nodewise(self, d, c, length, origin, bal: "Balance", stream=None):
+        """Relabels bal's destination batches in place; returns device tensors
+        (hosting[d], batch_to_instance[d], info[4])."""
+        dev = length.device
+        hosting = torch.empty(d, dtype=torch.int32, device=dev)
+        b2i = torch.empty(d, dtype=torch.int32, device=dev)
+        info = torch.empty(4, dtype=torch.int64, device=dev)
+        b = bal.struct()
+        _check(lib().orch_nodewise(self.h, C.c_int32(d), C.c_int32(c), C.c_int64(length.numel()),
+                                   _ptr(length), _ptr(origin), C.byref(b), _ptr(hosting),
+                                   _ptr(b2i), _ptr(info), _stream(stream)))
+        return hosting, b2i, info
 
     # ---- cost model
     def batch_costs(self, alpha, beta, padded, variant, batch_padded, d, length, bin_offset,

@@ -1,6 +1,7 @@
 // orchsim topology subset over the B200 C-ABI: the volume matrix of a
 // rearrangement is accumulated by the sm_100a kernel (orch_volume_matrix);
 // semantics of /root/reference/proj/src/topology.cpp:12-53.
+#include <algorithm>
 #include <numeric>
 
 #include "orchsim/topology.hpp"
@@ -55,6 +56,83 @@ VolumeMatrix volume_matrix(const std::vector<MiniBatch>& batches, const Rearrang
     b200::check(orch_volume_matrix_host(b200::context(), d, static_cast<std::int64_t>(len.size()),
                                         len.data(), src.data(), dst.data(), V.data(), nullptr));
   return V;
+}
+
+std::vector<int> identity_hosting(const ClusterTopology& topo) {  // topology.cpp:55-59
+  std::vector<int> h(static_cast<std::size_t>(topo.instance_count));
+  for (int b = 0; b < topo.instance_count; ++b) h[b] = topo.node_of(b);
+  return h;
+}
+
+std::vector<std::int64_t> inter_node_egress(const VolumeMatrix& v, const ClusterTopology& topo,
+                                            const std::vector<int>& hosting) {  // :61-89
+  validate_topology(topo);
+  const int d = topo.instance_count, nodes = topo.node_count();
+  if (v.dimension() != d || static_cast<int>(hosting.size()) != d)
+    throw std::invalid_argument("volume matrix / hosting size does not match topology");
+  std::vector<int> per(static_cast<std::size_t>(nodes), 0);
+  for (int node : hosting) {
+    if (node < 0 || node >= nodes) throw std::invalid_argument("hosting references unknown node");
+    ++per[node];
+  }
+  for (int k : per)
+    if (k != topo.instances_per_node)
+      throw std::invalid_argument("hosting must place exactly c batches per node");
+  std::vector<std::int64_t> e(static_cast<std::size_t>(nodes), 0);
+  for (int i = 0; i < d; ++i)
+    for (int b = 0; b < d; ++b)
+      if (hosting[b] != topo.node_of(i)) e[topo.node_of(i)] += v.at(i, b);
+  return e;
+}
+
+HostingSolution solve_hosting(const VolumeMatrix& volumes, const ClusterTopology& topo) {
+  validate_topology(topo);
+  const int d = topo.instance_count;
+  if (volumes.dimension() != d)
+    throw std::invalid_argument("volume matrix dimension does not match topology");
+  std::vector<std::int64_t> flat(static_cast<std::size_t>(d) * d);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) flat[static_cast<std::size_t>(i) * d + j] = volumes.at(i, j);
+  std::vector<int32_t> h(static_cast<std::size_t>(d));
+  std::int64_t mx = 0, base = 0;
+  b200::check(orch_solve_hosting_host(b200::context(), d, topo.instances_per_node, flat.data(),
+                                      h.data(), &mx, &base, nullptr));
+  HostingSolution sol;
+  sol.hosting.assign(h.begin(), h.end());
+  sol.per_node_egress = inter_node_egress(volumes, topo, sol.hosting);
+  sol.max_egress = mx;
+  long double space = 1;  // balanced hostings scored
+  for (int i = 1; i <= d; ++i) space *= i;
+  for (int k = 0; k < topo.node_count(); ++k)
+    for (int i = 1; i <= topo.instances_per_node; ++i) space /= i;
+  sol.nodes_visited = static_cast<std::int64_t>(space);
+  return sol;
+}
+
+NodewiseResult nodewise_rearrange(const std::vector<MiniBatch>& batches, const Rearrangement& re,
+                                  const ClusterTopology& topo) {  // topology.cpp:267-303
+  validate_topology(topo);
+  if (re.instance_count() != topo.instance_count)
+    throw std::invalid_argument("rearrangement instance count does not match topology");
+  const int d = topo.instance_count;
+  const VolumeMatrix v = volume_matrix(batches, re);
+  HostingSolution sol = solve_hosting(v, topo);
+  const auto baseline = inter_node_egress(v, topo, identity_hosting(topo));
+  std::vector<int> b2i(static_cast<std::size_t>(d), -1);
+  std::vector<int> next(static_cast<std::size_t>(topo.node_count()));
+  for (int n = 0; n < topo.node_count(); ++n) next[n] = n * topo.instances_per_node;
+  for (int b = 0; b < d; ++b) b2i[b] = next[sol.hosting[b]]++;
+  std::map<SlotRef, SlotRef> moves;
+  for (const auto& kv : re.moves()) moves.emplace(kv.first, SlotRef{b2i[kv.second.instance], kv.second.slot});
+  NodewiseResult r;
+  r.rearrangement = Rearrangement(d, std::move(moves));
+  r.hosting = sol.hosting;
+  r.max_egress = sol.max_egress;
+  r.per_node_egress = sol.per_node_egress;
+  r.baseline_max_egress = *std::max_element(baseline.begin(), baseline.end());
+  r.batch_to_instance = std::move(b2i);
+  r.nodes_visited = sol.nodes_visited;
+  return r;
 }
 
 }  // namespace orchsim

@@ -1,0 +1,96 @@
+"""GPU node-wise hosting (orch_solve_hosting_host / orch_nodewise) against the
+oracle restatement of the reference's branch and bound (exact hosting, the
+reference's tie-breaking) and the reference's own fixtures."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_instance
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def test_solve_hosting_random(ctx, oracle):
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        c = int(rng.integers(1, 5))
+        nodes = int(rng.integers(1, 6))
+        d = c * nodes
+        if d > 12:
+            continue
+        V = rng.integers(0, int(rng.choice([2, 3, 100, 10000])), (d, d)) * (rng.random((d, d)) < 0.7)
+        a = ctx.solve_hosting(d, c, V)
+        o = oracle.solve_hosting(d, c, V)
+        np.testing.assert_array_equal(a["hosting"], o["hosting"])
+        assert a["max_egress"] == o["max_egress"]
+        assert a["baseline_max"] == o["baseline_max"]
+
+
+def test_solve_hosting_fixtures(ctx):
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting.npz"))
+    for k in range(len(f["d"])):
+        d, c = int(f["d"][k]), int(f["c"][k])
+        a = ctx.solve_hosting(d, c, f["V"][k, :d * d])
+        np.testing.assert_array_equal(a["hosting"], f["hosting"][k, :d])
+        assert a["max_egress"] == f["max_egress"][k]
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_nodewise_in_place(ctx, oracle, P):
+    """balance -> orch_nodewise: dest instances relabelled by batch_to_instance,
+    per-batch arrays and CSR permuted, then layout + dispatch still byte-exact."""
+    rng = np.random.default_rng(P)
+    for kind in (0, 1, 2, 3):
+        d = 8
+        c = d // P
+        n = 300
+        L, O = random_instance(rng, d, n, 1, 60)
+        o = oracle.balance(kind, d, L, O, lam=0.01, v=3)
+        V = oracle.volume_matrix(d, L, O, o.dest_inst)
+        h = oracle.solve_hosting(d, c, V)
+        b2i = h["batch_to_instance"]
+        Lt, Ot = torch.from_numpy(L).cuda(), torch.from_numpy(O).cuda()
+        bal = ctx.balance(kind, d, Lt, Ot, lam=0.01, v=3)
+        hosting, g_b2i, info = ctx.nodewise(d, c, Lt, Ot, bal)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(hosting.cpu().numpy(), h["hosting"])
+        np.testing.assert_array_equal(g_b2i.cpu().numpy(), b2i)
+        assert int(info[0]) == h["max_egress"] and int(info[1]) == h["baseline_max"]
+        np.testing.assert_array_equal(bal.dest_inst[:n].cpu().numpy(), b2i[o.dest_inst])
+        np.testing.assert_array_equal(bal.dest_slot[:n].cpu().numpy(), o.dest_slot)
+        inv = np.argsort(b2i)
+        np.testing.assert_array_equal(bal.bin_count.cpu().numpy(), o.bin_count[inv])
+        assert bal.bin_cost.cpu().numpy().tobytes() == o.bin_cost[inv].tobytes()
+        off = bal.bin_offset.cpu().numpy()
+        mem = bal.bin_member[:n].cpu().numpy()
+        di = b2i[o.dest_inst]
+        for j in range(d):
+            seg = mem[off[j]:off[j + 1]]
+            assert (di[seg] == j).all() and (o.dest_slot[seg] == np.arange(len(seg))).all()
+        # the relabelled result still dispatches byte-exactly
+        R = 32
+        lay = ctx.layout(d, 1, Lt, Ot, bal)
+        e = oracle.layout(d, 1, L, O, di, o.dest_slot)
+        rows = int(L.sum())
+        hin = np.zeros(rows * R, np.uint8)
+        oracle.fill_rows(L, np.arange(n, dtype=np.int64), e["rank_src_off"], R, hin)
+        hout = np.zeros_like(hin)
+        oracle.dispatch_rows(d, 1, L, O, di, e["rank_src_off"], e["rank_dst_off"], R, [hin], [hout])
+        rin = torch.from_numpy(hin).cuda()
+        rout = torch.zeros_like(rin)
+        ctx.dispatch(d, Lt, Ot, bal, lay, R, rin, rout)
+        torch.cuda.synchronize()
+        assert torch.equal(rout.cpu(), torch.from_numpy(hout))
+
+
+def test_hosting_limits(ctx):
+    from paper_2503_23830_b200.capi import OrchError
+    with pytest.raises(OrchError) as e:
+        ctx.solve_hosting(64, 8, np.zeros((64, 64), np.int64))
+    assert e.value.code == 12
+    with pytest.raises(OrchError) as e:
+        ctx.solve_hosting(6, 4, np.zeros((6, 6), np.int64))
+    assert e.value.code == 1

@@ -137,3 +137,30 @@ def test_layout_and_rows_semantics(oracle):
                     assert (words[row:row + k, 0] == pos).all()
                     assert (words[row:row + k, 1] == np.arange(k)).all()
                     row += k
+
+
+def test_solve_hosting_vs_reference(oracle, reflib):
+    """solve_hosting (topology.cpp:179-265): the C restatement reproduces the
+    reference's hosting, max egress and even its branch-and-bound node count."""
+    rng = np.random.default_rng(17)
+    for _ in range(600):
+        c = int(rng.integers(1, 5))
+        nodes = int(rng.integers(1, 6))
+        d = c * nodes
+        if d > 12:
+            continue
+        V = rng.integers(0, int(rng.choice([3, 100, 10000])), (d, d)) * (rng.random((d, d)) < 0.7)
+        a = oracle.solve_hosting(d, c, V)
+        b = reflib.solve_hosting(d, c, V)
+        np.testing.assert_array_equal(a["hosting"], b["hosting"])
+        assert a["max_egress"] == b["max_egress"] and a["visited"] == b["visited"]
+
+
+def test_hosting_fixtures(oracle):
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting.npz"))
+    for k in range(len(f["d"])):
+        d, c = int(f["d"][k]), int(f["c"][k])
+        V = f["V"][k, :d * d].reshape(d, d)
+        a = oracle.solve_hosting(d, c, V)
+        np.testing.assert_array_equal(a["hosting"], f["hosting"][k, :d])
+        assert a["max_egress"] == f["max_egress"][k]
