@@ -289,9 +289,11 @@ def run_b200(args):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(data_stream)
-            if s["win"] is not None:
-                ctx_data.dispatch_put(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R,
-                                      s["rin"], s["win"], comm_data, stream=data_stream)
+            if s["win"] is not None:  # one barrier per step closes both phases' puts
+                ctx_data.put(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
+                             s["win"], comm_data, stream=data_stream)
+                if s is st[-1]:
+                    ctx_data.barrier(comm_data, stream=data_stream)
             else:
                 ctx_data.dispatch(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
                                   s["rout"], s["send"], s["recv"], comm_data, stream=data_stream)
@@ -414,13 +416,16 @@ def run_b200(args):
         "clocks": clocks.summary(),
     }
     if P > 1:
-        a2a_bytes = sum(s["send_rows"] for s in st) * R
+        a2a_bytes = max_over_ranks(sum(s["send_rows"] for s in st) * R)  # bottleneck rank
+        disp_ms = max_over_ranks(disp_ms)
         line["exchange"] = args.exchange
         line["nodewise_hosting"] = bool(args.nodewise)
         line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes,
                        "busbw_gbs_rank": a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9,
                        "nvlink_peak_gbs": 900.0, "nvlink_measured_gbs": 770.0,
-                       "note": "off-rank bytes of this rank / device time of its dispatch calls"}
+                       "note": "max over ranks of off-rank bytes / max over ranks of the device "
+                               "time of the dispatch calls; NVLink push ceiling measured with "
+                               "scratch/p2pbench.cu: ~710 GB/s per direction"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         times, ctoks, kind, nthreads = cpu_arm(phases, 1, 1)
         line["cpu_baseline"] = {"value": ctoks / times[0], "unit": "tokens/s", "cores": nthreads,

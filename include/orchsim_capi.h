@@ -295,6 +295,12 @@ int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, cons
                       const int32_t* d_origin, const orch_balance_out* bal,
                       const orch_layout_out* layout, size_t row_bytes, const void* d_in,
                       int64_t in_cap, orch_window* out_win, void* stream);
+/* The put alone (no barrier): several exchanges (e.g. the phases of one
+ * iteration) can share one orch_barrier. */
+int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+             const int32_t* d_origin, const orch_balance_out* bal,
+             const orch_layout_out* layout, size_t row_bytes, const void* d_in, int64_t in_cap,
+             orch_window* out_win, void* stream);
 
 /* gather_lengths (exchange.cpp:34-47) realised as ncclAllGather: every rank
  * contributes its local items (global input position, length, origin) and

@@ -31,7 +31,7 @@ EXPORTED = [
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
     "orch_solve_hosting_host", "orch_nodewise",
     "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
-    "orch_window_destroy", "orch_dispatch_put",
+    "orch_window_destroy", "orch_dispatch_put", "orch_put",
 ]
 
 
@@ -431,6 +431,20 @@ class Context:
                                        C.c_size_t(R), _ptr(rows_in),
                                        C.c_int64(self._rows(rows_in, R)), window.h,
                                        _stream(stream)))
+
+    def put(self, d, length, origin, bal: Balance, lay: Layout, row_bytes, rows_in,
+            window: "Window", comm: Comm, stream=None):
+        """Fused pack+put without the closing barrier (call barrier() after)."""
+        b, lo = bal.struct(), lay.struct()
+        R = row_bytes
+        _check(lib().orch_put(self.h, comm.h, C.c_int32(d), C.c_int64(length.numel()),
+                              _ptr(length), _ptr(origin), C.byref(b), C.byref(lo), C.c_size_t(R),
+                              _ptr(rows_in), C.c_int64(self._rows(rows_in, R)), window.h,
+                              _stream(stream)))
+
+    @staticmethod
+    def barrier(comm: Comm, stream=None):
+        _check(lib().orch_barrier(comm.h, _stream(stream)))
 
     def allgather_items(self, comm: Comm, local_pos, local_len, local_origin, max_local, n,
                         out_len, out_origin, stream=None):

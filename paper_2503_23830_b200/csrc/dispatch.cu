@@ -1173,7 +1173,7 @@ int orch_window_destroy(orch_window* w) {
   return rc;
 }
 
-int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
                       const int32_t* d_origin, const orch_balance_out* bal,
                       const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap,
                       orch_window* out_win, void* stream) {
@@ -1196,6 +1196,15 @@ int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, cons
     rc = run_move(ctx, kPut, a, n, L->rank_src_off, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
   }
+  return ORCH_OK;
+}
+
+int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                      const int32_t* d_origin, const orch_balance_out* bal,
+                      const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap,
+                      orch_window* out_win, void* stream) {
+  int rc = orch_put(ctx, comm, d, n, d_len, d_origin, bal, L, R, d_in, in_cap, out_win, stream);
+  if (rc) return rc;
   // rows from every peer have landed once every rank passed its put kernel
   return orch_barrier(comm, stream);
 }
