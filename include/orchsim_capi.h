@@ -215,6 +215,34 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
                   const int32_t* d_origin, const orch_balance_out* bal, int32_t* d_hosting,
                   int32_t* d_batch_to_instance, int64_t* d_info, void* stream);
 
+/* -------------------------------------------------- composed delivery */
+/* Any rearrangement of n items, given per item as (src_inst, src_slot) ->
+ * (dst_inst, dst_slot), laid out as a flat balance result (dest arrays,
+ * token offsets, both CSRs, bin_count/bin_tokens) so orch_layout and
+ * orch_dispatch / orch_put move its rows, with d_src_inst as the origin array.
+ * Validated like Rearrangement + apply (core.cpp:14-43, 120-161): instances in
+ * range, source and destination slots dense and unique per instance; a
+ * violation sets out->summary->error = ORCH_INVALID_ARGUMENT.
+ * compose(outer, inner) (exchange.cpp:125-137) of flat rearrangements is this
+ * call with inner's destination as the source and outer's destination as the
+ * target; inverse (exchange.cpp:115-123) swaps the two sides. */
+int orch_rearrange(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
+                   const int32_t* d_src_inst, const int32_t* d_src_slot,
+                   const int32_t* d_dst_inst, const int32_t* d_dst_slot,
+                   const orch_balance_out* out, void* stream);
+
+/* backbone_mapping_for (orchestrator.cpp:367-388): the backbone destination of
+ * every item of an encoder universe. Examples e in [0, E) with LLM result
+ * (d_llm_dest_inst, CSR d_llm_bin_offset / d_llm_bin_member from orch_balance);
+ * parts of example e are [part_offset[e], part_offset[e+1]) with interleave
+ * position d_interleave_pos[part]; universe items are the global part indices
+ * d_item_part[n]. Out: d_dst_inst[n], d_dst_slot[n]. */
+int orch_backbone_targets(orch_ctx* ctx, int32_t d, int64_t E, const int32_t* d_llm_dest_inst,
+                          const int32_t* d_llm_bin_offset, const int32_t* d_llm_bin_member,
+                          const int32_t* d_part_offset, const int32_t* d_interleave_pos,
+                          int64_t num_parts, int64_t n, const int32_t* d_item_part,
+                          int32_t* d_dst_inst, int32_t* d_dst_slot, void* stream);
+
 /* ------------------------------------------------------ layout / movement */
 /* volume_matrix (topology.cpp:40-53): d_V[d*d] (src-major) token volumes. */
 int orch_volume_matrix(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,

@@ -83,6 +83,7 @@ class Oracle:
         L.orc_volume_matrix.restype = None
         L.orc_fill_rows.restype = None
         L.orc_batch_to_instance.restype = None
+        L.orc_backbone_targets.restype = None
 
     def _check(self, rc):
         if rc != 0:
@@ -200,6 +201,29 @@ class Oracle:
                                        _p(b2i, C.c_int32))
         return dict(hosting=hosting, per_node_egress=eg, max_egress=mx.value,
                     baseline_max=base.value, visited=vis.value, batch_to_instance=b2i)
+
+    def backbone_targets(self, d, llm_dest_inst, llm_dest_slot, part_offset, interleave_pos,
+                         item_part):
+        a = [np.ascontiguousarray(x, np.int32) for x in
+             (llm_dest_inst, llm_dest_slot, part_offset, interleave_pos, item_part)]
+        n = len(a[4])
+        di, ds = np.zeros(n, np.int32), np.zeros(n, np.int32)
+        self.lib.orc_backbone_targets(C.c_int(d), C.c_int64(len(a[0])), _p(a[0], C.c_int32),
+                                      _p(a[1], C.c_int32), _p(a[2], C.c_int32),
+                                      _p(a[3], C.c_int32), C.c_int64(n), _p(a[4], C.c_int32),
+                                      _p(di, C.c_int32), _p(ds, C.c_int32))
+        return di, ds
+
+    def rearrange_offsets(self, d, length, src_inst, src_slot, dst_inst, dst_slot):
+        length = _i64(length)
+        si, ss, di, ds = (_i32(x) for x in (src_inst, src_slot, dst_inst, dst_slot))
+        n = len(length)
+        so, do = np.zeros(n, np.int64), np.zeros(n, np.int64)
+        self._check(self.lib.orc_rearrange_offsets(
+            C.c_int(d), C.c_int64(n), _p(length, C.c_int64), _p(si, C.c_int32),
+            _p(ss, C.c_int32), _p(di, C.c_int32), _p(ds, C.c_int32), _p(so, C.c_int64),
+            _p(do, C.c_int64)))
+        return so, do
 
     def fill_rows(self, length, tag, row_off, row_bytes, buf):
         length, tag, row_off = _i64(length), _i64(tag), _i64(row_off)

@@ -838,3 +838,104 @@ void orc_batch_to_instance(int d, int c, const int32_t* hosting, int32_t* batch_
   for (int b = 0; b < d; ++b) batch_to_instance[b] = next[hosting[b]]++;
   free(next);
 }
+
+/* ------------------------------------------------------- composed delivery */
+
+typedef struct {
+  int32_t slot;
+  int32_t ex;
+} arrival;
+static int cmp_arrival(const void* a, const void* b) {
+  const arrival* x = a;
+  const arrival* y = b;
+  return x->slot < y->slot ? -1 : (x->slot > y->slot);
+}
+
+void orc_backbone_targets(int d, int64_t E, const int32_t* llm_dest_inst,
+                          const int32_t* llm_dest_slot, const int32_t* part_offset,
+                          const int32_t* interleave_pos, int64_t n, const int32_t* item_part,
+                          int32_t* dst_inst, int32_t* dst_slot) {
+  /* part -> universe item */
+  const int64_t parts = part_offset[E];
+  int64_t* item_of = malloc((size_t)(parts ? parts : 1) * sizeof(int64_t));
+  for (int64_t p = 0; p < parts; ++p) item_of[p] = -1;
+  for (int64_t k = 0; k < n; ++k) item_of[item_part[k]] = k;
+  /* per instance: examples by LLM slot (orchestrator.cpp:370-378) */
+  arrival* arr = malloc((size_t)(E ? E : 1) * sizeof(arrival));
+  for (int inst = 0; inst < d; ++inst) {
+    int64_t m = 0;
+    for (int64_t e = 0; e < E; ++e)
+      if (llm_dest_inst[e] == inst) arr[m++] = (arrival){llm_dest_slot[e], (int32_t)e};
+    qsort(arr, (size_t)m, sizeof(arrival), cmp_arrival);
+    int slot = 0;
+    for (int64_t k = 0; k < m; ++k) {
+      const int32_t e = arr[k].ex;
+      const int np = part_offset[e + 1] - part_offset[e];
+      for (int q = 0; q < np; ++q) { /* parts in interleave order (:380-384) */
+        for (int p = part_offset[e]; p < part_offset[e + 1]; ++p) {
+          if (interleave_pos[p] != q) continue;
+          const int64_t it = item_of[p];
+          if (it >= 0) {
+            dst_inst[it] = inst;
+            dst_slot[it] = slot++;
+          }
+        }
+      }
+    }
+  }
+  free(arr);
+  free(item_of);
+}
+
+typedef struct {
+  int64_t key; /* inst * 2^31 + slot */
+  int32_t pos;
+} skey;
+static int cmp_skey(const void* a, const void* b) {
+  const skey* x = a;
+  const skey* y = b;
+  return x->key < y->key ? -1 : (x->key > y->key);
+}
+
+static int slot_offsets(int d, int64_t n, const int64_t* len, const int32_t* inst,
+                        const int32_t* slot, int64_t* off, const char* what) {
+  skey* k = malloc((size_t)(n ? n : 1) * sizeof(skey));
+  for (int64_t i = 0; i < n; ++i) {
+    if (inst[i] < 0 || inst[i] >= d) {
+      free(k);
+      return fail(1, "rearrangement references instance outside [0, d)");
+    }
+    k[i].key = (int64_t)inst[i] * 2147483648LL + slot[i];
+    k[i].pos = (int32_t)i;
+  }
+  qsort(k, (size_t)n, sizeof(skey), cmp_skey);
+  int64_t run = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    const int32_t i = k[j].pos;
+    const int new_inst = j == 0 || inst[k[j - 1].pos] != inst[i];
+    if (!new_inst && k[j].key == k[j - 1].key) {
+      free(k);
+      return fail(1, what[0] == 'd' ? "rearrangement maps two items to one destination slot"
+                                    : "rearrangement covers a slot twice");
+    }
+    const int expect = new_inst ? 0 : slot[k[j - 1].pos] + 1;
+    if (slot[i] != expect) {
+      free(k);
+      return fail(1, what[0] == 'd' ? "destination slots are not dense"
+                                    : "rearrangement covers a slot absent from the input batches");
+    }
+    if (new_inst) run = 0;
+    off[i] = run;
+    run += len[i];
+  }
+  free(k);
+  return 0;
+}
+
+int orc_rearrange_offsets(int d, int64_t n, const int64_t* len, const int32_t* src_inst,
+                          const int32_t* src_slot, const int32_t* dst_inst,
+                          const int32_t* dst_slot, int64_t* src_off, int64_t* dst_off) {
+  int rc = slot_offsets(d, n, len, dst_inst, dst_slot, dst_off, "dst");
+  if (rc) return rc;
+  return slot_offsets(d, n, len, src_inst, src_slot, src_off, "src");
+}

@@ -39,7 +39,7 @@ def _nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu", "exhaustive.cu", "hosting.cu"]
+CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu", "exhaustive.cu", "hosting.cu", "compose.cu"]
 HOST_SOURCES = ["host/core.cpp", "host/balancers.cpp", "host/topology.cpp", "host/exchange.cpp",
                 "host/runtime.cpp"]
 

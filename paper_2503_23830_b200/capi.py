@@ -29,7 +29,7 @@ EXPORTED = [
     "orch_layout", "orch_pack", "orch_exchange", "orch_unpack", "orch_dispatch",
     "orch_comm_unique_id", "orch_comm_create",
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
-    "orch_solve_hosting_host", "orch_nodewise",
+    "orch_solve_hosting_host", "orch_nodewise", "orch_rearrange", "orch_backbone_targets",
     "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
     "orch_window_destroy", "orch_dispatch_put", "orch_put",
 ]
@@ -312,6 +312,29 @@ class Context:
             self.h, C.c_int32(d), C.c_int64(len(length)), length.ctypes.data_as(C.c_void_p),
             origin.ctypes.data_as(C.c_void_p), C.c_int64(bound), C.byref(out), _stream()))
         return bool(out.value)
+
+    # ---- composed delivery
+    def rearrange(self, d, length, src_inst, src_slot, dst_inst, dst_slot, stream=None):
+        n = int(length.numel())
+        out = Balance.alloc(d, n, length.device)
+        b = out.struct()
+        _check(lib().orch_rearrange(self.h, C.c_int32(d), C.c_int64(n), _ptr(length),
+                                    _ptr(src_inst), _ptr(src_slot), _ptr(dst_inst),
+                                    _ptr(dst_slot), C.byref(b), _stream(stream)))
+        return out
+
+    def backbone_targets(self, d, llm: "Balance", part_offset, interleave_pos, item_part,
+                         stream=None):
+        E = part_offset.numel() - 1
+        n = item_part.numel()
+        di = torch.empty(max(n, 1), dtype=torch.int32, device=part_offset.device)
+        ds = torch.empty(max(n, 1), dtype=torch.int32, device=part_offset.device)
+        _check(lib().orch_backbone_targets(self.h, C.c_int32(d), C.c_int64(E), _ptr(llm.dest_inst),
+                                           _ptr(llm.bin_offset), _ptr(llm.bin_member),
+                                           _ptr(part_offset), _ptr(interleave_pos),
+                                           C.c_int64(interleave_pos.numel()), C.c_int64(n),
+                                           _ptr(item_part), _ptr(di), _ptr(ds), _stream(stream)))
+        return di[:n], ds[:n]
 
     # ---- node-wise hosting
     def solve_hosting(self, d, c, V):
