@@ -65,13 +65,6 @@ orch_cost_model policy_model(const orch_policy& p) {  // balancers.cpp:162-176
   return m;
 }
 
-size_t greedy_rounds_smem(int d) {
-  int p2 = 1;
-  while (p2 < d) p2 <<= 1;
-  if (p2 < 32) p2 = 32;
-  return 3 * sizeof(uint64_t) * p2 + sizeof(int32_t) * d;
-}
-
 // distribute_min_sum on [first, n) of the descending order.
 int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const uint32_t* xs,
                   const int32_t* order, const int64_t* init_load, const int32_t* init_count,
@@ -83,7 +76,7 @@ int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const u
                                       bc, bt, s);
     });
   } else if (d <= 512) {
-    const size_t sm = greedy_rounds_smem(d);
+    const size_t sm = rounds_smem_bytes<256>(d);
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_greedy_rounds<256>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     launch(ctx, [&] {
@@ -91,7 +84,7 @@ int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const u
                                                ds, doff, bc, bt, s);
     });
   } else {
-    const size_t sm = greedy_rounds_smem(d);
+    const size_t sm = rounds_smem_bytes<1024>(d);
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_greedy_rounds<1024>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     launch(ctx, [&] {
@@ -257,6 +250,14 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   plan.add(&starts, d + 2);
   plan.add(&n_groups, 1);
   plan.add(&bound, 1);
+  PadSearch* pads;
+  int32_t* pad_feas;
+  int64_t* pad_cand;
+  plan.add(&pads, 1);
+  plan.add(&pad_feas, kSMs);
+  plan.add(&pad_cand, kSMs);
+  uint16_t* pad_nx1;
+  plan.add(&pad_nx1, n <= kNxMax ? n : 1);
   // CUB temporary storage (max over the calls below)
   size_t cub_bytes = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, b, key_org, sorted_org, iota, ident_order, (int)nn, 0,
@@ -327,16 +328,48 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
     ORCH_CUDA_TRY(cudaMemsetAsync(asc_len + n, 0, sizeof(int64_t), st));
     tb = cub_bytes;
     ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, asc_len, asc_prefix, (int)n + 1, st));
-    constexpr int kPadSmemItems = 200 * 1024 / 4;
-    const int pad_items = n <= kPadSmemItems ? static_cast<int>(n) : 0;
-    const int pad_smem = pad_items * 4;
-    if (pad_smem > 48 * 1024)
+    const bool use_nx = n <= kNxMax;
+    const int nx_smem = static_cast<int>(n) * 2;
+    static bool pad_configured = false;
+    if (!pad_configured) {
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_pad_eval_nx, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kNxMax * 2));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_pad_starts_nx,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kNxMax * 2));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_padded_search,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, pad_smem));
-    launch(ctx, [&] {
-      k_padded_search<<<1, 1024, pad_smem, st>>>(d, n, xs, mode == 3 ? 1 : 0, probe, starts,
-                                                 n_groups, bound, S, pad_items);
-    });
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      pad_configured = true;
+    }
+    if (mode == 3) {  // one feasibility probe
+      if (use_nx) {
+        launch(ctx, [&] {
+          k_pad_eval_nx<<<1, 1024, nx_smem, st>>>(d, n, xs, pads, pad_feas, pad_cand, 1, probe,
+                                                  n_groups, S);
+        });
+      } else {
+        launch(ctx, [&] {
+          k_padded_search<<<1, 1024, 0, st>>>(d, n, xs, 1, probe, starts, n_groups, bound, S, 0);
+        });
+      }
+    } else {
+      launch(ctx, [&] { k_pad_init<<<1, 32, 0, st>>>(d, n, xs, pads, S); });
+      for (int r = 0; r < kPadRounds; ++r) {
+        launch(ctx, [&] {
+          if (use_nx)
+            k_pad_eval_nx<<<kSMs, 1024, nx_smem, st>>>(d, n, xs, pads, pad_feas, pad_cand, 0, 0,
+                                                       nullptr, S);
+          else
+            k_pad_eval_warp<<<kSMs, 32, 0, st>>>(d, n, xs, pads, pad_feas, pad_cand, S);
+        });
+      }
+      launch(ctx, [&] {
+        if (use_nx)
+          k_pad_starts_nx<<<1, 1024, nx_smem, st>>>(d, n, xs, pads, pad_nx1, starts, n_groups,
+                                                    bound, S);
+        else
+          k_pad_starts_warp<<<1, 32, 0, st>>>(d, n, xs, pads, starts, n_groups, bound, S);
+      });
+    }
     if (padded_only) {
       if (mode == 2 && d_bound_out)
         ORCH_CUDA_TRY(cudaMemcpyAsync(d_bound_out, bound, sizeof(int64_t),

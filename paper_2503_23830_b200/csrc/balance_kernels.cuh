@@ -4,6 +4,8 @@
 // non-FMA build.
 #pragma once
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -12,6 +14,9 @@ namespace orchb {
 namespace {  // internal linkage: included by several translation units
 
 constexpr uint64_t kU64Max = ~0ull;
+#ifndef ORCH_RSORT_BITS
+#define ORCH_RSORT_BITS 4
+#endif
 
 // Workspace flags shared by the pipeline kernels of one balance call.
 struct Flags {
@@ -213,6 +218,26 @@ __device__ void block_bitonic(uint64_t* U, int p) {
   }
 }
 
+template <int kThreads>
+struct RoundsSort {
+  static constexpr int kItems = (kThreads == 1024 ? 4096 : 512) / kThreads;
+  using Sort = cub::BlockRadixSort<uint32_t, kThreads, kItems, cub::NullType, ORCH_RSORT_BITS>;
+};
+
+// dynamic shared memory of k_greedy_rounds: S, T, U (p2 keys each), cnt[d],
+// then the block radix sort's temporary storage (16-byte aligned)
+__host__ __device__ inline size_t rounds_sort_offset(int d) {
+  int p2 = 1;
+  while (p2 < d) p2 <<= 1;
+  if (p2 < 32) p2 = 32;
+  const size_t base = 3 * sizeof(uint64_t) * p2 + sizeof(int32_t) * d;
+  return (base + 15) & ~size_t{15};
+}
+template <int kThreads>
+__host__ __device__ inline size_t rounds_smem_bytes(int d) {
+  return rounds_sort_offset(d) + sizeof(typename RoundsSort<kThreads>::Sort::TempStorage);
+}
+
 // ---------------------------------------------------------------- K4b
 // distribute_min_sum for any d <= ORCH_MAX_INSTANCES: exact round-batched
 // LPT. Bins are kept sorted by the packed key
@@ -239,6 +264,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* U = T + p2;                                  // [p2] updated keys
   int32_t* cnt = reinterpret_cast<int32_t*>(U + p2);     // [d]
   __shared__ int s_k;
+  __shared__ unsigned long long s_maxrel;
+  // The k updated keys of a round span a narrow load range above L_(0): as
+  // 32-bit (load - L_(0)) << ib | bin keys a block radix sort over only the
+  // needed bits replaces the 64-bit bitonic network (fallback when they do
+  // not fit).
+  using RSort = typename RoundsSort<kThreads>::Sort;
+  constexpr int kItems = RoundsSort<kThreads>::kItems;
+  typename RSort::TempStorage& rsort_tmp = *reinterpret_cast<typename RSort::TempStorage*>(
+      smem_raw + rounds_sort_offset(d));
   unsigned ib = 0;
   while ((1u << ib) < static_cast<unsigned>(d)) ++ib;
   if (ib == 0) ib = 1;
@@ -259,6 +293,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   int64_t next = d_first ? *d_first : 0;
   int64_t rounds = 0;
+#ifdef ORCH_ROUNDS_PROFILE
+  long long t_cond = 0, t_upd = 0, t_sort = 0, t_merge = 0, t_mark = clock64();
+#define RP_MARK(acc) do { if (tid == 0) { const long long t = clock64(); acc += t - t_mark; t_mark = t; } } while (0)
+#else
+#define RP_MARK(acc) do { } while (0)
+#endif
   while (next < n) {
     const int m = static_cast<int>(n - next < d ? n - next : d);
     if (tid == 0) s_k = m;
@@ -269,9 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!(Lr - L0 < static_cast<int64_t>(xs[next + r]))) atomicMin(&s_k, r);
     }
     __syncthreads();
+    RP_MARK(t_cond);
     const int k = s_k;  // >= 1: x_0 >= 1 > 0 = L_(0) - L_(0)
     int pk = 1;
     while (pk < k) pk <<= 1;
+    if (tid == 0) s_maxrel = 0;
+    __syncthreads();
     for (int r = tid; r < pk; r += kThreads) {
       if (r < k) {
         const uint64_t key = S[r];
@@ -283,12 +326,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         dest_slot[pos] = cnt[b]++;  // each bin appears once per round
         dst_off[pos] = L;
         U[r] = (static_cast<uint64_t>(L + x) << ib) | static_cast<uint64_t>(b);
+        atomicMax(&s_maxrel, static_cast<unsigned long long>(L + x - L0));
       } else {
         U[r] = kU64Max;
       }
     }
     __syncthreads();
-    block_bitonic<kThreads>(U, pk);
+    RP_MARK(t_upd);
+    const unsigned long long maxrel = s_maxrel;
+    const int rbits = maxrel ? 64 - __clzll(maxrel) : 1;
+    if (rbits + static_cast<int>(ib) <= 31 && pk <= kItems * kThreads && pk >= 64) {
+      uint32_t keys[kItems];
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        const int i = tid * kItems + j;
+        if (i < k) {
+          const uint64_t key = U[i];
+          keys[j] = static_cast<uint32_t>((((key >> ib) - static_cast<uint64_t>(L0)) << ib) |
+                                          (key & mask));
+        } else {
+          keys[j] = 0xffffffffu;  // above every real key (< 2^31)
+        }
+      }
+      RSort(rsort_tmp).Sort(keys, 0, rbits + static_cast<int>(ib));
+#pragma unroll
+      for (int j = 0; j < kItems; ++j) {
+        const int i = tid * kItems + j;
+        if (i < pk)
+          U[i] = keys[j] == 0xffffffffu
+                     ? kU64Max
+                     : ((((static_cast<uint64_t>(keys[j]) >> ib) + static_cast<uint64_t>(L0)) << ib) |
+                        (static_cast<uint64_t>(keys[j]) & mask));
+      }
+      __syncthreads();
+    } else {
+      block_bitonic<kThreads>(U, pk);
+    }
+    RP_MARK(t_sort);
     // merge U[0,k) with S[k,d) into T (keys are unique: distinct bin index)
     const int rest = d - k;
     for (int i = tid; i < d; i += kThreads) {
@@ -314,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       T[pos] = key;
     }
     __syncthreads();
+    RP_MARK(t_merge);
     uint64_t* tmp = S;  // T becomes the sorted bins (S[d..p2) and T[d..p2) stay MAX)
     S = T;
     T = tmp;
@@ -327,6 +402,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     bin_count[b] = cnt[b];
   }
   if (tid == 0) s->rounds = rounds;
+#ifdef ORCH_ROUNDS_PROFILE
+  if (tid == 0) printf("rounds=%lld cond=%lld upd=%lld sort=%lld merge=%lld (cycles)\n", (long long)rounds, t_cond, t_upd, t_sort, t_merge);
+#endif
 }
 
 // ---------------------------------------------------------------- K6
@@ -519,6 +597,279 @@ __global__ void __launch_bounds__(1024, 1)
       s->bound = bound;
     }
   }
+}
+
+// Multi-SM k-ary search (general path). Every round G = 148 CTAs evaluate G
+// candidate bounds, one per SM. A CTA does not walk the group chain warp-
+// serially (one galloping search per group, ~300 cycles each): it builds the
+// successor table nx[p] = next_start(p) for EVERY p in parallel (1024 threads,
+// coalesced gallops over a[]), squares it three times in place into
+// nx8 = next^8, and walks nx8 from 0 — d/8 shared-memory hops. Feasibility is
+// monotone in the bound, so the last CTA to finish narrows [lo, hi] (hi stays
+// feasible); the span shrinks ~G-fold per round and kPadRounds covers any
+// 2^56 span. Tables are u16 deltas (kNxFar = group of >= 65535 items: the
+// walker falls back to a galloping search there); n > kNxMax uses the
+// one-warp-per-candidate scan instead.
+constexpr int kPadRounds = 9;
+constexpr int kNxMax = 100 * 1024;  // u16 table in 200 KiB of shared memory
+constexpr uint16_t kNxFar = 0xFFFF;
+struct PadSearch {
+  int64_t lo, hi;
+  unsigned done;  // CTAs finished this round (last-block-done narrowing)
+};
+
+__global__ void k_pad_init(int d, int64_t n, const uint32_t* __restrict__ a, PadSearch* st,
+                           const orch_summary* s) {
+  if (pipeline_failed(s) || threadIdx.x != 0) return;
+  const int64_t max_len = a[n - 1];
+  st->lo = max_len;
+  st->hi = max_len * (n / d + 1);  // always feasible
+  st->done = 0;
+}
+
+// next_start for one thread: gallop then bisect on cond(t) = t >= n ||
+// (t - p + 1) * a[t] > b (monotone in t, cond(p) false).
+__device__ __forceinline__ int64_t thread_next_start(const uint32_t* __restrict__ a, int64_t n,
+                                                     int64_t p, int64_t b) {
+  int64_t lo = p, hi, k = 1;
+  for (;; k <<= 1) {
+    const int64_t t = p + k;
+    if (t >= n || (k + 1) * static_cast<int64_t>(__ldg(a + t)) > b) {
+      hi = t < n ? t : n;
+      break;
+    }
+    lo = t;
+  }
+  while (hi - lo > 1) {
+    const int64_t t = lo + ((hi - lo) >> 1);
+    if ((t - p + 1) * static_cast<int64_t>(__ldg(a + t)) > b) hi = t;
+    else lo = t;
+  }
+  return hi;
+}
+
+// nx (and optionally a global copy nx1) then nx8 in place. Phase 2 handles
+// ascending chunks of blockDim positions and reads only positions >= the
+// chunk start, which the chunk has not overwritten yet.
+__device__ void build_nx8(const uint32_t* __restrict__ a, int64_t n, int64_t b, uint16_t* nx,
+                          uint16_t* __restrict__ nx1) {
+  for (int64_t p = threadIdx.x; p < n; p += blockDim.x) {
+    const int64_t dl = thread_next_start(a, n, p, b) - p;
+    const uint16_t v = dl < kNxFar ? static_cast<uint16_t>(dl) : kNxFar;
+    nx[p] = v;
+    if (nx1) nx1[p] = v;
+  }
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < n; c0 += blockDim.x) {
+    const int64_t p = c0 + threadIdx.x;
+    uint16_t v = kNxFar;
+    if (p < n) {
+      int64_t q = p;
+      bool far = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (q < n) {
+          const uint16_t sv = nx[q];
+          if (sv == kNxFar) far = true;
+          if (!far) q += sv;
+        }
+      }
+      const int64_t dl = q - p;
+      if (!far && dl < kNxFar) v = static_cast<uint16_t>(dl);
+    }
+    __syncthreads();
+    if (p < n) nx[p] = v;
+    __syncthreads();
+  }
+}
+
+// Warp 0: group count at bound b by nx8 hops (8 full groups each) plus single
+// galloping steps where a hop is far or would reach n. Stops once > d.
+// heads/starts (optional): records each group start and the indices g of the
+// 8-hop heads, for the parallel fill in k_pad_starts2.
+__device__ int warp_walk_nx8(const uint32_t* __restrict__ a, int64_t n, int d, int64_t b,
+                             const uint16_t* nx8, int lane, int64_t* __restrict__ starts,
+                             int32_t* heads, int* n_heads) {
+  int64_t p = 0;
+  int g = 0, m = 0;
+  while (p < n) {
+    const uint16_t v = nx8[p];
+    if (starts && lane == 0) starts[g] = p;
+    if (v != kNxFar && p + v < n) {
+      if (heads && lane == 0) heads[m] = g;
+      ++m;
+      g += 8;
+      p += v;
+    } else {
+      g += 1;
+      p = warp_next_start(a, n, p, b, lane);
+    }
+    if (g > d && !starts) return g;
+  }
+  if (n_heads) *n_heads = m;
+  return g;
+}
+
+// Last CTA of the round: lanes of warp 0 reduce min feasible / max infeasible.
+__device__ void pad_narrow_last(PadSearch* st, const int32_t* feas, const int64_t* cand, int G,
+                                int64_t lo, int64_t hi) {
+  __shared__ unsigned s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&st->done, 1u) == static_cast<unsigned>(G - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
+  __threadfence();
+  int64_t nhi = hi, mx = lo - 1;
+  for (int w = threadIdx.x; w < G; w += 32) {
+    const int64_t c = __ldcg(cand + w);
+    if (c >= hi) continue;
+    if (__ldcg(feas + w)) nhi = c < nhi ? c : nhi;
+    else mx = c > mx ? c : mx;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t h2 = __shfl_xor_sync(~0u, nhi, o), m2 = __shfl_xor_sync(~0u, mx, o);
+    nhi = h2 < nhi ? h2 : nhi;
+    mx = m2 > mx ? m2 : mx;
+  }
+  if (threadIdx.x == 0) {
+    const int64_t nlo = mx + 1 > lo ? mx + 1 : lo;
+    st->hi = nhi;
+    st->lo = nlo < nhi ? nlo : nhi;
+    st->done = 0;
+  }
+}
+
+__device__ __forceinline__ int64_t pad_candidate(int64_t lo, int64_t hi, int G, int b) {
+  const int64_t span = hi - lo;
+  return span <= G ? lo + b : lo + (span / G) * b + ((span % G) * b) / G;
+}
+
+// One CTA (1024 threads) per candidate; mode 1 = feasibility of `probe` only.
+__global__ void __launch_bounds__(1024, 1)
+    k_pad_eval_nx(int d, int64_t n, const uint32_t* __restrict__ a, PadSearch* st,
+                  int32_t* __restrict__ feas, int64_t* __restrict__ cand, int mode, int64_t probe,
+                  int32_t* __restrict__ probe_out, const orch_summary* s) {
+  if (pipeline_failed(s)) return;
+  extern __shared__ __align__(16) uint16_t nx[];
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0);
+  if (mode == 1) {
+    const bool ok = probe >= static_cast<int64_t>(a[n - 1]);
+    if (ok) build_nx8(a, n, probe, nx, nullptr);
+    if (warp == 0) {
+      const bool f = ok && warp_walk_nx8(a, n, d, probe, nx, lane, nullptr, nullptr, nullptr) <= d;
+      if (lane == 0) *probe_out = f ? 1 : 0;
+    }
+    return;
+  }
+  const int64_t lo = st->lo, hi = st->hi;
+  if (lo >= hi) return;
+  const int G = gridDim.x;
+  const int64_t c = pad_candidate(lo, hi, G, blockIdx.x);
+  if (c < hi) {
+    build_nx8(a, n, c, nx, nullptr);
+    if (warp == 0) {
+      const bool f = warp_walk_nx8(a, n, d, c, nx, lane, nullptr, nullptr, nullptr) <= d;
+      if (lane == 0) {
+        feas[blockIdx.x] = f;
+        cand[blockIdx.x] = c;
+      }
+    }
+  } else if (threadIdx.x == 0) {
+    cand[blockIdx.x] = hi;  // not a candidate this round
+  }
+  pad_narrow_last(st, feas, cand, G, lo, hi);
+}
+
+// Group starts at the minimal bound: warp 0 walks nx8 recording every start
+// it visits and the 8-hop heads; then all threads fill the 7 starts inside
+// each hop from the single-step table nx1 in parallel.
+__global__ void __launch_bounds__(1024, 1)
+    k_pad_starts_nx(int d, int64_t n, const uint32_t* __restrict__ a, const PadSearch* st,
+                    uint16_t* __restrict__ nx1, int64_t* __restrict__ starts,
+                    int32_t* __restrict__ n_groups, int64_t* __restrict__ out_bound,
+                    orch_summary* s) {
+  if (pipeline_failed(s)) return;
+  extern __shared__ __align__(16) uint16_t nx[];
+  __shared__ int32_t heads[ORCH_MAX_INSTANCES / 8 + 2];
+  __shared__ int s_m, s_g;
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0);
+  const int64_t bound = st->hi;
+  build_nx8(a, n, bound, nx, nx1);
+  __threadfence_block();
+  if (warp == 0) {
+    int m = 0;
+    const int g = warp_walk_nx8(a, n, d, bound, nx, lane, starts, heads, &m);
+    if (lane == 0) {
+      s_m = m;
+      s_g = g;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < s_m; i += blockDim.x) {
+    const int g0 = heads[i];
+    int64_t p = starts[g0];
+    for (int j = 1; j < 8; ++j) {
+      const uint16_t v = nx1[p];
+      p = v == kNxFar ? thread_next_start(a, n, p, bound) : p + v;
+      starts[g0 + j] = p;
+    }
+  }
+  if (threadIdx.x == 0) {
+    starts[s_g] = n;
+    *n_groups = s_g;
+    *out_bound = bound;
+    s->bound = bound;
+  }
+}
+
+// Fallbacks for n > kNxMax: one warp per candidate walks the chain serially.
+__global__ void __launch_bounds__(32)
+    k_pad_starts_warp(int d, int64_t n, const uint32_t* __restrict__ a, const PadSearch* st,
+                      int64_t* __restrict__ starts, int32_t* __restrict__ n_groups,
+                      int64_t* __restrict__ out_bound, orch_summary* s) {
+  if (pipeline_failed(s)) return;
+  const int lane = threadIdx.x;
+  const int64_t bound = st->hi;
+  int64_t p = 0;
+  int g = 0;
+  while (p < n) {
+    if (lane == 0) starts[g] = p;
+    ++g;
+    p = warp_next_start(a, n, p, bound, lane);
+  }
+  if (lane == 0) {
+    starts[g] = n;
+    *n_groups = g;
+    *out_bound = bound;
+    s->bound = bound;
+  }
+}
+
+__global__ void __launch_bounds__(32)
+    k_pad_eval_warp(int d, int64_t n, const uint32_t* __restrict__ a, PadSearch* st,
+                    int32_t* __restrict__ feas, int64_t* __restrict__ cand,
+                    const orch_summary* s) {
+  if (pipeline_failed(s)) return;
+  const int64_t lo = st->lo, hi = st->hi;
+  if (lo >= hi) return;
+  const int G = gridDim.x, lane = threadIdx.x;
+  const int64_t c = pad_candidate(lo, hi, G, blockIdx.x);
+  if (c < hi) {
+    const bool f = warp_feasible(a, n, d, c, lane);
+    if (lane == 0) {
+      feas[blockIdx.x] = f;
+      cand[blockIdx.x] = c;
+    }
+  } else if (lane == 0) {
+    cand[blockIdx.x] = hi;
+  }
+  pad_narrow_last(st, feas, cand, G, lo, hi);
 }
 
 // Item placement from group starts: group g -> bin g (balancers.cpp:203-206),

@@ -207,6 +207,31 @@ def test_padded_bound_functions(ctx, oracle):
         assert ctx.padded_bound_feasible(d, L, O, int(L.max()) * (n // d + 1))
 
 
+def test_padded_search_paths(ctx, oracle):
+    """BinaryPadded on the general path: the successor-table search (n <= 100K),
+    groups of >= 65535 items (the table's far marker), and the one-warp-per-
+    candidate scan for n > 100K; bounds checked against the oracle's bisection."""
+    rng = np.random.default_rng(65535)
+    cases = [
+        (300, rng.integers(1, 5000, 50000)),           # table path, ~170 items/group
+        (1, np.ones(70000, np.int64)),                   # one group of 70000 (far)
+        (3, np.concatenate([np.ones(90000, np.int64), rng.integers(1, 9, 50)])),
+        (2560, rng.integers(64, 4097, 99999)),           # C4-like, just under the table cap
+        (1000, rng.integers(1, 3000, 120001)),           # warp scan, n > 100K
+        (2, np.ones(150000, np.int64)),                  # warp scan with huge groups
+    ]
+    for d, length in cases:
+        length = np.asarray(length, np.int64)
+        n = len(length)
+        origin = (np.arange(n) % d).astype(np.int32)
+        run_case(ctx, oracle, 1, d, length, origin)
+        if n <= 100000:
+            b = ctx.min_feasible_padded_bound(d, length, origin)
+            assert b == oracle.min_feasible_padded_bound(d, length, origin)
+            assert ctx.padded_bound_feasible(d, length, origin, b)
+            assert not ctx.padded_bound_feasible(d, length, origin, b - 1)
+
+
 def test_pre_post_stats(ctx, oracle):
     rng = np.random.default_rng(13)
     for kind in KINDS:
