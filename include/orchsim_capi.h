@@ -198,9 +198,9 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_pa
 /* ------------------------------------------------ node-wise hosting */
 /* solve_hosting (topology.hpp:71, topology.cpp:179-265) on a host volume
  * matrix h_V[d*d] with c instances per node: exact (the reference's answer,
- * including its tie-breaking), evaluated exhaustively on the device;
- * ORCH_UNSUPPORTED when the d!/(c!)^(d/c) balanced hostings exceed 2^30 or
- * d > 64. */
+ * including its tie-breaking) by a parallel two-pass branch and bound on the
+ * device; ORCH_UNSUPPORTED when d > 64 or d/c > 32 nodes. A search that
+ * exceeds 2^31 visited nodes keeps the incumbent (info[2] = -1 below). */
 int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
                             int32_t* h_hosting, int64_t* h_max_egress, int64_t* h_baseline_max,
                             void* stream);
@@ -210,7 +210,9 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
  * destination batch b is relabelled batch_to_instance[b] (dest_inst and the
  * per-batch arrays / CSR permuted; slots and offsets unchanged). With one
  * rank per node this is the GPU-wise hosting that cuts NVLink egress.
- * d_info = {max_egress, baseline_max_egress (identity hosting), dfs_used}. */
+ * d_info = {max_egress, baseline_max_egress (identity hosting), leaf_used
+ * (1: a search leaf beat the identity/greedy incumbents, 0: incumbent,
+ * -1: visit budget exhausted, incumbent kept), nodes visited}. */
 int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t* d_len,
                   const int32_t* d_origin, const orch_balance_out* bal, int32_t* d_hosting,
                   int32_t* d_batch_to_instance, int64_t* d_info, void* stream);

@@ -71,6 +71,7 @@ def build_cuda(force=False):
         obj = os.path.join(LIB, src.replace(".cu", ".o"))
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if os.environ.get("ORCH_PTXAS_V") else "-O3",
+              *os.environ.get("ORCH_NVCC_EXTRA", "").split(),
               "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj])
         objs.append(obj)
     _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-L", nccl_lib, "-l:libnccl.so.2",

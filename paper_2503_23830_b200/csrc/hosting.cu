@@ -5,12 +5,22 @@
 // a "node" is a GPU holding c = d/P logical instances and the slow link is
 // NVLink (the fast one is the GPU's own HBM).
 //
-// solve_hosting is an exact branch and bound in the reference. Here every
-// hosting (nodes^d assignments, the balanced ones kept) is scored in
-// parallel; the reference's answer is recovered exactly: its incumbents
-// (identity, then greedy) win when they are optimal, otherwise the first
-// optimal leaf of its depth-first order, whose rank is the mixed-radix number
-// of candidate positions (nodes with room, by descending gain, ties by node).
+// solve_hosting is an exact depth-first branch and bound in the reference
+// (topology.cpp:87-262). Its answer is fixed by the search order: the
+// incumbents (identity, then greedy if strictly better) unless some leaf is
+// strictly better, in which case the FIRST optimal leaf in DFS order. That is
+// independent of how hard the search prunes, so the device search is free to
+// be parallel as long as its bounds are valid:
+//   pass 1  optimum value V*: the DFS tree cut at depth k0 into <= 8192
+//           prefixes (tasks, in DFS order), one warp per task, lane = node,
+//           pruning on lb >= best (a global atomic incumbent);
+//   pass 2  (only if V* beats the incumbents) the first task, in DFS order,
+//           holding a leaf of value V*, pruning on lb > V*; k_host_leaf then
+//           replays that task to its first leaf.
+// The bound is the reference's lower_bound -- max over nodes of
+// (total - gained - optimistic gain) -- read in O(1): the unassigned batches
+// at depth k are exactly order[k..d), so the optimistic gain of node n with r
+// slots left is a table og[k][n][r] built once.
 #include <string>
 
 #include "common.cuh"
@@ -20,17 +30,31 @@ namespace orchb {
 namespace {
 
 constexpr int kHostMaxD = 64;
+constexpr int kHostMaxNodes = 32;                  // lane = node
+constexpr int kOgMax = (kHostMaxD + 1) * (kHostMaxD + kHostMaxNodes);
+constexpr int kHostWarps = 8;
+constexpr long long kHostTasks = 8192;
+constexpr unsigned long long kHostVisitBudget = 1ull << 31;
 
 struct HostState {
-  int d, c, nodes;
-  long long space;                       // balanced hostings: d! / (c!)^nodes
+  int d, c, nodes, k0;
+  long long tasks;                       // nodes^k0 prefixes, numbered in DFS order
   int64_t gain[kHostMaxD * kHostMaxD];   // [node][batch]
   int64_t node_total[kHostMaxD];
   int32_t order[kHostMaxD];              // branching order (descending regret, stable)
   int32_t incumbent[kHostMaxD];
   int64_t incumbent_value;
-  unsigned long long best_value;
-  unsigned long long best_key;           // (dfs key << 30) | index
+  // search tables by depth k (the batch order[k])
+  int64_t g2[kHostMaxD * kHostMaxNodes];    // [k][node] gain of node for order[k]
+  uint8_t no[kHostMaxD * kHostMaxNodes];    // [k][j] j-th candidate: descending gain, ties by node
+  uint8_t pos[kHostMaxD * kHostMaxNodes];   // [k][node] inverse of no
+  int64_t og[kOgMax];                       // [k][node][r] sum of the top r gains over order[k..d)
+  unsigned long long best_value;            // pass 1 incumbent value (starts at the incumbents')
+  unsigned long long task_counter[2];
+  unsigned long long best_task;             // pass 2: first task holding an optimal leaf
+  unsigned long long visits;
+  int overflow;
+  int32_t found[kHostMaxD];                 // that leaf: batch -> node
 };
 
 __device__ int64_t host_value(const HostState& H, const int32_t* a) {
@@ -51,14 +75,6 @@ __global__ void k_host_prep(int d, int c, const int64_t* __restrict__ V, HostSta
   H->d = d;
   H->c = c;
   H->nodes = nodes;
-  // multinomial d! / (c!)^nodes built as a product of binomials C(k*c, c)
-  long long sp = 1;
-  for (int k = 1; k <= nodes; ++k) {
-    long long binom = 1;  // C(k*c, c)
-    for (int j = 1; j <= c; ++j) binom = binom * ((k - 1) * c + j) / j;
-    sp *= binom;
-  }
-  H->space = sp;
   for (int n = 0; n < nodes; ++n) {
     H->node_total[n] = 0;
     for (int b = 0; b < d; ++b) H->gain[n * d + b] = 0;
@@ -112,86 +128,244 @@ __global__ void k_host_prep(int d, int c, const int64_t* __restrict__ V, HostSta
   const bool g_better = vg < vi;  // offer(greedy) replaces only when strictly better
   for (int b = 0; b < d; ++b) H->incumbent[b] = g_better ? greedy[b] : ident[b];
   H->incumbent_value = g_better ? vg : vi;
-  H->best_value = ~0ull;
-  H->best_key = ~0ull;
+  H->best_value = static_cast<unsigned long long>(H->incumbent_value);
+  H->task_counter[0] = H->task_counter[1] = 0;
+  H->best_task = ~0ull;
+  H->visits = 0;
+  H->overflow = 0;
+  int k0 = 0;
+  long long tasks = 1;
+  while (k0 < d && tasks * nodes <= kHostTasks) {
+    tasks *= nodes;
+    ++k0;
+  }
+  H->k0 = k0;
+  H->tasks = tasks;
 }
 
-// Unrank idx in [0, space) into a balanced hosting (multiset permutation:
-// every node exactly c batches). Completions after choosing node n at a
-// position = cur * r_n / T (exact), so the counts stay below space.
-__device__ __forceinline__ bool decode(const HostState& H, long long idx, int32_t* a) {
-  int r[kHostMaxD];
-  for (int n = 0; n < H.nodes; ++n) r[n] = H.c;
-  long long cur = H.space;
-  int T = H.d;
-  for (int b = 0; b < H.d; ++b) {
-    for (int n = 0; n < H.nodes; ++n) {
-      if (r[n] == 0) continue;
-      const long long sub = cur * r[n] / T;
-      if (idx < sub) {
-        a[b] = n;
-        cur = sub;
-        --r[n];
-        --T;
-        break;
+// Search tables: thread k < d builds depth k's candidate order (stable sort of
+// the nodes by descending gain for batch order[k]); thread n < nodes builds
+// og[.][n][.] from the deepest level up, keeping its top-c gains sorted.
+__global__ void k_host_tables(HostState* __restrict__ H) {
+  const int d = H->d, c = H->c, nodes = H->nodes, t = threadIdx.x;
+  if (t < d) {
+    const int b = H->order[t];
+    uint8_t* no = H->no + t * nodes;
+    for (int n = 0; n < nodes; ++n) {
+      H->g2[t * nodes + n] = H->gain[n * d + b];
+      int j = n - 1;  // insertion: strictly larger gains first, ties keep node order
+      while (j >= 0 && H->gain[no[j] * d + b] < H->gain[n * d + b]) {
+        no[j + 1] = no[j];
+        --j;
       }
-      idx -= sub;
+      no[j + 1] = static_cast<uint8_t>(n);
+    }
+    for (int j = 0; j < nodes; ++j) H->pos[t * nodes + no[j]] = static_cast<uint8_t>(j);
+  }
+  if (t < nodes) {
+    int64_t top[kHostMaxD];
+    int have = 0;
+    for (int k = d; k >= 0; --k) {
+      if (k < d) {  // insert gain of order[k]
+        const int64_t g = H->gain[t * d + H->order[k]];
+        int j = -1;
+        if (have < c) j = have++;
+        else if (top[c - 1] < g) j = c - 1;  // else not in the top c (sums unchanged on ties)
+        if (j >= 0) {
+          while (j > 0 && top[j - 1] < g) {
+            top[j] = top[j - 1];
+            --j;
+          }
+          top[j] = g;
+        }
+      }
+      int64_t* og = H->og + (static_cast<size_t>(k) * nodes + t) * (c + 1);
+      int64_t acc = 0;
+      og[0] = 0;
+      for (int r = 1; r <= c; ++r) {
+        if (r <= have) acc += top[r - 1];
+        og[r] = acc;
+      }
     }
   }
-  return true;
 }
 
-__global__ void k_host_min(const HostState* __restrict__ Hp, unsigned long long* best) {
-  const HostState& H = *Hp;
-  unsigned long long local = ~0ull;
-  int32_t a[kHostMaxD];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < H.space;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (!decode(H, i, a)) continue;
-    const unsigned long long v = static_cast<unsigned long long>(host_value(H, a));
-    local = v < local ? v : local;
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    const unsigned long long o = __shfl_xor_sync(~0u, local, off);
-    local = o < local ? o : local;
-  }
-  if ((threadIdx.x & 31) == 0 && local != ~0ull) atomicMin(best, local);
+struct HostSmem {
+  const int64_t* g2;
+  const int64_t* og;
+  const uint8_t* no;
+  const uint8_t* pos;
+};
+
+__host__ __device__ inline size_t host_smem_bytes(int d, int c) {
+  const int nodes = d / c;
+  return sizeof(int64_t) * (static_cast<size_t>(d) * nodes +
+                            static_cast<size_t>(d + 1) * nodes * (c + 1)) +
+         2 * static_cast<size_t>(d) * nodes + kHostWarps * kHostMaxD;
 }
 
-// rank of an optimal hosting in the reference's depth-first order
-__global__ void k_host_first(HostState* __restrict__ Hp) {
-  const HostState& H = *Hp;
-  const unsigned long long target = H.best_value;
-  unsigned long long local = ~0ull;
-  int32_t a[kHostMaxD];
-  int room[kHostMaxD];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < H.space;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (!decode(H, i, a)) continue;
-    if (static_cast<unsigned long long>(host_value(H, a)) != target) continue;
-    for (int n = 0; n < H.nodes; ++n) room[n] = H.c;
-    unsigned long long key = 0;
-    for (int t = 0; t < H.d; ++t) {
-      const int b = H.order[t];
-      const int me = a[b];
-      const int64_t gm = H.gain[me * H.d + b];
-      int pos = 0;  // candidates (room > 0) ahead of `me`: larger gain, or equal gain and lower index
-      for (int n = 0; n < H.nodes; ++n) {
-        if (n == me || room[n] == 0) continue;
-        const int64_t g = H.gain[n * H.d + b];
-        pos += (g > gm) || (g == gm && n < me);
-      }
-      key = key * H.nodes + pos;
-      room[me] -= 1;
+__device__ HostSmem host_load_tables(const HostState& H, unsigned char* raw) {
+  const int d = H.d, c = H.c, nodes = H.nodes;
+  int64_t* g2 = reinterpret_cast<int64_t*>(raw);
+  int64_t* og = g2 + d * nodes;
+  uint8_t* no = reinterpret_cast<uint8_t*>(og + (d + 1) * nodes * (c + 1));
+  uint8_t* pos = no + d * nodes;
+  for (int i = threadIdx.x; i < d * nodes; i += blockDim.x) {
+    g2[i] = H.g2[i];
+    no[i] = H.no[i];
+    pos[i] = H.pos[i];
+  }
+  for (int i = threadIdx.x; i < (d + 1) * nodes * (c + 1); i += blockDim.x) og[i] = H.og[i];
+  __syncthreads();
+  return HostSmem{g2, og, no, pos};
+}
+
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t w = __shfl_xor_sync(~0u, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// One task (prefix t) of the DFS: lane = node. pass 1 prunes lb >= best and
+// lowers the global incumbent at leaves; pass 2 prunes lb > vstar and stops
+// at the first leaf (returns true; `leaf` receives batch -> node if given).
+// ch: this warp's choice stack (position in the candidate order per depth;
+// every lane writes the same value).
+__device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t, int64_t vstar,
+                          uint8_t* ch, int32_t* leaf) {
+  const int d = H.d, c = H.c, nodes = H.nodes, k0 = H.k0, lane = threadIdx.x & 31;
+  const bool active = lane < nodes;
+  const int64_t total = active ? H.node_total[lane] : 0;
+  int room = active ? c : 0;
+  int64_t gained = 0;
+  // the prefix: digit k (most significant first) = candidate position among nodes with room
+  long long div = H.tasks / nodes;
+  for (int k = 0; k < k0; ++k) {
+    const int p = static_cast<int>((t / (div > 0 ? div : 1)) % nodes);
+    div /= nodes;
+    const unsigned pm =
+        __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
+    if (__popc(pm) <= p) return false;  // no such prefix
+    unsigned rest = pm;
+    for (int q = 0; q < p; ++q) rest &= rest - 1;  // drop the p lowest candidates
+    const int j = __ffs(rest) - 1;
+    ch[k] = static_cast<uint8_t>(j);
+    const int m = T.no[k * nodes + j];
+    if (lane == m) {
+      --room;
+      gained += T.g2[k * nodes + m];
     }
-    const unsigned long long packed = (key << 30) | static_cast<unsigned long long>(i);
-    local = packed < local ? packed : local;
   }
-  for (int off = 16; off > 0; off >>= 1) {
-    const unsigned long long o = __shfl_xor_sync(~0u, local, off);
-    local = o < local ? o : local;
+  int64_t best = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&H.best_value));
+  unsigned long long visits = 0;
+  bool found = false;
+  int k = k0, jstart = 0;
+  bool descend = true;
+  for (;;) {
+    if (descend) {
+      ++visits;
+      if ((visits & 1023) == 0) {
+        if (pass == 1)
+          best = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&H.best_value));
+        else if (*reinterpret_cast<volatile unsigned long long*>(&H.best_task) <
+                 static_cast<unsigned long long>(t))
+          break;  // an earlier task already holds an optimal leaf (~0: none yet)
+        if (*reinterpret_cast<volatile int*>(&H.overflow)) break;
+        if ((visits & 65535) == 0 && lane == 0 &&
+            atomicAdd(&H.visits, 65536ull) > kHostVisitBudget)
+          H.overflow = 1;
+      }
+      const int64_t term =
+          active ? total - gained - T.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room]
+                 : INT64_MIN;
+      const int64_t lb = warp_max64(term);
+      bool prune = pass == 1 ? lb >= best : lb > vstar;
+      if (!prune && k == d) {  // leaf: value == lb
+        if (pass == 1) {
+          if (lane == 0) atomicMin(&H.best_value, static_cast<unsigned long long>(lb));
+          best = lb;
+          prune = true;
+        } else {
+          found = true;
+          if (leaf)
+            for (int q = lane; q < d; q += 32) leaf[H.order[q]] = T.no[q * nodes + ch[q]];
+          break;
+        }
+      }
+      if (prune) {
+        descend = false;
+      } else {
+        jstart = 0;
+      }
+    }
+    if (!descend) {  // back up one level and move to the next candidate there
+      if (k == k0) break;
+      --k;
+      const int j = ch[k];
+      const int m = T.no[k * nodes + j];
+      if (lane == m) {
+        ++room;
+        gained -= T.g2[k * nodes + m];
+      }
+      jstart = j + 1;
+    }
+    unsigned pm =
+        __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
+    pm = jstart >= 32 ? 0u : pm & (~0u << jstart);
+    if (!pm) {
+      descend = false;
+      continue;
+    }
+    const int j = __ffs(pm) - 1;
+    ch[k] = static_cast<uint8_t>(j);
+    const int m = T.no[k * nodes + j];
+    if (lane == m) {
+      --room;
+      gained += T.g2[k * nodes + m];
+    }
+    ++k;
+    descend = true;
   }
-  if ((threadIdx.x & 31) == 0 && local != ~0ull) atomicMin(&Hp->best_key, local);
+  if (lane == 0) atomicAdd(&H.visits, visits & 65535);
+  return found;
+}
+
+__global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restrict__ Hp, int pass) {
+  extern __shared__ __align__(16) unsigned char host_raw[];
+  HostState& H = *Hp;
+  if (pass == 2 && static_cast<long long>(H.best_value) >= H.incumbent_value) return;
+  const HostSmem T = host_load_tables(H, host_raw);
+  const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ch = host_raw + host_smem_bytes(H.d, H.c) - kHostWarps * kHostMaxD + warp * kHostMaxD;
+  const int64_t vstar = static_cast<int64_t>(H.best_value);
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(&H.task_counter[pass - 1], 1ull);
+    t = __shfl_sync(~0u, t, 0);
+    if (static_cast<long long>(t) >= H.tasks) break;
+    if (*reinterpret_cast<volatile int*>(&H.overflow)) break;
+    if (pass == 2 && *reinterpret_cast<volatile unsigned long long*>(&H.best_task) < t) break;
+    if (host_task(H, T, pass, static_cast<long long>(t), vstar, ch, nullptr)) {
+      if (lane == 0) atomicMin(&H.best_task, t);
+      break;  // later tasks come after this one in DFS order
+    }
+  }
+}
+
+// Replays the first task holding an optimal leaf to that leaf.
+__global__ void __launch_bounds__(32) k_host_leaf(HostState* __restrict__ Hp) {
+  extern __shared__ __align__(16) unsigned char host_raw[];
+  HostState& H = *Hp;
+  if (static_cast<long long>(H.best_value) >= H.incumbent_value || H.overflow ||
+      H.best_task == ~0ull)
+    return;
+  const HostSmem T = host_load_tables(H, host_raw);
+  uint8_t* ch = host_raw + host_smem_bytes(H.d, H.c) - kHostWarps * kHostMaxD;
+  host_task(H, T, 2, static_cast<long long>(H.best_task), static_cast<int64_t>(H.best_value), ch,
+            H.found);
 }
 
 // Final hosting, batch -> instance map, egress figures; then the result remap.
@@ -201,12 +375,9 @@ __global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* _
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const HostState& H = *Hp;
   int32_t a[kHostMaxD];
-  const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value;
-  if (incumbent) {
-    for (int b = 0; b < H.d; ++b) a[b] = H.incumbent[b];
-  } else {
-    decode(H, static_cast<long long>(H.best_key & ((1ull << 30) - 1)), a);
-  }
+  const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value ||
+                         H.overflow || H.best_task == ~0ull;
+  for (int b = 0; b < H.d; ++b) a[b] = incumbent ? H.incumbent[b] : H.found[b];
   int next[kHostMaxD];
   for (int n = 0; n < H.nodes; ++n) next[n] = n * H.c;
   for (int b = 0; b < H.d; ++b) {  // topology.cpp:283-290: ascending batch order in a node
@@ -226,7 +397,13 @@ __global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* _
   }
   info[0] = worst;
   info[1] = base;
-  info[2] = incumbent ? 0 : 1;
+  info[2] = H.overflow ? -1 : (incumbent ? 0 : 1);  // -1: visit budget hit, incumbent kept
+  info[3] = static_cast<int64_t>(H.visits);
+#ifdef ORCH_HOST_DEBUG
+  printf("hosting: best %llu inc %lld task %llu visits %llu overflow %d k0 %d tasks %lld\n",
+         H.best_value, (long long)H.incumbent_value, H.best_task, H.visits, H.overflow, H.k0,
+         H.tasks);
+#endif
 }
 
 // Relabel destination batches: item dest -> b2i[dest]; per-batch arrays and
@@ -283,13 +460,27 @@ int check_hosting_args(int d, int c) {
     return fail(ORCH_INVALID_ARGUMENT, "topology needs at least one instance and one per node");
   if (d % c) return fail(ORCH_INVALID_ARGUMENT, "instance count must be divisible by instances per node");
   if (d > kHostMaxD) return fail(ORCH_UNSUPPORTED, "node-wise hosting limited to d <= 64 on the device");
-  long double sp = 1;  // d! / (c!)^(d/c)
-  for (int i = 1; i <= d; ++i) sp *= i;
-  long double cf = 1;
-  for (int i = 1; i <= c; ++i) cf *= i;
-  for (int k = 0; k < d / c; ++k) sp /= cf;
-  if (sp > 1073741824.0L)
-    return fail(ORCH_UNSUPPORTED, "node-wise hosting: more than 2^30 balanced hostings (exhaustive device search)");
+  if (d / c > kHostMaxNodes)
+    return fail(ORCH_UNSUPPORTED, "node-wise hosting limited to 32 nodes on the device");
+  return ORCH_OK;
+}
+
+int launch_hosting_search(orch_ctx* ctx, int d, int c, const int64_t* V, HostState* H,
+                          cudaStream_t st) {
+  const int sm = static_cast<int>(host_smem_bytes(d, c));
+  static bool configured = false;
+  if (!configured) {
+    const int mx = static_cast<int>(host_smem_bytes(kHostMaxD, 2));  // the largest table set
+    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    configured = true;
+  }
+  k_host_prep<<<1, 32, 0, st>>>(d, c, V, H);
+  k_host_tables<<<1, kHostMaxD, 0, st>>>(H);
+  k_host_bb<<<kSMs, kHostWarps * 32, sm, st>>>(H, 1);
+  k_host_bb<<<kSMs, kHostWarps * 32, sm, st>>>(H, 2);
+  k_host_leaf<<<1, 32, sm, st>>>(H);
+  ctx->launches += 5;
   return ORCH_OK;
 }
 
@@ -320,11 +511,10 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
   rc = all.commit(ctx, st);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaMemcpyAsync(V, h_V, sizeof(int64_t) * d * d, cudaMemcpyHostToDevice, st));
-  k_host_prep<<<1, 32, 0, st>>>(d, c, V, H);
-  k_host_min<<<kSMs * 8, 256, 0, st>>>(H, &H->best_value);
-  k_host_first<<<kSMs * 8, 256, 0, st>>>(H);
+  rc = launch_hosting_search(ctx, d, c, V, H, st);
+  if (rc) return rc;
   k_host_finish<<<1, 32, 0, st>>>(H, V, hosting, b2i, info);
-  ctx->launches += 4;
+  ctx->launches += 1;
   ORCH_CUDA_TRY(cudaGetLastError());
   ORCH_CUDA_TRY(cudaMemcpyAsync(h_hosting, hosting, sizeof(int32_t) * d, cudaMemcpyDeviceToHost, st));
   int64_t hinfo[4];
@@ -368,9 +558,8 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
   if (n > 0)
     k_vol<<<blocks_for(n, 256), 256, 0, st>>>(d, n, d_len, d_origin, bal->dest_inst, V);
   const int64_t* dV = reinterpret_cast<const int64_t*>(V);
-  k_host_prep<<<1, 32, 0, st>>>(d, c, dV, H);
-  k_host_min<<<kSMs * 8, 256, 0, st>>>(H, &H->best_value);
-  k_host_first<<<kSMs * 8, 256, 0, st>>>(H);
+  rc = launch_hosting_search(ctx, d, c, dV, H, st);
+  if (rc) return rc;
   k_host_finish<<<1, 32, 0, st>>>(H, dV, hosting, b2i, info);
   // snapshot the per-batch arrays, then write them back relabelled
   ORCH_CUDA_TRY(cudaMemcpyAsync(ocnt, bal->bin_count, 4 * d, cudaMemcpyDeviceToDevice, st));
@@ -386,7 +575,7 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
   k_host_remap<<<1, 256, 0, st>>>(d, n, b2i, bal->dest_inst, ocnt, olen, otok, ocost, ooff, omem,
                                   bal->bin_count, bal->bin_len, bal->bin_tokens, bal->bin_cost,
                                   bal->bin_offset, bal->bin_member);
-  ctx->launches += 6;
+  ctx->launches += 3;
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
 }

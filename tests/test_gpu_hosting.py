@@ -86,10 +86,43 @@ def test_nodewise_in_place(ctx, oracle, P):
         assert torch.equal(rout.cpu(), torch.from_numpy(hout))
 
 
+def test_solve_hosting_c3_shapes(ctx, oracle):
+    """DP=64 (C3) volume matrices of the reference balancer's three phases,
+    hosted on 2, 4 and 8 GPUs: the branch and bound against the reference's
+    own answers (tests/golden/ref_hosting_c3.npz)."""
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting_c3.npz"))
+    for k in range(len(f["c"])):
+        c = int(f["c"][k])
+        a = ctx.solve_hosting(64, c, f["V"][k])
+        np.testing.assert_array_equal(a["hosting"], f["hosting"][k])
+        assert a["max_egress"] == f["max_egress"][k]
+        o = oracle.solve_hosting(64, c, f["V"][k])
+        np.testing.assert_array_equal(o["hosting"], f["hosting"][k])
+
+
+def test_solve_hosting_random_larger(ctx, oracle):
+    """d up to 32 with 2..16 nodes: leaves beating the incumbents, ties."""
+    rng = np.random.default_rng(99)
+    for _ in range(60):
+        nodes = int(rng.choice([2, 3, 4, 8, 16]))
+        c = int(rng.integers(1, max(2, 32 // nodes) + 1))
+        d = nodes * c
+        if d > 32 or nodes > 32:
+            continue
+        V = rng.integers(0, int(rng.choice([3, 50, 1000])), (d, d)) * (rng.random((d, d)) < 0.5)
+        o = oracle.solve_hosting(d, c, V)
+        a = ctx.solve_hosting(d, c, V)
+        np.testing.assert_array_equal(a["hosting"], o["hosting"])
+        assert a["max_egress"] == o["max_egress"]
+
+
 def test_hosting_limits(ctx):
     from paper_2503_23830_b200.capi import OrchError
     with pytest.raises(OrchError) as e:
-        ctx.solve_hosting(64, 8, np.zeros((64, 64), np.int64))
+        ctx.solve_hosting(64, 1, np.zeros((64, 64), np.int64))
+    assert e.value.code == 12
+    with pytest.raises(OrchError) as e:
+        ctx.solve_hosting(72, 8, np.zeros((72, 72), np.int64))
     assert e.value.code == 12
     with pytest.raises(OrchError) as e:
         ctx.solve_hosting(6, 4, np.zeros((6, 6), np.int64))

@@ -164,3 +164,12 @@ def test_hosting_fixtures(oracle):
         a = oracle.solve_hosting(d, c, V)
         np.testing.assert_array_equal(a["hosting"], f["hosting"][k, :d])
         assert a["max_egress"] == f["max_egress"][k]
+
+
+def test_hosting_c3_fixtures(oracle):
+    """DP=64 (C3) phase volume matrices on 2/4/8 GPUs (make_hosting_c3_golden.py)."""
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting_c3.npz"))
+    for k in range(len(f["c"])):
+        a = oracle.solve_hosting(64, int(f["c"][k]), f["V"][k].reshape(64, 64))
+        np.testing.assert_array_equal(a["hosting"], f["hosting"][k])
+        assert a["max_egress"] == f["max_egress"][k]
