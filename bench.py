@@ -32,13 +32,23 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 METRIC = "balance+dispatch tokens/s at 1–8 B200; a2a GB/s vs NVLink; max/mean load"
-D_INST = 8
-PER_INSTANCE = 64
-SEED = 2
-ROW_BYTES = 8192  # bf16, d_model = 4096
-WORKLOAD = ("C2: DP=8 vision+text MCI batch (64 examples/instance, reference generator seed 2), "
-            "per-phase GreedyUnpadded rebalancing (vision metadata lengths, LLM interleaved "
-            "lengths, vision rate 4), bf16 d=4096 token rows (8 KiB)")
+LAM_LONG = 1.0 / (6 * 8192)  # attention vs dense FLOPs per token at d_model 8192
+CONFIGS = {
+    # the driver's bench line (BASELINE.json configs[1])
+    "C2": dict(d=8, per=64, seed=2, mix=2, R=8192,
+               workload="C2: DP=8 vision+text MCI batch (64 examples/instance, reference generator "
+                        "seed 2), per-phase GreedyUnpadded rebalancing (vision metadata lengths, LLM "
+                        "interleaved lengths, vision rate 4), bf16 d=4096 token rows (8 KiB)"),
+    # evidence lines (configs[2], configs[4]): python bench.py --config C3|C5
+    "C3": dict(d=64, per=64, seed=7, mix=3, R=16384,
+               workload="C3: DP=64 vision+audio+text MCI batch (64 examples/instance, seed 7): "
+                        "vision GreedyUnpadded, audio BinaryPadded, LLM GreedyUnpadded, bf16 "
+                        "d=8192 token rows (16 KiB)"),
+    "C5": dict(d=8, per=8, seed=5, mix=0, R=16384,
+               workload="C5: DP=8 long-context, 8 sequences/instance, lengths U[8192,32768], "
+                        "QuadraticTolerance (lambda=1/(6*8192), v=2048), bf16 d=8192 rows (16 KiB)"),
+}
+CFG = dict(CONFIGS["C2"], name="C2")
 
 
 def peaks():
@@ -106,11 +116,25 @@ class ClockSampler:
 
 
 def build_inputs():
+    """Phases of one step: (name, lengths, origins, policy kind, lambda, v)."""
     from paper_2503_23830_b200 import workload
-    b = workload.make_batch(2, D_INST, PER_INSTANCE, SEED)
+    d = CFG["d"]
+    if CFG["mix"] == 0:  # long context (C5)
+        rng = np.random.default_rng(CFG["seed"])
+        n = d * CFG["per"]
+        L = rng.integers(8192, 32769, n).astype(np.int64)
+        O = (np.arange(n) % d).astype(np.int32)
+        return None, [("llm", L, O, 2, LAM_LONG, 2048)]
+    b = workload.make_batch(CFG["mix"], d, CFG["per"], CFG["seed"])
+    phases = []
     lv, ov, _ = b.phase_items("vision")
+    phases.append(("vision", lv, ov, 0, 0.0, 0))
+    if CFG["mix"] == 3:
+        la, oa, _ = b.phase_items("audio")
+        phases.append(("audio", la, oa, 1, 0.0, 0))
     ll, ol = b.llm_items()
-    return b, [("vision", lv, ov), ("llm", ll, ol)]
+    phases.append(("llm", ll, ol, 0, 0.0, 0))
+    return b, phases
 
 
 # --------------------------------------------------------------- reference arm
@@ -119,15 +143,16 @@ def cpu_reference_step(phases, nthreads, ref, oracle, bufs):
     restatement when _ref was not built) + threaded host memcpy dispatch
     restating apply() on token rows."""
     t0 = time.perf_counter()
-    for (name, L, O), (ins, outs) in zip(phases, bufs):
+    d, R = CFG["d"], CFG["R"]
+    for (name, L, O, kind, lam, v), (ins, outs) in zip(phases, bufs):
         if ref is not None:
-            di, ds, _, _ = ref.balance(0, D_INST, L, O)
+            di, ds, _, _ = ref.balance(kind, d, L, O, lam=lam, v=v)
         else:
-            r = oracle.balance(0, D_INST, L, O)
+            r = oracle.balance(kind, d, L, O, lam=lam, v=v)
             di, ds = r.dest_inst, r.dest_slot
-        lay = oracle.layout(D_INST, 1, L, O, di, ds)
-        oracle.dispatch_rows(D_INST, 1, L, O, di, lay["rank_src_off"], lay["rank_dst_off"],
-                             ROW_BYTES, ins, outs, nthreads)
+        lay = oracle.layout(d, 1, L, O, di, ds)
+        oracle.dispatch_rows(d, 1, L, O, di, lay["rank_src_off"], lay["rank_dst_off"],
+                             R, ins, outs, nthreads)
     return time.perf_counter() - t0
 
 
@@ -138,13 +163,13 @@ def cpu_arm(phases, steps, warmup):
     kind = "reference" if ref is not None else "port"
     nthreads = os.cpu_count() or 1
     bufs = []
-    for name, L, O in phases:
-        rows = int(L.sum())
-        bufs.append(([np.ones(rows * ROW_BYTES, np.uint8)], [np.empty(rows * ROW_BYTES, np.uint8)]))
+    for ph in phases:
+        rows = int(ph[1].sum())
+        bufs.append(([np.ones(rows * CFG["R"], np.uint8)], [np.empty(rows * CFG["R"], np.uint8)]))
     for _ in range(warmup):
         cpu_reference_step(phases, nthreads, ref, oracle, bufs)
     times = [cpu_reference_step(phases, nthreads, ref, oracle, bufs) for _ in range(steps)]
-    tokens = sum(int(L.sum()) for _, L, _ in phases)
+    tokens = sum(int(ph[1].sum()) for ph in phases)
     return times, tokens, kind, nthreads
 
 
@@ -162,10 +187,10 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": D_INST * PER_INSTANCE,
-                   "dp_instances": D_INST, "row_bytes": ROW_BYTES, "tokens_per_step": tokens},
+        "config": {"workload": CFG["workload"], "global_batch": CFG["d"] * CFG["per"],
+                   "dp_instances": CFG["d"], "row_bytes": CFG["R"], "tokens_per_step": tokens},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": kind,
-                         "sample": f"full C2 step x{steps}: reference balance() per phase "
+                         "sample": f"full {CFG['name']} step x{steps}: reference balance() per phase "
                                    f"(single thread) + {nthreads}-thread host memcpy dispatch"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -185,8 +210,9 @@ def run_b200(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    D_INST = CFG["d"]
     if D_INST % world:
-        raise SystemExit("N must divide the 8 DP instances")
+        raise SystemExit(f"N must divide the {D_INST} DP instances")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm_meta = comm_data = None
@@ -200,7 +226,7 @@ def run_b200(args):
         comm_data = Comm(world, rank, uid[0][1])
     # one context (workspace arena) per stream
     ctx_meta, ctx_data = Context(local), Context(local)
-    P, c, R = world, D_INST // world, ROW_BYTES
+    P, c, R = world, D_INST // world, CFG["R"]
     batch, phases = build_inputs()
     meta_stream = torch.cuda.Stream(device=dev)
     data_stream = torch.cuda.Stream(device=dev)
@@ -210,11 +236,11 @@ def run_b200(args):
     # on the metadata stream while step i's rows move on the data stream (the
     # paper overlaps the solver with the forward pass).
     st = []
-    for name, L, O in phases:
+    for name, L, O, kind, lam, v in phases:
         n = len(L)
         mine = np.nonzero(O // c == rank)[0]
         max_local = int(max(np.bincount(O // c, minlength=P)))
-        s = dict(name=name, n=n, L=L, O=O, max_local=max_local,
+        s = dict(name=name, n=n, L=L, O=O, kind=kind, lam=lam, v=v, max_local=max_local,
                  h_pos=torch.from_numpy(mine.astype(np.int64)).pin_memory(),
                  h_len=torch.from_numpy(L[mine]).pin_memory(),
                  h_org=torch.from_numpy(O[mine]).pin_memory(),
@@ -233,7 +259,8 @@ def run_b200(args):
         if comm_meta is not None:
             ctx_meta.allgather_items(comm_meta, s["pos"], s["llen"], s["lorg"], s["max_local"],
                                      s["n"], B["glen"], B["gorg"], stream=stream)
-        ctx_meta.balance(0, D_INST, B["glen"], B["gorg"], out=B["bal"], stream=stream)
+        ctx_meta.balance(s["kind"], D_INST, B["glen"], B["gorg"], lam=s["lam"], v=s["v"],
+                         out=B["bal"], stream=stream)
         if P > 1 and args.nodewise:  # GPU-wise hosting (orchestrator.cpp:283 with node = GPU)
             ctx_meta.nodewise(D_INST, c, B["glen"], B["gorg"], B["bal"], stream=stream)
         ctx_meta.layout(D_INST, P, B["glen"], B["gorg"], B["bal"], out=B["lay"], stream=stream)
@@ -243,15 +270,16 @@ def run_b200(args):
         for B in s["buf"]:
             meta(s, B, torch.cuda.current_stream())
     torch.cuda.synchronize()
+    # Input rows and the NCCL staging buffers are shared by the phases (they
+    # run one after another on the data stream); each phase has its own output.
     for s in st:
         lay = s["buf"][0]["lay"]
-        in_rows = int(lay.in_rows[rank].item())
+        s["in_rows"] = int(lay.in_rows[rank].item())
         out_rows = int(lay.out_rows[rank].item())
         S = lay.send_rows.cpu().numpy().reshape(P, P)
         s["moved_rows"] = out_rows  # every row of this rank's output is written once
         s["send_rows"] = int(S[rank].sum() - S[rank, rank])
         s["recv_rows"] = int(S[:, rank].sum() - S[rank, rank])
-        s["rin"] = torch.randint(0, 255, (max(in_rows, 1) * R,), dtype=torch.uint8, device=dev)
         s["win"] = None
         if P > 1 and args.exchange == "put":
             wrows = int(lay.out_rows.max().item())
@@ -259,10 +287,17 @@ def run_b200(args):
             s["rout"] = s["win"].tensor_view(dev)
         else:
             s["rout"] = torch.empty(max(out_rows, 1) * R, dtype=torch.uint8, device=dev)
-        s["send"] = torch.empty(max(s["send_rows"], 1) * R, dtype=torch.uint8, device=dev) \
-            if P > 1 else None
-        s["recv"] = torch.empty(max(s["recv_rows"], 1) * R, dtype=torch.uint8, device=dev) \
-            if P > 1 else None
+    rin = torch.randint(0, 255, (max(max(s["in_rows"] for s in st), 1) * R,), dtype=torch.uint8,
+                        device=dev)
+    send = recv = None
+    if P > 1:
+        send = torch.empty(max(max(s["send_rows"] for s in st), 1) * R, dtype=torch.uint8,
+                           device=dev)
+        recv = torch.empty(max(max(s["recv_rows"] for s in st), 1) * R, dtype=torch.uint8,
+                           device=dev)
+    for s in st:
+        s["rin"] = rin[:max(s["in_rows"], 1) * R]
+        s["send"], s["recv"] = send, recv
 
     disp_events = []
     counter = [0]
@@ -396,7 +431,7 @@ def run_b200(args):
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "global_batch": D_INST * PER_INSTANCE,
+        "config": {"workload": CFG["workload"], "global_batch": D_INST * CFG["per"],
                    "dp_instances": D_INST, "instances_per_gpu": c, "row_bytes": R,
                    "tokens_per_step": tokens, "seqs_per_step": seqs,
                    "l2": f"row buffers {tokens * R / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"},
@@ -426,13 +461,17 @@ def run_b200(args):
                        "note": "max over ranks of off-rank bytes / max over ranks of the device "
                                "time of the dispatch calls; NVLink push ceiling measured with "
                                "scratch/p2pbench.cu: ~710 GB/s per direction"}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    host_bytes = 2 * tokens * R
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and host_bytes <= 16e9:
         times, ctoks, kind, nthreads = cpu_arm(phases, 1, 1)
         line["cpu_baseline"] = {"value": ctoks / times[0], "unit": "tokens/s", "cores": nthreads,
                                 "kind": kind,
-                                "sample": "one full C2 step after one warm-up step: reference "
-                                          f"balance() per phase + {nthreads}-thread host "
-                                          "memcpy dispatch"}
+                                "sample": f"one full {CFG['name']} step after one warm-up step: "
+                                          f"reference balance() per phase + {nthreads}-thread "
+                                          "host memcpy dispatch"}
+    elif rank == 0 and world == 1:
+        line["cpu_baseline"] = {"value": None, "note": f"skipped: host row buffers of "
+                                                       f"{host_bytes / 1e9:.0f} GB"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     for s in st:
@@ -452,12 +491,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS),
+                    help="workload: C2 (default, the driver's line) or the C3 / C5 evidence lines")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nodewise", dest="nodewise", action="store_false",
                     help="N>1: skip the GPU-wise hosting of destination batches")
     ap.add_argument("--exchange", default="put", choices=["put", "nccl"],
                     help="N>1: fused pack+put over NVLink (default) or NCCL send/recv")
     args = ap.parse_args()
+    CFG.clear()
+    CFG.update(CONFIGS[args.config], name=args.config)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

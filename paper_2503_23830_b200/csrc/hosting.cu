@@ -15,8 +15,8 @@
 //           prefixes (tasks, in DFS order), one warp per task, lane = node,
 //           pruning on lb >= best (a global atomic incumbent);
 //   pass 2  (only if V* beats the incumbents) the first task, in DFS order,
-//           holding a leaf of value V*, pruning on lb > V*; k_host_leaf then
-//           replays that task to its first leaf.
+//           holding a leaf of value V*, pruning on lb > V*; the warp that
+//           finds a leaf stores it, the smallest task wins.
 // The bound is the reference's lower_bound -- max over nodes of
 // (total - gained - optimistic gain) -- read in O(1): the unassigned batches
 // at depth k are exactly order[k..d), so the optimistic gain of node n with r
@@ -34,6 +34,8 @@ constexpr int kHostMaxNodes = 32;                  // lane = node
 constexpr int kOgMax = (kHostMaxD + 1) * (kHostMaxD + kHostMaxNodes);
 constexpr int kHostWarps = 8;
 constexpr long long kHostTasks = 8192;
+constexpr int kHostGrid = 148;
+constexpr int kTaskShift = 11;  // best_task = task << 11 | warp (< 2048)
 constexpr unsigned long long kHostVisitBudget = 1ull << 31;
 
 struct HostState {
@@ -51,10 +53,10 @@ struct HostState {
   int64_t og[kOgMax];                       // [k][node][r] sum of the top r gains over order[k..d)
   unsigned long long best_value;            // pass 1 incumbent value (starts at the incumbents')
   unsigned long long task_counter[2];
-  unsigned long long best_task;             // pass 2: first task holding an optimal leaf
+  unsigned long long best_task;             // pass 2: (first task with an optimal leaf) << 11 | warp
   unsigned long long visits;
   int overflow;
-  int32_t found[kHostMaxD];                 // that leaf: batch -> node
+  uint8_t found[kHostGrid * kHostWarps][kHostMaxD];  // per warp: its pass-2 leaf, batch -> node
 };
 
 __device__ int64_t host_value(const HostState& H, const int32_t* a) {
@@ -220,13 +222,13 @@ __device__ HostSmem host_load_tables(const HostState& H, unsigned char* raw) {
   return HostSmem{g2, og, no, pos};
 }
 
-__device__ __forceinline__ int64_t warp_max64(int64_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const int64_t w = __shfl_xor_sync(~0u, v, o);
-    v = w > v ? w : v;
-  }
-  return v;
+// max over the warp of nonnegative 64-bit values: two 32-bit REDUX steps
+__device__ __forceinline__ int64_t warp_max_nonneg(int64_t v) {
+  const uint64_t u = v > 0 ? static_cast<uint64_t>(v) : 0ull;
+  const unsigned hi = static_cast<unsigned>(u >> 32), lo = static_cast<unsigned>(u);
+  const unsigned mh = __reduce_max_sync(~0u, hi);
+  const unsigned ml = __reduce_max_sync(~0u, hi == mh ? lo : 0u);
+  return static_cast<int64_t>((static_cast<uint64_t>(mh) << 32) | ml);
 }
 
 // One task (prefix t) of the DFS: lane = node. pass 1 prunes lb >= best and
@@ -235,7 +237,7 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
 // ch: this warp's choice stack (position in the candidate order per depth;
 // every lane writes the same value).
 __device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t, int64_t vstar,
-                          uint8_t* ch, int32_t* leaf) {
+                          uint8_t* ch, uint8_t* leaf) {
   const int d = H.d, c = H.c, nodes = H.nodes, k0 = H.k0, lane = threadIdx.x & 31;
   const bool active = lane < nodes;
   const int64_t total = active ? H.node_total[lane] : 0;
@@ -270,7 +272,7 @@ __device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t
       if ((visits & 1023) == 0) {
         if (pass == 1)
           best = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&H.best_value));
-        else if (*reinterpret_cast<volatile unsigned long long*>(&H.best_task) <
+        else if ((*reinterpret_cast<volatile unsigned long long*>(&H.best_task) >> kTaskShift) <
                  static_cast<unsigned long long>(t))
           break;  // an earlier task already holds an optimal leaf (~0: none yet)
         if (*reinterpret_cast<volatile int*>(&H.overflow)) break;
@@ -280,8 +282,8 @@ __device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t
       }
       const int64_t term =
           active ? total - gained - T.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room]
-                 : INT64_MIN;
-      const int64_t lb = warp_max64(term);
+                 : 0;
+      const int64_t lb = warp_max_nonneg(term);  // egress >= 0: clamping keeps the bound valid
       bool prune = pass == 1 ? lb >= best : lb > vstar;
       if (!prune && k == d) {  // leaf: value == lb
         if (pass == 1) {
@@ -347,25 +349,16 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
     t = __shfl_sync(~0u, t, 0);
     if (static_cast<long long>(t) >= H.tasks) break;
     if (*reinterpret_cast<volatile int*>(&H.overflow)) break;
-    if (pass == 2 && *reinterpret_cast<volatile unsigned long long*>(&H.best_task) < t) break;
-    if (host_task(H, T, pass, static_cast<long long>(t), vstar, ch, nullptr)) {
-      if (lane == 0) atomicMin(&H.best_task, t);
+    if (pass == 2 && (*reinterpret_cast<volatile unsigned long long*>(&H.best_task) >> kTaskShift) < t)
+      break;
+    const int gw = blockIdx.x * kHostWarps + warp;
+    if (host_task(H, T, pass, static_cast<long long>(t), vstar, ch, H.found[gw])) {
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) atomicMin(&H.best_task, (t << kTaskShift) | static_cast<unsigned long long>(gw));
       break;  // later tasks come after this one in DFS order
     }
   }
-}
-
-// Replays the first task holding an optimal leaf to that leaf.
-__global__ void __launch_bounds__(32) k_host_leaf(HostState* __restrict__ Hp) {
-  extern __shared__ __align__(16) unsigned char host_raw[];
-  HostState& H = *Hp;
-  if (static_cast<long long>(H.best_value) >= H.incumbent_value || H.overflow ||
-      H.best_task == ~0ull)
-    return;
-  const HostSmem T = host_load_tables(H, host_raw);
-  uint8_t* ch = host_raw + host_smem_bytes(H.d, H.c) - kHostWarps * kHostMaxD;
-  host_task(H, T, 2, static_cast<long long>(H.best_task), static_cast<int64_t>(H.best_value), ch,
-            H.found);
 }
 
 // Final hosting, batch -> instance map, egress figures; then the result remap.
@@ -377,7 +370,8 @@ __global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* _
   int32_t a[kHostMaxD];
   const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value ||
                          H.overflow || H.best_task == ~0ull;
-  for (int b = 0; b < H.d; ++b) a[b] = incumbent ? H.incumbent[b] : H.found[b];
+  const uint8_t* leaf = H.found[incumbent ? 0 : (H.best_task & ((1ull << kTaskShift) - 1))];
+  for (int b = 0; b < H.d; ++b) a[b] = incumbent ? H.incumbent[b] : leaf[b];
   int next[kHostMaxD];
   for (int n = 0; n < H.nodes; ++n) next[n] = n * H.c;
   for (int b = 0; b < H.d; ++b) {  // topology.cpp:283-290: ascending batch order in a node
@@ -401,8 +395,8 @@ __global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* _
   info[3] = static_cast<int64_t>(H.visits);
 #ifdef ORCH_HOST_DEBUG
   printf("hosting: best %llu inc %lld task %llu visits %llu overflow %d k0 %d tasks %lld\n",
-         H.best_value, (long long)H.incumbent_value, H.best_task, H.visits, H.overflow, H.k0,
-         H.tasks);
+         H.best_value, (long long)H.incumbent_value, H.best_task >> kTaskShift, H.visits,
+         H.overflow, H.k0, H.tasks);
 #endif
 }
 
@@ -472,15 +466,13 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, const int64_t* V, HostSta
   if (!configured) {
     const int mx = static_cast<int>(host_smem_bytes(kHostMaxD, 2));  // the largest table set
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     configured = true;
   }
   k_host_prep<<<1, 32, 0, st>>>(d, c, V, H);
   k_host_tables<<<1, kHostMaxD, 0, st>>>(H);
-  k_host_bb<<<kSMs, kHostWarps * 32, sm, st>>>(H, 1);
-  k_host_bb<<<kSMs, kHostWarps * 32, sm, st>>>(H, 2);
-  k_host_leaf<<<1, 32, sm, st>>>(H);
-  ctx->launches += 5;
+  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
+  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
+  ctx->launches += 4;
   return ORCH_OK;
 }
 
