@@ -17,6 +17,7 @@
 
 #include "balance_kernels.cuh"
 #include "balance_small.cuh"
+#include "greedy_lpt.cuh"
 #include "plan.cuh"
 
 namespace orchb {
@@ -75,22 +76,24 @@ int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const u
       k_greedy_warp<<<1, 32, 0, st>>>(d, n, first, xs, order, init_load, init_count, di, ds, doff,
                                       bc, bt, s);
     });
-  } else if (d <= 512) {
-    const size_t sm = rounds_smem_bytes<256>(d);
-    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_greedy_rounds<256>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    launch(ctx, [&] {
-      k_greedy_rounds<256><<<1, 256, sm, st>>>(d, n, first, xs, order, init_load, init_count, di,
-                                               ds, doff, bc, bt, s);
-    });
   } else {
-    const size_t sm = rounds_smem_bytes<1024>(d);
-    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_greedy_rounds<1024>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    launch(ctx, [&] {
-      k_greedy_rounds<1024><<<1, 1024, sm, st>>>(d, n, first, xs, order, init_load, init_count,
-                                                 di, ds, doff, bc, bt, s);
-    });
+    auto run = [&](auto kern, size_t sm, int threads) -> int {
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sm)));
+      launch(ctx, [&] {
+        kern<<<1, threads, sm, st>>>(d, n, first, xs, order, init_load, init_count, di, ds, doff,
+                                     bc, bt, s);
+      });
+      return ORCH_OK;
+    };
+    int rc;
+    if (d <= LptShape<64>::kSlots)
+      rc = run(k_greedy_lpt<64>, lpt_smem_bytes<64>(d), 64);
+    else if (d <= LptShape<256>::kSlots)
+      rc = run(k_greedy_lpt<256>, lpt_smem_bytes<256>(d), 256);
+    else
+      rc = run(k_greedy_lpt<1024>, lpt_smem_bytes<1024>(d), 1024);
+    if (rc) return rc;
   }
   return ORCH_OK;
 }

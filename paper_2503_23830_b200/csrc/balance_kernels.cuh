@@ -4,8 +4,6 @@
 // non-FMA build.
 #pragma once
 
-#include <cub/block/block_radix_sort.cuh>
-
 #include <cstdint>
 
 #include "common.cuh"
@@ -14,9 +12,6 @@ namespace orchb {
 namespace {  // internal linkage: included by several translation units
 
 constexpr uint64_t kU64Max = ~0ull;
-#ifndef ORCH_RSORT_BITS
-#define ORCH_RSORT_BITS 4
-#endif
 
 // Workspace flags shared by the pipeline kernels of one balance call.
 struct Flags {
@@ -216,195 +211,6 @@ __device__ void block_bitonic(uint64_t* U, int p) {
     reg_stages(size, size);
     __syncthreads();
   }
-}
-
-template <int kThreads>
-struct RoundsSort {
-  static constexpr int kItems = (kThreads == 1024 ? 4096 : 512) / kThreads;
-  using Sort = cub::BlockRadixSort<uint32_t, kThreads, kItems, cub::NullType, ORCH_RSORT_BITS>;
-};
-
-// dynamic shared memory of k_greedy_rounds: S, T, U (p2 keys each), cnt[d],
-// then the block radix sort's temporary storage (16-byte aligned)
-__host__ __device__ inline size_t rounds_sort_offset(int d) {
-  int p2 = 1;
-  while (p2 < d) p2 <<= 1;
-  if (p2 < 32) p2 = 32;
-  const size_t base = 3 * sizeof(uint64_t) * p2 + sizeof(int32_t) * d;
-  return (base + 15) & ~size_t{15};
-}
-template <int kThreads>
-__host__ __device__ inline size_t rounds_smem_bytes(int d) {
-  return rounds_sort_offset(d) + sizeof(typename RoundsSort<kThreads>::Sort::TempStorage);
-}
-
-// ---------------------------------------------------------------- K4b
-// distribute_min_sum for any d <= ORCH_MAX_INSTANCES: exact round-batched
-// LPT. Bins are kept sorted by the packed key
-// (load << ib | idx). With x_0 >= x_1 >= ... the next items, if
-// load_(r) - load_(0) < x_r for all r < k, items 0..k-1 go to the bins of
-// rank 0..k-1 in order (every bin already updated this round is strictly
-// heavier than load_(r), so the sequential heap would pick rank r). One round
-// = one block-wide step; the k updated keys are bitonic-sorted and merged back.
-template <int kThreads>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_greedy_rounds(int d, int64_t n, const int64_t* __restrict__ d_first,
-                    const uint32_t* __restrict__ xs, const int32_t* __restrict__ order,
-                    const int64_t* __restrict__ init_load, const int32_t* __restrict__ init_count,
-                    int32_t* __restrict__ dest_inst, int32_t* __restrict__ dest_slot,
-                    int64_t* __restrict__ dst_off, int32_t* __restrict__ bin_count,
-                    int64_t* __restrict__ bin_tokens, orch_summary* s) {
-  if (pipeline_failed(s)) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  int p2 = 1;
-  while (p2 < d) p2 <<= 1;
-  if (p2 < 32) p2 = 32;
-  uint64_t* S = reinterpret_cast<uint64_t*>(smem_raw);  // [p2] sorted bins
-  uint64_t* T = S + p2;                                  // [p2] merge output
-  uint64_t* U = T + p2;                                  // [p2] updated keys
-  int32_t* cnt = reinterpret_cast<int32_t*>(U + p2);     // [d]
-  __shared__ int s_k;
-  __shared__ unsigned long long s_maxrel;
-  // The k updated keys of a round span a narrow load range above L_(0): as
-  // 32-bit (load - L_(0)) << ib | bin keys a block radix sort over only the
-  // needed bits replaces the 64-bit bitonic network (fallback when they do
-  // not fit).
-  using RSort = typename RoundsSort<kThreads>::Sort;
-  constexpr int kItems = RoundsSort<kThreads>::kItems;
-  typename RSort::TempStorage& rsort_tmp = *reinterpret_cast<typename RSort::TempStorage*>(
-      smem_raw + rounds_sort_offset(d));
-  unsigned ib = 0;
-  while ((1u << ib) < static_cast<unsigned>(d)) ++ib;
-  if (ib == 0) ib = 1;
-  const uint64_t mask = (1ull << ib) - 1;
-  const int tid = threadIdx.x;
-
-  for (int i = tid; i < p2; i += kThreads) {
-    if (i < d) {
-      const int64_t l0 = init_load ? init_load[i] : 0;
-      S[i] = (static_cast<uint64_t>(l0) << ib) | static_cast<uint64_t>(i);
-      cnt[i] = init_count ? init_count[i] : 0;
-    } else {
-      S[i] = kU64Max;
-    }
-  }
-  __syncthreads();
-  if (init_load) block_bitonic<kThreads>(S, p2);  // pre-seeded bins: sort them once
-
-  int64_t next = d_first ? *d_first : 0;
-  int64_t rounds = 0;
-#ifdef ORCH_ROUNDS_PROFILE
-  long long t_cond = 0, t_upd = 0, t_sort = 0, t_merge = 0, t_mark = clock64();
-#define RP_MARK(acc) do { if (tid == 0) { const long long t = clock64(); acc += t - t_mark; t_mark = t; } } while (0)
-#else
-#define RP_MARK(acc) do { } while (0)
-#endif
-  while (next < n) {
-    const int m = static_cast<int>(n - next < d ? n - next : d);
-    if (tid == 0) s_k = m;
-    __syncthreads();
-    const int64_t L0 = static_cast<int64_t>(S[0] >> ib);
-    for (int r = tid; r < m; r += kThreads) {
-      const int64_t Lr = static_cast<int64_t>(S[r] >> ib);
-      if (!(Lr - L0 < static_cast<int64_t>(xs[next + r]))) atomicMin(&s_k, r);
-    }
-    __syncthreads();
-    RP_MARK(t_cond);
-    const int k = s_k;  // >= 1: x_0 >= 1 > 0 = L_(0) - L_(0)
-    int pk = 1;
-    while (pk < k) pk <<= 1;
-    if (tid == 0) s_maxrel = 0;
-    __syncthreads();
-    for (int r = tid; r < pk; r += kThreads) {
-      if (r < k) {
-        const uint64_t key = S[r];
-        const int b = static_cast<int>(key & mask);
-        const int64_t L = static_cast<int64_t>(key >> ib);
-        const int64_t x = xs[next + r];
-        const int32_t pos = order[next + r];
-        dest_inst[pos] = b;
-        dest_slot[pos] = cnt[b]++;  // each bin appears once per round
-        dst_off[pos] = L;
-        U[r] = (static_cast<uint64_t>(L + x) << ib) | static_cast<uint64_t>(b);
-        atomicMax(&s_maxrel, static_cast<unsigned long long>(L + x - L0));
-      } else {
-        U[r] = kU64Max;
-      }
-    }
-    __syncthreads();
-    RP_MARK(t_upd);
-    const unsigned long long maxrel = s_maxrel;
-    const int rbits = maxrel ? 64 - __clzll(maxrel) : 1;
-    if (rbits + static_cast<int>(ib) <= 31 && pk <= kItems * kThreads && pk >= 64) {
-      uint32_t keys[kItems];
-#pragma unroll
-      for (int j = 0; j < kItems; ++j) {
-        const int i = tid * kItems + j;
-        if (i < k) {
-          const uint64_t key = U[i];
-          keys[j] = static_cast<uint32_t>((((key >> ib) - static_cast<uint64_t>(L0)) << ib) |
-                                          (key & mask));
-        } else {
-          keys[j] = 0xffffffffu;  // above every real key (< 2^31)
-        }
-      }
-      RSort(rsort_tmp).Sort(keys, 0, rbits + static_cast<int>(ib));
-#pragma unroll
-      for (int j = 0; j < kItems; ++j) {
-        const int i = tid * kItems + j;
-        if (i < pk)
-          U[i] = keys[j] == 0xffffffffu
-                     ? kU64Max
-                     : ((((static_cast<uint64_t>(keys[j]) >> ib) + static_cast<uint64_t>(L0)) << ib) |
-                        (static_cast<uint64_t>(keys[j]) & mask));
-      }
-      __syncthreads();
-    } else {
-      block_bitonic<kThreads>(U, pk);
-    }
-    RP_MARK(t_sort);
-    // merge U[0,k) with S[k,d) into T (keys are unique: distinct bin index)
-    const int rest = d - k;
-    for (int i = tid; i < d; i += kThreads) {
-      uint64_t key;
-      int pos;
-      if (i < k) {
-        key = U[i];
-        int lo = 0, hi = rest;  // lower_bound in S[k..d)
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (S[k + mid] < key) lo = mid + 1; else hi = mid;
-        }
-        pos = i + lo;
-      } else {
-        key = S[i];
-        int lo = 0, hi = k;  // lower_bound in U[0..k)
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (U[mid] < key) lo = mid + 1; else hi = mid;
-        }
-        pos = (i - k) + lo;
-      }
-      T[pos] = key;
-    }
-    __syncthreads();
-    RP_MARK(t_merge);
-    uint64_t* tmp = S;  // T becomes the sorted bins (S[d..p2) and T[d..p2) stay MAX)
-    S = T;
-    T = tmp;
-    next += k;
-    ++rounds;
-  }
-  for (int i = tid; i < d; i += kThreads) {
-    const uint64_t key = S[i];
-    const int b = static_cast<int>(key & mask);
-    bin_tokens[b] = static_cast<int64_t>(key >> ib);
-    bin_count[b] = cnt[b];
-  }
-  if (tid == 0) s->rounds = rounds;
-#ifdef ORCH_ROUNDS_PROFILE
-  if (tid == 0) printf("rounds=%lld cond=%lld upd=%lld sort=%lld merge=%lld (cycles)\n", (long long)rounds, t_cond, t_upd, t_sort, t_merge);
-#endif
 }
 
 // ---------------------------------------------------------------- K6

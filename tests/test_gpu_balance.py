@@ -207,6 +207,18 @@ def test_padded_bound_functions(ctx, oracle):
         assert ctx.padded_bound_feasible(d, L, O, int(L.max()) * (n // d + 1))
 
 
+def test_greedy_wide_loads(ctx, oracle):
+    """d > 32 with loads 2^32 and more apart: the LPT's relative 32-bit radix keys
+    overflow and the round falls back to 64-bit bitonic keys."""
+    rng = np.random.default_rng(4242)
+    for d, n in [(40, 300), (300, 2000), (1500, 6000)]:
+        length = rng.integers(1, 2 ** 32 - 1, n).astype(np.int64)
+        length[: n // 10] = 2 ** 32 - 1
+        origin = rng.integers(0, d, n).astype(np.int32)
+        for kind in (0, 3):
+            run_case(ctx, oracle, kind, d, length, origin, lam=1e-9)
+
+
 def test_padded_search_paths(ctx, oracle):
     """BinaryPadded on the general path: the successor-table search (n <= 100K),
     groups of >= 65535 items (the table's far marker), and the one-warp-per-
