@@ -11,12 +11,15 @@
 // strictly better, in which case the FIRST optimal leaf in DFS order. That is
 // independent of how hard the search prunes, so the device search is free to
 // be parallel as long as its bounds are valid:
-//   pass 1  optimum value V*: the DFS tree cut at depth k0 into <= 8192
-//           prefixes (tasks, in DFS order), one warp per task, lane = node,
-//           pruning on lb >= best (a global atomic incumbent);
-//   pass 2  (only if V* beats the incumbents) the first task, in DFS order,
-//           holding a leaf of value V*, pruning on lb > V*; the warp that
-//           finds a leaf stores it, the smallest task wins.
+//   pass 1  optimum value V*, pruning on lb >= best (a global atomic incumbent);
+//   pass 2  (only if V* beats the incumbents) the first leaf of value V* in DFS
+//           order, pruning on lb > V* and on paths that already sort after the
+//           best V*-leaf found so far.
+// Work: the DFS tree cut at depth k0 into <= 8192 prefixes, then work stealing:
+// one warp runs a subtree depth-first (lane = node); when warps are idle, a busy
+// warp donates the shallowest untried sibling of its current path to a global
+// queue. A subtree is identified by its path of candidate positions, and DFS
+// order is the lexicographic order of paths, so pass 2 stays exact.
 // The bound is the reference's lower_bound -- max over nodes of
 // (total - gained - optimistic gain) -- read in O(1): the unassigned batches
 // at depth k are exactly order[k..d), so the optimistic gain of node n with r
@@ -35,8 +38,14 @@ constexpr int kOgMax = (kHostMaxD + 1) * (kHostMaxD + kHostMaxNodes);
 constexpr int kHostWarps = 8;
 constexpr long long kHostTasks = 8192;
 constexpr int kHostGrid = 148;
-constexpr int kTaskShift = 11;  // best_task = task << 11 | warp (< 2048)
+constexpr int kHostQueue = 16384;  // donated subtrees waiting for a warp
 constexpr unsigned long long kHostVisitBudget = 1ull << 31;
+#ifndef ORCH_HOST_SLEEP
+#define ORCH_HOST_SLEEP 2000
+#endif
+#ifndef ORCH_HOST_CHECK
+#define ORCH_HOST_CHECK 63
+#endif
 
 struct HostState {
   int d, c, nodes, k0;
@@ -52,11 +61,19 @@ struct HostState {
   uint8_t pos[kHostMaxD * kHostMaxNodes];   // [k][node] inverse of no
   int64_t og[kOgMax];                       // [k][node][r] sum of the top r gains over order[k..d)
   unsigned long long best_value;            // pass 1 incumbent value (starts at the incumbents')
-  unsigned long long task_counter[2];
-  unsigned long long best_task;             // pass 2: (first task with an optimal leaf) << 11 | warp
   unsigned long long visits;
   int overflow;
-  uint8_t found[kHostGrid * kHostWarps][kHostMaxD];  // per warp: its pass-2 leaf, batch -> node
+  // work distribution, reset before each pass
+  unsigned long long task_counter;          // initial prefixes handed out
+  unsigned q_head, q_tail;                  // donated subtrees
+  int pending;                              // tasks queued or running
+  int idle;                                 // warps waiting for work
+  int lock;
+  int have_best;                            // pass 2: best_path holds a V*-leaf
+  uint8_t best_path[kHostMaxD];             // candidate position per depth
+  unsigned q_ready[kHostQueue];             // pass << 30 | (index + 1) once published
+  uint8_t q_depth[kHostQueue];
+  uint8_t q_path[kHostQueue][kHostMaxD];
 };
 
 __device__ int64_t host_value(const HostState& H, const int32_t* a) {
@@ -131,10 +148,9 @@ __global__ void k_host_prep(int d, int c, const int64_t* __restrict__ V, HostSta
   for (int b = 0; b < d; ++b) H->incumbent[b] = g_better ? greedy[b] : ident[b];
   H->incumbent_value = g_better ? vg : vi;
   H->best_value = static_cast<unsigned long long>(H->incumbent_value);
-  H->task_counter[0] = H->task_counter[1] = 0;
-  H->best_task = ~0ull;
   H->visits = 0;
   H->overflow = 0;
+  H->have_best = 0;
   int k0 = 0;
   long long tasks = 1;
   while (k0 < d && tasks * nodes <= kHostTasks) {
@@ -192,6 +208,9 @@ __global__ void k_host_tables(HostState* __restrict__ H) {
   }
 }
 
+// per warp: choice stack ch[64] (u8), then avail[64] and donated[64] (u32 masks)
+constexpr int kWarpStack = kHostMaxD + 2 * 4 * kHostMaxD;
+
 struct HostSmem {
   const int64_t* g2;
   const int64_t* og;
@@ -199,11 +218,15 @@ struct HostSmem {
   const uint8_t* pos;
 };
 
-__host__ __device__ inline size_t host_smem_bytes(int d, int c) {
+__host__ __device__ inline size_t host_table_bytes(int d, int c) {  // 16-byte aligned
   const int nodes = d / c;
-  return sizeof(int64_t) * (static_cast<size_t>(d) * nodes +
-                            static_cast<size_t>(d + 1) * nodes * (c + 1)) +
-         2 * static_cast<size_t>(d) * nodes + kHostWarps * kHostMaxD;
+  const size_t b = sizeof(int64_t) * (static_cast<size_t>(d) * nodes +
+                                      static_cast<size_t>(d + 1) * nodes * (c + 1)) +
+                   2 * static_cast<size_t>(d) * nodes;
+  return (b + 15) & ~size_t{15};
+}
+__host__ __device__ inline size_t host_smem_bytes(int d, int c) {
+  return host_table_bytes(d, c) + kHostWarps * kWarpStack;
 }
 
 __device__ HostSmem host_load_tables(const HostState& H, unsigned char* raw) {
@@ -231,54 +254,114 @@ __device__ __forceinline__ int64_t warp_max_nonneg(int64_t v) {
   return static_cast<int64_t>((static_cast<uint64_t>(mh) << 32) | ml);
 }
 
-// One task (prefix t) of the DFS: lane = node. pass 1 prunes lb >= best and
-// lowers the global incumbent at leaves; pass 2 prunes lb > vstar and stops
-// at the first leaf (returns true; `leaf` receives batch -> node if given).
-// ch: this warp's choice stack (position in the candidate order per depth;
-// every lane writes the same value).
-__device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t, int64_t vstar,
-                          uint8_t* ch, uint8_t* leaf) {
-  const int d = H.d, c = H.c, nodes = H.nodes, k0 = H.k0, lane = threadIdx.x & 31;
-  const bool active = lane < nodes;
-  const int64_t total = active ? H.node_total[lane] : 0;
-  int room = active ? c : 0;
-  int64_t gained = 0;
-  // the prefix: digit k (most significant first) = candidate position among nodes with room
-  long long div = H.tasks / nodes;
-  for (int k = 0; k < k0; ++k) {
-    const int p = static_cast<int>((t / (div > 0 ? div : 1)) % nodes);
-    div /= nodes;
-    const unsigned pm =
-        __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
-    if (__popc(pm) <= p) return false;  // no such prefix
-    unsigned rest = pm;
-    for (int q = 0; q < p; ++q) rest &= rest - 1;  // drop the p lowest candidates
-    const int j = __ffs(rest) - 1;
-    ch[k] = static_cast<uint8_t>(j);
-    const int m = T.no[k * nodes + j];
-    if (lane == m) {
-      --room;
-      gained += T.g2[k * nodes + m];
+__device__ __forceinline__ unsigned long long volatile_load(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ unsigned volatile_u32(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+__device__ __forceinline__ int volatile_i32(const int* p) {
+  return *reinterpret_cast<const volatile int*>(p);
+}
+
+// Lane-parallel lexicographic compare of path a[0, k) with b[0, k): -1, 0, 1.
+__device__ __forceinline__ int path_cmp(const uint8_t* a, const volatile uint8_t* b, int k,
+                                        int lane) {
+  for (int l0 = 0; l0 < k; l0 += 32) {
+    const int l = l0 + lane;
+    const int x = l < k ? a[l] : 0, y = l < k ? b[l] : 0;
+    const unsigned diff = __ballot_sync(~0u, x != y);
+    if (diff) {
+      const int f = __ffs(diff) - 1;
+      const int xf = __shfl_sync(~0u, x, f), yf = __shfl_sync(~0u, y, f);
+      return xf < yf ? -1 : 1;
     }
   }
-  int64_t best = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&H.best_value));
+  return 0;
+}
+
+struct WarpStack {
+  uint8_t* ch;        // candidate position chosen per depth
+  unsigned* avail;    // positions with room per depth (as of choosing there)
+  unsigned* donated;  // positions given away per depth (current path only)
+};
+
+// Depth-first search of the subtree below the path ch[0, root) (state: this
+// lane's room / gained). pass 1 prunes lb >= best and lowers the global
+// incumbent at leaves; pass 2 prunes lb > vstar and paths after the best
+// V*-leaf, and records a V*-leaf if it sorts first. Donates siblings to idle
+// warps. Returns when the subtree is exhausted (or cut).
+__device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vstar, WarpStack W,
+                         int root, int room, int64_t gained) {
+  const int d = H.d, c = H.c, nodes = H.nodes, lane = threadIdx.x & 31;
+  const bool active = lane < nodes;
+  const int64_t total = active ? H.node_total[lane] : 0;
+  int64_t best = static_cast<int64_t>(volatile_load(&H.best_value));
   unsigned long long visits = 0;
-  bool found = false;
-  int k = k0, jstart = 0;
+  int k = root, jstart = 0;
   bool descend = true;
+  W.donated[root] = 0;
   for (;;) {
     if (descend) {
       ++visits;
-      if ((visits & 1023) == 0) {
-        if (pass == 1)
-          best = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&H.best_value));
-        else if ((*reinterpret_cast<volatile unsigned long long*>(&H.best_task) >> kTaskShift) <
-                 static_cast<unsigned long long>(t))
-          break;  // an earlier task already holds an optimal leaf (~0: none yet)
-        if (*reinterpret_cast<volatile int*>(&H.overflow)) break;
+      if ((visits & ORCH_HOST_CHECK) == 0) {
+        if (volatile_i32(&H.overflow)) break;
         if ((visits & 65535) == 0 && lane == 0 &&
             atomicAdd(&H.visits, 65536ull) > kHostVisitBudget)
           H.overflow = 1;
+        if (pass == 1) {
+          best = static_cast<int64_t>(volatile_load(&H.best_value));
+        } else if (volatile_i32(&H.have_best) &&
+                   path_cmp(W.ch, H.best_path, k, lane) > 0) {
+          break;  // everything left in this subtree sorts after the best V*-leaf
+        }
+        // donate the shallowest untried sibling when warps wait for work
+        int want = 0;
+        if (lane == 0) {
+          const unsigned queued = volatile_u32(&H.q_tail) - volatile_u32(&H.q_head);
+          want = volatile_i32(&H.idle) > static_cast<int>(queued) && queued < kHostQueue - 2048;
+        }
+        if (__shfl_sync(~0u, want, 0)) {
+          int lvl = -1;
+          unsigned untried = 0;
+          for (int l0 = root; l0 < k && lvl < 0; l0 += 32) {
+            const int l = l0 + lane;
+            unsigned u = 0;
+            if (l < k) {
+              const int j = W.ch[l];
+              u = W.avail[l] & ~W.donated[l] & (j >= 31 ? 0u : (~0u << (j + 1)));
+            }
+            const unsigned has = __ballot_sync(~0u, u != 0);
+            if (has) {
+              const int f = __ffs(has) - 1;
+              lvl = l0 + f;
+              untried = __shfl_sync(~0u, u, f);
+            }
+          }
+          if (lvl >= 0) {
+            const int q = __ffs(untried) - 1;
+            unsigned slot = 0;
+            if (lane == 0) {
+              atomicAdd(&H.pending, 1);
+              slot = atomicAdd(&H.q_tail, 1u);
+            }
+            slot = __shfl_sync(~0u, slot, 0);
+            uint8_t* dst = H.q_path[slot % kHostQueue];
+            for (int l = lane; l < lvl; l += 32) dst[l] = W.ch[l];
+            if (lane == 0) {
+              dst[lvl] = static_cast<uint8_t>(q);
+              H.q_depth[slot % kHostQueue] = static_cast<uint8_t>(lvl + 1);
+            }
+            __syncwarp();
+            __threadfence();
+            __syncwarp();
+            if (lane == 0)
+              *reinterpret_cast<volatile unsigned*>(&H.q_ready[slot % kHostQueue]) =
+                  (static_cast<unsigned>(pass) << 30) | (slot + 1);
+            W.donated[lvl] |= 1u << q;
+            __syncwarp();
+          }
+        }
       }
       const int64_t term =
           active ? total - gained - T.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room]
@@ -290,11 +373,24 @@ __device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t
           if (lane == 0) atomicMin(&H.best_value, static_cast<unsigned long long>(lb));
           best = lb;
           prune = true;
-        } else {
-          found = true;
-          if (leaf)
-            for (int q = lane; q < d; q += 32) leaf[H.order[q]] = T.no[q * nodes + ch[q]];
-          break;
+        } else {  // a V*-leaf: keep it if it is the first in DFS order so far
+          if (lane == 0)
+            while (atomicCAS(&H.lock, 0, 1) != 0) {
+            }
+          __syncwarp();
+          __threadfence();
+          const bool first = !volatile_i32(&H.have_best) || path_cmp(W.ch, H.best_path, d, lane) < 0;
+          if (first) {
+            volatile uint8_t* bp = H.best_path;
+            for (int l = lane; l < d; l += 32) bp[l] = W.ch[l];
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) *reinterpret_cast<volatile int*>(&H.have_best) = 1;
+          }
+          __syncwarp();
+          __threadfence();
+          if (lane == 0) atomicExch(&H.lock, 0);
+          break;  // the rest of this subtree sorts after this leaf
         }
       }
       if (prune) {
@@ -304,9 +400,9 @@ __device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t
       }
     }
     if (!descend) {  // back up one level and move to the next candidate there
-      if (k == k0) break;
+      if (k == root) break;
       --k;
-      const int j = ch[k];
+      const int j = W.ch[k];
       const int m = T.no[k * nodes + j];
       if (lane == m) {
         ++room;
@@ -314,49 +410,138 @@ __device__ bool host_task(HostState& H, const HostSmem& T, int pass, long long t
       }
       jstart = j + 1;
     }
-    unsigned pm =
+    const unsigned av =
         __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
+    W.avail[k] = av;
+    unsigned pm = av & ~W.donated[k];
     pm = jstart >= 32 ? 0u : pm & (~0u << jstart);
     if (!pm) {
       descend = false;
       continue;
     }
     const int j = __ffs(pm) - 1;
-    ch[k] = static_cast<uint8_t>(j);
+    W.ch[k] = static_cast<uint8_t>(j);
     const int m = T.no[k * nodes + j];
     if (lane == m) {
       --room;
       gained += T.g2[k * nodes + m];
     }
     ++k;
+    if (k < d) W.donated[k] = 0;
     descend = true;
   }
   if (lane == 0) atomicAdd(&H.visits, visits & 65535);
-  return found;
+}
+
+__global__ void k_host_reset(HostState* __restrict__ H) {
+  H->task_counter = 0;
+  H->q_head = H->q_tail = 0;
+  H->pending = static_cast<int>(H->tasks);
+  H->idle = 0;
+  H->lock = 0;
 }
 
 __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restrict__ Hp, int pass) {
   extern __shared__ __align__(16) unsigned char host_raw[];
   HostState& H = *Hp;
+  if (H.overflow) return;
   if (pass == 2 && static_cast<long long>(H.best_value) >= H.incumbent_value) return;
   const HostSmem T = host_load_tables(H, host_raw);
   const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  uint8_t* ch = host_raw + host_smem_bytes(H.d, H.c) - kHostWarps * kHostMaxD + warp * kHostMaxD;
+  unsigned char* ws = host_raw + host_table_bytes(H.d, H.c) + warp * kWarpStack;
+  WarpStack W{ws, reinterpret_cast<unsigned*>(ws + kHostMaxD),
+              reinterpret_cast<unsigned*>(ws + kHostMaxD) + kHostMaxD};
   const int64_t vstar = static_cast<int64_t>(H.best_value);
+  const int c = H.c, nodes = H.nodes, k0 = H.k0;
+  const bool active = lane < nodes;
+  bool waiting = false;
   for (;;) {
-    unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(&H.task_counter[pass - 1], 1ull);
+    long long t = -1;
+    long long qs = -1;
+    if (lane == 0) {
+      if (volatile_load(&H.task_counter) < static_cast<unsigned long long>(H.tasks)) {
+        const unsigned long long x = atomicAdd(&H.task_counter, 1ull);
+        if (x < static_cast<unsigned long long>(H.tasks)) t = static_cast<long long>(x);
+      }
+      while (t < 0) {
+        if (volatile_i32(&H.overflow)) break;
+        const unsigned h = volatile_u32(&H.q_head), tl = volatile_u32(&H.q_tail);
+        if (h < tl) {
+          if (atomicCAS(&H.q_head, h, h + 1) == h) {
+            qs = h;
+            break;
+          }
+          continue;
+        }
+        if (volatile_i32(&H.pending) == 0) break;  // nothing queued, nothing running: done
+        if (!waiting) {
+          atomicAdd(&H.idle, 1);
+          waiting = true;
+        }
+        __nanosleep(ORCH_HOST_SLEEP);
+      }
+      if (waiting && (t >= 0 || qs >= 0)) {
+        atomicSub(&H.idle, 1);
+        waiting = false;
+      }
+    }
     t = __shfl_sync(~0u, t, 0);
-    if (static_cast<long long>(t) >= H.tasks) break;
-    if (*reinterpret_cast<volatile int*>(&H.overflow)) break;
-    if (pass == 2 && (*reinterpret_cast<volatile unsigned long long*>(&H.best_task) >> kTaskShift) < t)
-      break;
-    const int gw = blockIdx.x * kHostWarps + warp;
-    if (host_task(H, T, pass, static_cast<long long>(t), vstar, ch, H.found[gw])) {
+    qs = __shfl_sync(~0u, qs, 0);
+    if (t < 0 && qs < 0) break;
+    int room = active ? c : 0;
+    int64_t gained = 0;
+    int root = 0;
+    bool ok = true;
+    if (t >= 0) {  // initial prefix: digit k = candidate position among nodes with room
+      long long div = H.tasks / nodes;
+      for (int k = 0; k < k0; ++k) {
+        const int p = static_cast<int>((t / (div > 0 ? div : 1)) % nodes);
+        div /= nodes;
+        const unsigned pm =
+            __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
+        if (__popc(pm) <= p) {
+          ok = false;  // no such prefix
+          break;
+        }
+        unsigned rest = pm;
+        for (int q = 0; q < p; ++q) rest &= rest - 1;  // drop the p lowest candidates
+        const int j = __ffs(rest) - 1;
+        W.ch[k] = static_cast<uint8_t>(j);
+        const int m = T.no[k * nodes + j];
+        if (lane == m) {
+          --room;
+          gained += T.g2[k * nodes + m];
+        }
+      }
+      root = k0;
+    } else {  // donated subtree: wait until published, then replay its path
+      const unsigned slot = static_cast<unsigned>(qs) % kHostQueue;
+      const unsigned want = (static_cast<unsigned>(pass) << 30) | (static_cast<unsigned>(qs) + 1);
+      if (lane == 0)
+        while (volatile_u32(&H.q_ready[slot]) != want) {
+        }
       __syncwarp();
       __threadfence();
-      if (lane == 0) atomicMin(&H.best_task, (t << kTaskShift) | static_cast<unsigned long long>(gw));
-      break;  // later tasks come after this one in DFS order
+      root = *reinterpret_cast<volatile uint8_t*>(&H.q_depth[slot]);
+      const volatile uint8_t* src = H.q_path[slot];
+      for (int k = 0; k < root; ++k) {
+        const int j = src[k];
+        W.ch[k] = static_cast<uint8_t>(j);
+        const int m = T.no[k * nodes + j];
+        if (lane == m) {
+          --room;
+          gained += T.g2[k * nodes + m];
+        }
+      }
+    }
+    __syncwarp();
+    if (ok && pass == 2 && volatile_i32(&H.have_best) && path_cmp(W.ch, H.best_path, root, lane) > 0)
+      ok = false;  // the whole subtree sorts after the best V*-leaf
+    if (ok) host_dfs(H, T, pass, vstar, W, root, room, gained);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicSub(&H.pending, 1);
     }
   }
 }
@@ -369,9 +554,10 @@ __global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* _
   const HostState& H = *Hp;
   int32_t a[kHostMaxD];
   const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value ||
-                         H.overflow || H.best_task == ~0ull;
-  const uint8_t* leaf = H.found[incumbent ? 0 : (H.best_task & ((1ull << kTaskShift) - 1))];
-  for (int b = 0; b < H.d; ++b) a[b] = incumbent ? H.incumbent[b] : leaf[b];
+                         H.overflow || !H.have_best;
+  for (int b = 0; b < H.d; ++b) a[b] = H.incumbent[b];
+  if (!incumbent)
+    for (int l = 0; l < H.d; ++l) a[H.order[l]] = H.no[l * H.nodes + H.best_path[l]];
   int next[kHostMaxD];
   for (int n = 0; n < H.nodes; ++n) next[n] = n * H.c;
   for (int b = 0; b < H.d; ++b) {  // topology.cpp:283-290: ascending batch order in a node
@@ -394,9 +580,9 @@ __global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* _
   info[2] = H.overflow ? -1 : (incumbent ? 0 : 1);  // -1: visit budget hit, incumbent kept
   info[3] = static_cast<int64_t>(H.visits);
 #ifdef ORCH_HOST_DEBUG
-  printf("hosting: best %llu inc %lld task %llu visits %llu overflow %d k0 %d tasks %lld\n",
-         H.best_value, (long long)H.incumbent_value, H.best_task >> kTaskShift, H.visits,
-         H.overflow, H.k0, H.tasks);
+  printf("hosting: best %llu inc %lld visits %llu overflow %d k0 %d tasks %lld queued %u\n",
+         H.best_value, (long long)H.incumbent_value, H.visits, H.overflow, H.k0, H.tasks,
+         H.q_tail);
 #endif
 }
 
@@ -470,9 +656,11 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, const int64_t* V, HostSta
   }
   k_host_prep<<<1, 32, 0, st>>>(d, c, V, H);
   k_host_tables<<<1, kHostMaxD, 0, st>>>(H);
+  k_host_reset<<<1, 1, 0, st>>>(H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
+  k_host_reset<<<1, 1, 0, st>>>(H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
-  ctx->launches += 4;
+  ctx->launches += 6;
   return ORCH_OK;
 }
 
