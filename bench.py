@@ -451,16 +451,31 @@ def run_b200(args):
         "clocks": clocks.summary(),
     }
     if P > 1:
-        a2a_bytes = max_over_ranks(sum(s["send_rows"] for s in st) * R)  # bottleneck rank
+        # NVLink bottleneck: the busiest direction of the busiest rank (egress =
+        # rows this rank sends off-rank, ingress = rows it receives)
+        egress = max_over_ranks(sum(s["send_rows"] for s in st) * R)
+        ingress = max_over_ranks(sum(s["recv_rows"] for s in st) * R)
+        a2a_bytes = max(egress, ingress)
         disp_ms = max_over_ranks(disp_ms)
+        busbw = a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9
         line["exchange"] = args.exchange
         line["nodewise_hosting"] = bool(args.nodewise)
-        line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes,
-                       "busbw_gbs_rank": a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9,
+        line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes, "max_egress_bytes": egress,
+                       "max_ingress_bytes": ingress, "busbw_gbs_rank": busbw,
                        "nvlink_peak_gbs": 900.0, "nvlink_measured_gbs": 770.0,
-                       "note": "max over ranks of off-rank bytes / max over ranks of the device "
-                               "time of the dispatch calls; NVLink push ceiling measured with "
-                               "scratch/p2pbench.cu: ~710 GB/s per direction"}
+                       "note": "max over ranks of max(off-rank bytes sent, received) / max over "
+                               "ranks of the device time of the dispatch calls; NVLink push "
+                               "ceiling measured with scratch/p2pbench.cu: ~710 GB/s per direction"}
+        # at N > 1 the row movement is NVLink-bound: roofline against the
+        # measured peer copy (B200_PROFILING.md: 770 GB/s per direction per GPU)
+        hbm_view = line["roofline"]
+        line["roofline"] = {"bound": "nvlink", "achieved": busbw, "peak": 770.0, "unit": "GB/s",
+                            "frac": busbw / 770.0, "traffic": None,
+                            "kernel": ("k_move_tma<kPut> (orch_put)" if args.exchange == "put"
+                                       else "ncclSend/ncclRecv (orch_dispatch)"),
+                            "peak_kind": "measured peer copy (B200_PROFILING.md)",
+                            "share_of_step": hbm_view["share_of_step"],
+                            "hbm_view": {k: hbm_view[k] for k in ("achieved", "peak", "frac")}}
     host_bytes = 2 * tokens * R
     if rank == 0 and world == 1 and not args.no_cpu_baseline and host_bytes <= 16e9:
         times, ctoks, kind, nthreads = cpu_arm(phases, 1, 1)

@@ -71,7 +71,7 @@ struct HostState {
   int lock;
   int have_best;                            // pass 2: best_path holds a V*-leaf
   uint8_t best_path[kHostMaxD];             // candidate position per depth
-  unsigned q_ready[kHostQueue];             // pass << 30 | (index + 1) once published
+  unsigned q_ready[kHostQueue];             // pass << 30 | (index + 1) once published, 0 once read
   uint8_t q_depth[kHostQueue];
   uint8_t q_path[kHostQueue][kHostMaxD];
 };
@@ -296,7 +296,8 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
   const int d = H.d, c = H.c, nodes = H.nodes, lane = threadIdx.x & 31;
   const bool active = lane < nodes;
   const int64_t total = active ? H.node_total[lane] : 0;
-  int64_t best = static_cast<int64_t>(volatile_load(&H.best_value));
+  int64_t best = static_cast<int64_t>(
+      __shfl_sync(~0u, (threadIdx.x & 31) == 0 ? volatile_load(&H.best_value) : 0ull, 0));
   unsigned long long visits = 0;
   int k = root, jstart = 0;
   bool descend = true;
@@ -305,13 +306,16 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
     if (descend) {
       ++visits;
       if ((visits & ORCH_HOST_CHECK) == 0) {
-        if (volatile_i32(&H.overflow)) break;
+        // shared flags are read by lane 0 and broadcast: every branch below
+        // must be warp-uniform (the warp-collective ops need all 32 lanes)
+        if (__shfl_sync(~0u, lane == 0 ? volatile_i32(&H.overflow) : 0, 0)) break;
         if ((visits & 65535) == 0 && lane == 0 &&
             atomicAdd(&H.visits, 65536ull) > kHostVisitBudget)
           H.overflow = 1;
         if (pass == 1) {
-          best = static_cast<int64_t>(volatile_load(&H.best_value));
-        } else if (volatile_i32(&H.have_best) &&
+          best = static_cast<int64_t>(
+              __shfl_sync(~0u, lane == 0 ? volatile_load(&H.best_value) : 0ull, 0));
+        } else if (__shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) &&
                    path_cmp(W.ch, H.best_path, k, lane) > 0) {
           break;  // everything left in this subtree sorts after the best V*-leaf
         }
@@ -346,6 +350,10 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
               slot = atomicAdd(&H.q_tail, 1u);
             }
             slot = __shfl_sync(~0u, slot, 0);
+            if (lane == 0)  // the slot's previous subtree must have been read out
+              while (volatile_u32(&H.q_ready[slot % kHostQueue]) != 0u) {
+              }
+            __syncwarp();
             uint8_t* dst = H.q_path[slot % kHostQueue];
             for (int l = lane; l < lvl; l += 32) dst[l] = W.ch[l];
             if (lane == 0) {
@@ -379,7 +387,8 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
             }
           __syncwarp();
           __threadfence();
-          const bool first = !volatile_i32(&H.have_best) || path_cmp(W.ch, H.best_path, d, lane) < 0;
+          const bool first = !__shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) ||
+                             path_cmp(W.ch, H.best_path, d, lane) < 0;
           if (first) {
             volatile uint8_t* bp = H.best_path;
             for (int l = lane; l < d; l += 32) bp[l] = W.ch[l];
@@ -433,12 +442,18 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
   if (lane == 0) atomicAdd(&H.visits, visits & 65535);
 }
 
+// Before each pass. The queue's publish flags are cleared too: the state lives
+// in the reused workspace arena, and a flag left over from an earlier search
+// (same pass, same slot) would let a reader take a path before it is written.
 __global__ void k_host_reset(HostState* __restrict__ H) {
-  H->task_counter = 0;
-  H->q_head = H->q_tail = 0;
-  H->pending = static_cast<int>(H->tasks);
-  H->idle = 0;
-  H->lock = 0;
+  for (int i = threadIdx.x; i < kHostQueue; i += blockDim.x) H->q_ready[i] = 0u;
+  if (threadIdx.x == 0) {
+    H->task_counter = 0;
+    H->q_head = H->q_tail = 0;
+    H->pending = static_cast<int>(H->tasks);
+    H->idle = 0;
+    H->lock = 0;
+  }
 }
 
 __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restrict__ Hp, int pass) {
@@ -533,9 +548,14 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
           gained += T.g2[k * nodes + m];
         }
       }
+      __syncwarp();
+      __threadfence();
+      if (lane == 0)  // path copied out: the slot may be reused
+        *reinterpret_cast<volatile unsigned*>(&H.q_ready[slot]) = 0u;
     }
     __syncwarp();
-    if (ok && pass == 2 && volatile_i32(&H.have_best) && path_cmp(W.ch, H.best_path, root, lane) > 0)
+    if (ok && pass == 2 && __shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) &&
+        path_cmp(W.ch, H.best_path, root, lane) > 0)
       ok = false;  // the whole subtree sorts after the best V*-leaf
     if (ok) host_dfs(H, T, pass, vstar, W, root, room, gained);
     __syncwarp();
@@ -656,9 +676,9 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, const int64_t* V, HostSta
   }
   k_host_prep<<<1, 32, 0, st>>>(d, c, V, H);
   k_host_tables<<<1, kHostMaxD, 0, st>>>(H);
-  k_host_reset<<<1, 1, 0, st>>>(H);
+  k_host_reset<<<1, 1024, 0, st>>>(H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
-  k_host_reset<<<1, 1, 0, st>>>(H);
+  k_host_reset<<<1, 1024, 0, st>>>(H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
   ctx->launches += 6;
   return ORCH_OK;

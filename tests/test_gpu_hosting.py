@@ -127,3 +127,15 @@ def test_hosting_limits(ctx):
     with pytest.raises(OrchError) as e:
         ctx.solve_hosting(6, 4, np.zeros((6, 6), np.int64))
     assert e.value.code == 1
+
+
+def test_solve_hosting_repeated(ctx):
+    """The search state lives in the reused workspace: back-to-back searches
+    (the pipelined bench re-hosts every phase of every step) must not see
+    each other's work-queue entries."""
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting_c3.npz"))
+    for _ in range(6):
+        for k in range(len(f["c"])):
+            a = ctx.solve_hosting(64, int(f["c"][k]), f["V"][k])
+            np.testing.assert_array_equal(a["hosting"], f["hosting"][k])
+            assert a["max_egress"] == f["max_egress"][k]
