@@ -203,7 +203,7 @@ def run_reference(args):
 def run_b200(args):
     import torch
     import torch.distributed as dist
-    from paper_2503_23830_b200.capi import Balance, Comm, Context, Layout, Window
+    from paper_2503_23830_b200.capi import Balance, Comm, Context, GatherWindow, Layout, Window
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -226,9 +226,14 @@ def run_b200(args):
         comm_data = Comm(world, rank, uid[0][1])
     # one context (workspace arena) per stream
     ctx_meta, ctx_data = Context(local), Context(local)
+    gwin = None
     P, c, R = world, D_INST // world, CFG["R"]
     batch, phases = build_inputs()
-    meta_stream = torch.cuda.Stream(device=dev)
+    if comm_meta is not None and args.gather == "put":
+        gwin = GatherWindow(ctx_meta, comm_meta, max(len(ph[1]) for ph in phases))
+    # the metadata chain is latency-bound and runs beside the row movement:
+    # give its kernels the higher stream priority
+    meta_stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("ORCH_META_PRIO", "-1")))
     data_stream = torch.cuda.Stream(device=dev)
 
     # Per phase: local items (global input positions), and two buffer sets of
@@ -255,15 +260,41 @@ def run_b200(args):
                     for _ in range(2)]
         st.append(s)
 
+    meta_marks = []  # ORCH_BENCH_TRACE: events between the metadata sub-steps
+
+    def mark(stream):
+        if os.environ.get("ORCH_BENCH_TRACE"):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            meta_marks.append(e)
+
+    probe_x = torch.zeros(1, device=dev)
+    probe = []  # ORCH_BENCH_TRACE: one tiny kernel's event-timed latency per phase
+
     def meta(s, B, stream):
-        if comm_meta is not None:
+        if os.environ.get("ORCH_BENCH_TRACE"):
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(int(os.environ.get("ORCH_PROBE_CYCLES", "1000")))
+            p1.record(stream)
+            probe.append((p0, p1))
+        mark(stream)
+        if gwin is not None:  # one single-CTA kernel through peer memory
+            ctx_meta.allgather_items_put(gwin, s["pos"], s["llen"], s["lorg"], s["n"], B["glen"],
+                                         B["gorg"], stream=stream)
+        elif comm_meta is not None:
             ctx_meta.allgather_items(comm_meta, s["pos"], s["llen"], s["lorg"], s["max_local"],
                                      s["n"], B["glen"], B["gorg"], stream=stream)
+        mark(stream)
         ctx_meta.balance(s["kind"], D_INST, B["glen"], B["gorg"], lam=s["lam"], v=s["v"],
                          out=B["bal"], stream=stream)
+        mark(stream)
         if P > 1 and args.nodewise:  # GPU-wise hosting (orchestrator.cpp:283 with node = GPU)
             ctx_meta.nodewise(D_INST, c, B["glen"], B["gorg"], B["bal"], stream=stream)
+        mark(stream)
         ctx_meta.layout(D_INST, P, B["glen"], B["gorg"], B["bal"], out=B["lay"], stream=stream)
+        mark(stream)
 
     # sizing pass (not timed): buffers from this batch's layout
     for s in st:
@@ -301,6 +332,8 @@ def run_b200(args):
 
     disp_events = []
     counter = [0]
+    # ORCH_BENCH_TRACE=1: per-phase event timeline of the timed steps (stderr)
+    trace = [] if os.environ.get("ORCH_BENCH_TRACE") else None
 
     def step(record=False, h2d=False):
         b = counter[0] % 2
@@ -317,14 +350,24 @@ def run_b200(args):
                         s["pos"].copy_(s["h_pos"], non_blocking=True)
                         s["llen"].copy_(s["h_len"], non_blocking=True)
                         s["lorg"].copy_(s["h_org"], non_blocking=True)
+            if trace is not None:
+                m0 = torch.cuda.Event(enable_timing=True)
+                m0.record(meta_stream)
             meta(s, B, meta_stream)
             B["meta_done"].record(meta_stream)
+            if trace is not None:
+                m1 = torch.cuda.Event(enable_timing=True)
+                m1.record(meta_stream)
+                d0 = torch.cuda.Event(enable_timing=True)
+                d0.record(data_stream)  # data stream reaches this phase
             data_stream.wait_event(B["meta_done"])
             if record:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(data_stream)
-            if s["win"] is not None:  # one barrier per step closes both phases' puts
+            if os.environ.get("ORCH_BENCH_NOMOVE"):  # diagnostics only: metadata alone
+                pass
+            elif s["win"] is not None:  # one barrier per step closes both phases' puts
                 ctx_data.put(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
                              s["win"], comm_data, stream=data_stream)
                 if s is st[-1]:
@@ -335,6 +378,8 @@ def run_b200(args):
             if record:
                 e1.record(data_stream)
                 disp_events.append((s["name"], e0, e1))
+                if trace is not None:
+                    trace.append((counter[0], s["name"], m0, m1, d0, e0, e1))
             B["data_done"].record(data_stream)
         return b
 
@@ -365,6 +410,28 @@ def run_b200(args):
         t1.record(data_stream)
         barrier()
     launches = ctx_meta.launches + ctx_data.launches - launches0
+    if trace:
+        if gwin is not None:
+            stm = gwin.stamps().astype(np.int64)
+            for row in stm:
+                if row[0]:
+                    print(f"[trace r{rank}] gather stages us: free {(row[1] - row[0]) / 1e3:.1f} "
+                          f"store+fence {(row[2] - row[1]) / 1e3:.1f} wait peers "
+                          f"{(row[3] - row[2]) / 1e3:.1f} copy-out {(row[4] - row[3]) / 1e3:.1f}",
+                          file=sys.stderr)
+        pr = [a.elapsed_time(b) * 1e3 for a, b in probe[-3 * len(st):]]
+        print(f"[trace r{rank}] tiny kernel on the metadata stream: "
+              + " ".join(f"{x:.1f}" for x in pr) + " us", file=sys.stderr)
+        mm = meta_marks[-5 * 3 * len(st):]
+        for i in range(0, len(mm), 5):
+            g = [mm[i].elapsed_time(mm[i + j]) for j in range(1, 5)]
+            print(f"[trace r{rank}] meta allgather {g[0]:.3f} balance {g[1] - g[0]:.3f} "
+                  f"nodewise {g[2] - g[1]:.3f} layout {g[3] - g[2]:.3f} ms", file=sys.stderr)
+        for it, name, m0, m1, d0, e0, e1 in trace[-3 * len(st):]:
+            print(f"[trace r{rank}] step {it} {name:6s} meta {t0.elapsed_time(m0):8.3f}-"
+                  f"{t0.elapsed_time(m1):8.3f}  data ready {t0.elapsed_time(d0):8.3f} "
+                  f"move {t0.elapsed_time(e0):8.3f}-{t0.elapsed_time(e1):8.3f} ms",
+                  file=sys.stderr)
     ms = max_over_ranks(t0.elapsed_time(t1))
     tokens = sum(int(s["L"].sum()) for s in st)
     seqs = sum(s["n"] for s in st)
@@ -459,6 +526,7 @@ def run_b200(args):
         disp_ms = max_over_ranks(disp_ms)
         busbw = a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9
         line["exchange"] = args.exchange
+        line["gather"] = args.gather
         line["nodewise_hosting"] = bool(args.nodewise)
         line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes, "max_egress_bytes": egress,
                        "max_ingress_bytes": ingress, "busbw_gbs_rank": busbw,
@@ -493,6 +561,8 @@ def run_b200(args):
         if s.get("win") is not None:
             s["rout"] = None
             s["win"].close()
+    if gwin is not None:
+        gwin.close()
     if comm_meta is not None:
         comm_meta.close()
         comm_data.close()
@@ -511,6 +581,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nodewise", dest="nodewise", action="store_false",
                     help="N>1: skip the GPU-wise hosting of destination batches")
+    ap.add_argument("--gather", default="put", choices=["put", "nccl"],
+                    help="N>1 lengths all-gather: peer-memory kernel (default) or ncclAllGather")
     ap.add_argument("--exchange", default="put", choices=["put", "nccl"],
                     help="N>1: fused pack+put over NVLink (default) or NCCL send/recv")
     args = ap.parse_args()

@@ -341,6 +341,28 @@ int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_
                          const int32_t* d_local_origin, int64_t n, int64_t* d_len,
                          int32_t* d_origin, void* stream);
 
+/* gather_lengths (exchange.cpp:34-47) over NVLink peer memory, for the
+ * metadata path of a pipelined step: one single-CTA kernel per call stores
+ * this rank's records (length, origin) at their global input positions in
+ * every rank's gather window, raises this rank's arrival flag there, waits for
+ * all P flags, copies the window into d_len / d_origin and acknowledges, so
+ * the next call may overwrite the window. Same result as
+ * orch_allgather_items; no NCCL kernel, no ring. Calls are collective and
+ * numbered: every rank makes them in the same order. A position outside
+ * [0, n) sets *d_status = ORCH_INVALID_ARGUMENT (d_status optional); a peer
+ * that does not arrive within ~4 s sets ORCH_CUDA_ERROR instead of hanging. */
+typedef struct orch_gather_window orch_gather_window;
+int orch_gather_window_create(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
+                              orch_gather_window** out); /* collective */
+int orch_gather_window_destroy(orch_gather_window* g);   /* collective */
+/* Diagnostics: %globaltimer (ns) at the stages of the last 8 calls, [epoch % 8][k]:
+ * k = 0 start, 1 window free, 2 records stored + fenced, 3 all ranks arrived, 4 end. */
+int orch_gather_window_stamps(const orch_gather_window* g, uint64_t* h_out64);
+int orch_allgather_items_put(orch_ctx* ctx, orch_gather_window* g, int64_t local_n,
+                             const int64_t* d_local_pos, const int64_t* d_local_len,
+                             const int32_t* d_local_origin, int64_t n, int64_t* d_len,
+                             int32_t* d_origin, int32_t* d_status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

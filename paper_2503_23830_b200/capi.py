@@ -32,6 +32,8 @@ EXPORTED = [
     "orch_solve_hosting_host", "orch_nodewise", "orch_rearrange", "orch_backbone_targets",
     "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
     "orch_window_destroy", "orch_dispatch_put", "orch_put",
+    "orch_gather_window_create", "orch_gather_window_destroy", "orch_allgather_items_put",
+    "orch_gather_window_stamps",
 ]
 
 
@@ -224,6 +226,27 @@ class Window:
     def close(self):
         if self.h:
             _check(lib().orch_window_destroy(self.h))
+            self.h = C.c_void_p()
+
+
+class GatherWindow:
+    """orch_gather_window: peer-memory all-gather of item records (collective)."""
+
+    def __init__(self, ctx: "Context", comm: Comm, max_n: int):
+        self.h = C.c_void_p()
+        _check(lib().orch_gather_window_create(ctx.h, comm.h, C.c_int64(max_n), C.byref(self.h)))
+        self.max_n = max_n
+
+    def stamps(self):
+        """[8][8] %globaltimer ns of the last 8 calls' stages (diagnostics)."""
+        import numpy as np
+        out = np.zeros(64, np.uint64)
+        _check(lib().orch_gather_window_stamps(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out.reshape(8, 8)
+
+    def close(self):
+        if self.h:
+            _check(lib().orch_gather_window_destroy(self.h))
             self.h = C.c_void_p()
 
 
@@ -468,6 +491,15 @@ class Context:
     @staticmethod
     def barrier(comm: Comm, stream=None):
         _check(lib().orch_barrier(comm.h, _stream(stream)))
+
+    def allgather_items_put(self, gwin: GatherWindow, local_pos, local_len, local_origin, n,
+                            out_len, out_origin, status=None, stream=None):
+        _check(lib().orch_allgather_items_put(self.h, gwin.h, C.c_int64(local_len.numel()),
+                                              _ptr(local_pos), _ptr(local_len),
+                                              _ptr(local_origin), C.c_int64(n), _ptr(out_len),
+                                              _ptr(out_origin),
+                                              _ptr(status) if status is not None else None,
+                                              _stream(stream)))
 
     def allgather_items(self, comm: Comm, local_pos, local_len, local_origin, max_local, n,
                         out_len, out_origin, stream=None):

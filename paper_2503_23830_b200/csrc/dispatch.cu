@@ -35,6 +35,13 @@ struct orch_window {
   char** peers_dev = nullptr;     // device copy [P]
 };
 
+struct orch_gather_window {
+  orch_window* w = nullptr;
+  uint64_t* stamps = nullptr;  // device [8][8]
+  int64_t max_n = 0;
+  uint64_t epoch = 0;  // calls made so far (the same count on every rank)
+};
+
 namespace orchb {
 
 namespace {
@@ -283,6 +290,7 @@ struct MoveArgs {
   const int32_t* unit_first;
   char* const* peer_out;  // kPut: output buffer of every rank (IPC-mapped), [P]
   unsigned long long* chunk_counter;  // TMA path: next unclaimed chunk (zeroed by k_unit_map)
+  int scramble;                       // kPut: claim chunk batches in a scrambled order
   int32_t* status;
   size_t R;
   const char* in;
@@ -434,11 +442,32 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   };
 
+  // kPut: batches of 32 chunks are claimed in a scrambled order (batch b ->
+  // b * stride mod nb, stride coprime with nb, near nb / golden ratio), so the
+  // CTAs in flight are spread over the whole input buffer and every peer
+  // receives at a rate proportional to its share of the step. In input order,
+  // long items (C5: 128-512 MB each) would send to one peer at a time while the
+  // other ranks may pick the same peer: ingress collisions on that peer's links.
+  const int64_t nb = (chunks + 31) / 32;
+  int64_t stride = 1;
+  if (MODE == kPut && a.scramble && nb > 2) {
+    stride = static_cast<int64_t>(static_cast<double>(nb) * 0.6180339887) | 1;
+    for (;; ++stride) {
+      int64_t x = stride, y = nb;
+      while (y) {
+        const int64_t t = x % y;
+        x = y;
+        y = t;
+      }
+      if (x == 1) break;
+    }
+  }
   for (;;) {
     int64_t base = 0;
     if (lane == 0) base = static_cast<int64_t>(atomicAdd(claim, 32ull));
     base = __shfl_sync(~0u, base, 0);
     if (base >= chunks) break;
+    if (stride != 1) base = ((base / 32) * stride % nb) * 32;
     // ---- decode: lane j -> this CTA's chunk (base + j)
     const int64_t c = base + lane;
     int np = 0;
@@ -554,6 +583,109 @@ __global__ void k_scatter_records(int64_t total, int64_t n, const int64_t* __res
     len[p] = rec[3 * i + 1];
     org[p] = static_cast<int32_t>(rec[3 * i + 2]);
   }
+}
+
+// ------------------------------------------- gather_lengths over NVLink
+// One-shot all-gather of the (length, origin) records through peer memory
+// (gather_lengths, exchange.cpp:34-47). Gather window layout per rank:
+//   len[max_n] i64 | origin[max_n] i32 | arrived[P] u64 | consumed[P] u64
+// arrived[q] = the last call whose records rank q has fully stored here;
+// consumed[q] = the last call whose records rank q has copied out of ITS
+// window (so this rank may overwrite them). Calls are numbered 1, 2, ... in
+// the same order on every rank.
+struct GatherArgs {
+  char* const* peers;  // [P] gather windows
+  int me, P;
+  uint64_t epoch;
+  int64_t max_n, n, local_n;
+  const int64_t* pos;
+  const int64_t* len;
+  const int32_t* org;
+  int64_t* out_len;
+  int32_t* out_org;
+  int32_t* status;  // optional: ORCH_INVALID_ARGUMENT on a bad position, ORCH_CUDA_ERROR on timeout
+  uint64_t* stamps;  // [8][8] %globaltimer at the kernel's stages, slot epoch % 8 (diagnostics)
+};
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__host__ __device__ inline size_t gather_flags_off(int64_t max_n) {
+  return (static_cast<size_t>(max_n) * 12 + 15) & ~size_t{15};
+}
+
+// spin until *p >= want; false after ~4 s (a peer that never arrives)
+__device__ bool wait_at_least(const uint64_t* p, uint64_t want) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) < want) {
+    __nanosleep(64);
+    if (clock64() - t0 > 8000000000ll) return false;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(1024) k_gather_put(GatherArgs a) {
+  __shared__ int bad;
+  const int t = threadIdx.x;
+  const size_t fo = gather_flags_off(a.max_n);
+  auto len_of = [&](int q) { return reinterpret_cast<int64_t*>(a.peers[q]); };
+  auto org_of = [&](int q) { return reinterpret_cast<int32_t*>(a.peers[q] + 8 * a.max_n); };
+  auto arrived = [&](int q) { return reinterpret_cast<uint64_t*>(a.peers[q] + fo); };
+  auto consumed = [&](int q) { return reinterpret_cast<uint64_t*>(a.peers[q] + fo) + a.P; };
+  uint64_t* stamp = a.stamps + (a.epoch % 8) * 8;
+  if (t == 0) {
+    bad = 0;
+    stamp[0] = gtimer();
+  }
+  // 1. every peer has copied out our previous call's records
+  if (t < a.P && !wait_at_least(consumed(a.me) + t, a.epoch - 1)) bad = 2;
+  __syncthreads();
+  if (t == 0) stamp[1] = gtimer();
+  // 2. our records, at their global input positions, into every window
+  for (int64_t i = t; i < a.local_n && !bad; i += blockDim.x) {
+    const int64_t p = a.pos[i];
+    if (p < 0 || p >= a.n) {
+      bad = 1;
+      break;
+    }
+    const int64_t l = a.len[i];
+    const int32_t o = a.org[i];
+    for (int q = 0; q < a.P; ++q) {
+      len_of(q)[p] = l;
+      org_of(q)[p] = o;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (t == 0) stamp[2] = gtimer();
+  if (t < a.P) st_release_sys(arrived(t) + a.me, a.epoch);  // this rank's records are in
+  // 3. every rank's records are here
+  if (t < a.P && !wait_at_least(arrived(a.me) + t, a.epoch)) bad = 2;
+  __syncthreads();
+  if (t == 0) stamp[3] = gtimer();
+  const int64_t* wl = len_of(a.me);
+  const int32_t* wo = org_of(a.me);
+  for (int64_t i = t; i < a.n; i += blockDim.x) {  // L2 (the coherence point of peer stores)
+    a.out_len[i] = __ldcg(wl + i);
+    a.out_org[i] = __ldcg(wo + i);
+  }
+  __syncthreads();
+  // 4. the window may be overwritten by the next call
+  if (t < a.P) st_release_sys(consumed(t) + a.me, a.epoch);
+  if (t == 0 && bad && a.status) *a.status = bad == 1 ? ORCH_INVALID_ARGUMENT : ORCH_CUDA_ERROR;
+  if (t == 0) stamp[4] = gtimer();
 }
 
 // ------------------------------------------------------- encode_lengths
@@ -722,13 +854,23 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
       const int v = e ? atoi(e) : 1;
       return v >= 1 && v <= 2 ? v : 1;
     }();
-    const int tma_grid = kSMs * ctas_per_sm;
+    // experiment knobs: ORCH_PUT_FREE_SMS=k leaves k SMs to other streams and
+    // makes each put CTA claim a whole SM's shared memory (no co-residence)
+    static const int free_sms = [] {
+      const char* e = getenv("ORCH_PUT_FREE_SMS");
+      const int v = e ? atoi(e) : 0;
+      return v >= 0 && v < kSMs ? v : 0;
+    }();
+    const bool fat = mode == kPut && free_sms > 0;
+    const int tma_grid = fat ? kSMs - free_sms : kSMs * ctas_per_sm;
+    const int sm_req = fat ? 227 * 1024 - static_cast<int>(sizeof(TmaTable)) - 64 : sm;
     static bool attr_done = false;
     if (!attr_done) {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kUnpack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPut>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         free_sms > 0 ? sm_req : sm));
       attr_done = true;
     }
     launch(ctx, [&] {
@@ -737,7 +879,7 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
       else if (mode == kPack)
         k_move_tma<kPack><<<tma_grid, 32, sm, st>>>(a);
       else if (mode == kPut)
-        k_move_tma<kPut><<<tma_grid, 32, sm, st>>>(a);
+        k_move_tma<kPut><<<tma_grid, 32, sm_req, st>>>(a);
       else
         k_move_tma<kUnpack><<<tma_grid, 32, sm, st>>>(a);
     });
@@ -1193,6 +1335,11 @@ int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t
     a.in = static_cast<const char*>(d_in);
     a.out = out_win->base;
     a.peer_out = out_win->peers_dev;
+    static const int scramble = [] {
+      const char* e = getenv("ORCH_PUT_SCRAMBLE");
+      return e ? atoi(e) : 1;
+    }();
+    a.scramble = scramble;
     rc = run_move(ctx, kPut, a, n, L->rank_src_off, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
   }
@@ -1207,6 +1354,71 @@ int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, cons
   if (rc) return rc;
   // rows from every peer have landed once every rank passed its put kernel
   return orch_barrier(comm, stream);
+}
+
+int orch_gather_window_create(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
+                              orch_gather_window** out) {
+  if (!ctx || !comm || !out || max_n < 1) return fail(ORCH_INVALID_ARGUMENT, "bad gather window arguments");
+  const size_t bytes = gather_flags_off(max_n) + 16 * static_cast<size_t>(comm->size);
+  auto* g = new orch_gather_window();
+  g->max_n = max_n;
+  int rc = orch_window_create(ctx, comm, bytes, &g->w);
+  if (rc) {
+    delete g;
+    return rc;
+  }
+  ORCH_CUDA_TRY(cudaMalloc(&g->stamps, 64 * sizeof(uint64_t)));
+  ORCH_CUDA_TRY(cudaMemset(g->stamps, 0, 64 * sizeof(uint64_t)));
+  // flags start at 0 on every rank before any peer can store into them
+  ORCH_CUDA_TRY(cudaMemset(g->w->base, 0, bytes));
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  rc = orch_barrier(comm, nullptr);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  *out = g;
+  return ORCH_OK;
+}
+
+int orch_gather_window_destroy(orch_gather_window* g) {
+  if (!g) return ORCH_OK;
+  const int rc = orch_window_destroy(g->w);
+  cudaFree(g->stamps);
+  delete g;
+  return rc;
+}
+
+int orch_gather_window_stamps(const orch_gather_window* g, uint64_t* h_out) {
+  if (!g || !h_out) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  ORCH_CUDA_TRY(cudaMemcpy(h_out, g->stamps, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return ORCH_OK;
+}
+
+int orch_allgather_items_put(orch_ctx* ctx, orch_gather_window* g, int64_t local_n,
+                             const int64_t* d_local_pos, const int64_t* d_local_len,
+                             const int32_t* d_local_origin, int64_t n, int64_t* d_len,
+                             int32_t* d_origin, int32_t* d_status, void* stream) {
+  if (!ctx || !g) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (n > g->max_n || local_n < 0 || local_n > n)
+    return fail(ORCH_INVALID_ARGUMENT, "gather window holds fewer items than n");
+  GatherArgs a{};
+  a.peers = g->w->peers_dev;
+  a.me = g->w->comm->rank;
+  a.P = g->w->comm->size;
+  a.epoch = ++g->epoch;
+  a.max_n = g->max_n;
+  a.n = n;
+  a.local_n = local_n;
+  a.pos = d_local_pos;
+  a.len = d_local_len;
+  a.org = d_local_origin;
+  a.out_len = d_len;
+  a.out_org = d_origin;
+  a.status = d_status;
+  a.stamps = g->stamps;
+  auto st = static_cast<cudaStream_t>(stream);
+  launch(ctx, [&] { k_gather_put<<<1, 1024, 0, st>>>(a); });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
 }
 
 }  // extern "C"

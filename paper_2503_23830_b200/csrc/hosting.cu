@@ -24,6 +24,8 @@
 // (total - gained - optimistic gain) -- read in O(1): the unassigned batches
 // at depth k are exactly order[k..d), so the optimistic gain of node n with r
 // slots left is a table og[k][n][r] built once.
+#include <climits>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -655,6 +657,481 @@ __global__ void k_vol(int d, int64_t n, const int64_t* __restrict__ len,
               static_cast<unsigned long long>(len[i]));
 }
 
+// ------------------------------------------------ one-CTA node-wise path
+// For small searches (d <= 32, <= 2^18 leaves, n <= 12288: every C2 shape on
+// 2/4/8 GPUs) the whole of orch_nodewise runs in ONE kernel, in shared memory:
+// volume matrix -> gains, regret order, incumbents, search tables -> two-pass
+// branch and bound (32 warps, lane = node, DFS-ordered prefix tasks) -> hosting,
+// batch_to_instance, egress figures -> relabelling of the balance result.
+// The metadata chain runs beside the NVLink row exchange, where every global
+// round trip costs several microseconds; this path pays about four of them
+// instead of a dozen launches and copies. Same answer as the multi-CTA path
+// (first optimal leaf in DFS order, the incumbents otherwise).
+constexpr int kNwThreads = 1024;
+constexpr int kNwWarps = kNwThreads / 32;
+constexpr int kNwMaxD = 32;
+constexpr int kNwMaxItems = 12288;
+constexpr int kNwTasks = 64;  // at least two prefix tasks per warp
+constexpr double kNwMaxLeaves = 262144.0;
+
+struct NwSmem {
+  unsigned long long V[kNwMaxD * kNwMaxD];  // [src instance][dest batch]
+  int64_t gain[kNwMaxD * kNwMaxD];          // [node][batch]
+  int64_t g2[kNwMaxD * kNwMaxD];            // [k][node]
+  int64_t og[(kNwMaxD + 1) * 2 * kNwMaxD];  // [k][node][r], (d+1)*nodes*(c+1) <= (d+1)*2d
+  int64_t node_total[kNwMaxD];
+  int64_t regret[kNwMaxD];
+  int64_t node_e[kNwMaxD], node_e0[kNwMaxD];
+  int64_t incumbent_value;
+  unsigned long long best;  // pass 1: best value so far
+  unsigned long long visits;
+  int32_t order[kNwMaxD];
+  int32_t ident[kNwMaxD], greedy[kNwMaxD], incumbent[kNwMaxD], a[kNwMaxD];
+  int32_t b2i[kNwMaxD], inv[kNwMaxD], noff[kNwMaxD + 1];
+  int32_t ocnt[kNwMaxD], ooff[kNwMaxD + 1];
+  int64_t olen[kNwMaxD], otok[kNwMaxD];
+  double ocost[kNwMaxD];
+  uint8_t no[kNwMaxD * kNwMaxD];   // [k][j] j-th candidate node of depth k
+  uint8_t pos[kNwMaxD * kNwMaxD];  // [k][node]
+  uint8_t ch[kNwWarps][kNwMaxD];   // per-warp DFS path (candidate positions)
+  uint8_t best_path[kNwMaxD];
+  int64_t vals[2];
+  int tasks, k0, best_task, lock;
+  unsigned task_ctr;
+  int32_t members[kNwMaxItems];
+};
+
+struct NwArgs {
+  int d, c, n;
+  const int64_t* len;
+  const int32_t* origin;
+  int32_t* dest_inst;
+  int32_t* bin_count;
+  int64_t* bin_len;
+  int64_t* bin_tokens;
+  double* bin_cost;
+  int32_t* bin_offset;
+  int32_t* bin_member;
+  int32_t* hosting;
+  int32_t* b2i;
+  int64_t* info;
+};
+
+// argmax over lanes of v (v >= -1), lowest lane on ties
+__device__ __forceinline__ int warp_argmax_first(int64_t v) {
+  int lane = threadIdx.x & 31;
+  int64_t bv = v;
+  int bl = lane;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t ov = __shfl_xor_sync(~0u, bv, o);
+    const int ol = __shfl_xor_sync(~0u, bl, o);
+    if (ov > bv || (ov == bv && ol < bl)) {
+      bv = ov;
+      bl = ol;
+    }
+  }
+  return bl;
+}
+
+// DFS of the subtree below ch[0, root) for one warp (lane = node); the
+// prune rules and visiting order of host_dfs, without donation.
+__device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, int room,
+                       int64_t gained, int d, int c, int nodes, uint8_t* ch) {
+  const int lane = threadIdx.x & 31;
+  const bool active = lane < nodes;
+  const int64_t total = active ? S.node_total[lane] : 0;
+  unsigned long long visits = 0;
+  int k = root, jstart = 0;
+  bool descend = true;
+  for (;;) {
+    if (descend) {
+      ++visits;
+      if (pass == 2 &&
+          __shfl_sync(~0u, lane == 0 ? *reinterpret_cast<volatile int*>(&S.best_task) : 0, 0) < task)
+        break;  // an earlier task already holds a V*-leaf
+      const int64_t term =
+          active ? total - gained - S.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room] : 0;
+      const int64_t lb = warp_max_nonneg(term);
+      bool prune;
+      if (pass == 1) {
+        const int64_t best = static_cast<int64_t>(__shfl_sync(
+            ~0u, lane == 0 ? *reinterpret_cast<volatile unsigned long long*>(&S.best) : 0ull, 0));
+        prune = lb >= best;
+      } else {
+        prune = lb > vstar;
+      }
+      if (!prune && k == d) {  // leaf: value == lb
+        if (pass == 1) {
+          if (lane == 0) atomicMin(&S.best, static_cast<unsigned long long>(lb));
+          prune = true;
+        } else {  // the first V*-leaf of this task in DFS order
+          if (lane == 0)
+            while (atomicCAS(&S.lock, 0, 1) != 0) {
+            }
+          __syncwarp();
+          __threadfence_block();
+          const int won = __shfl_sync(~0u, lane == 0 ? (task < *reinterpret_cast<volatile int*>(&S.best_task)) : 0, 0);
+          if (won) {
+            for (int l = lane; l < d; l += 32) S.best_path[l] = ch[l];
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) *reinterpret_cast<volatile int*>(&S.best_task) = task;
+          }
+          __syncwarp();
+          __threadfence_block();
+          if (lane == 0) atomicExch(&S.lock, 0);
+          break;
+        }
+      }
+      if (prune) {
+        descend = false;
+      } else {
+        jstart = 0;
+      }
+    }
+    if (!descend) {
+      if (k == root) break;
+      --k;
+      const int j = ch[k];
+      const int m = S.no[k * nodes + j];
+      if (lane == m) {
+        ++room;
+        gained -= S.g2[k * nodes + m];
+      }
+      jstart = j + 1;
+    }
+    const unsigned av =
+        __reduce_or_sync(~0u, (active && room > 0) ? (1u << S.pos[k * nodes + lane]) : 0u);
+    const unsigned pm = jstart >= 32 ? 0u : av & (~0u << jstart);
+    if (!pm) {
+      descend = false;
+      continue;
+    }
+    const int j = __ffs(pm) - 1;
+    __syncwarp();
+    if (lane == 0) ch[k] = static_cast<uint8_t>(j);
+    __syncwarp();
+    const int m = S.no[k * nodes + j];
+    if (lane == m) {
+      --room;
+      gained += S.g2[k * nodes + m];
+    }
+    ++k;
+    descend = true;
+  }
+  if (lane == 0) atomicAdd(&S.visits, visits);
+}
+
+// one pass over the prefix tasks (DFS order), dynamic claiming
+__device__ void nw_pass(NwSmem& S, int pass, int64_t vstar, int d, int c, int nodes) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool active = lane < nodes;
+  uint8_t* ch = S.ch[warp];
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = static_cast<int>(atomicAdd(&S.task_ctr, 1u));
+    t = __shfl_sync(~0u, t, 0);
+    if (t >= S.tasks) break;
+    if (pass == 2 &&
+        __shfl_sync(~0u, lane == 0 ? *reinterpret_cast<volatile int*>(&S.best_task) : 0, 0) < t)
+      break;  // tasks are claimed in DFS order: the rest sort after the best leaf
+    int room = active ? c : 0;
+    int64_t gained = 0;
+    bool ok = true;
+    int div = S.tasks / nodes;
+    for (int k = 0; k < S.k0; ++k) {
+      const int p = (t / (div > 0 ? div : 1)) % nodes;
+      div /= nodes;
+      const unsigned pm =
+          __reduce_or_sync(~0u, (active && room > 0) ? (1u << S.pos[k * nodes + lane]) : 0u);
+      if (__popc(pm) <= p) {
+        ok = false;
+        break;
+      }
+      unsigned rest = pm;
+      for (int q = 0; q < p; ++q) rest &= rest - 1;
+      const int j = __ffs(rest) - 1;
+      __syncwarp();
+      if (lane == 0) ch[k] = static_cast<uint8_t>(j);
+      __syncwarp();
+      const int m = S.no[k * nodes + j];
+      if (lane == m) {
+        --room;
+        gained += S.g2[k * nodes + m];
+      }
+    }
+    if (ok) nw_dfs(S, pass, vstar, t, S.k0, room, gained, d, c, nodes, ch);
+  }
+}
+
+__global__ void __launch_bounds__(kNwThreads, 1) k_nodewise_small(NwArgs a) {
+  extern __shared__ __align__(16) unsigned char nw_raw[];
+  NwSmem& S = *reinterpret_cast<NwSmem*>(nw_raw);
+  const int d = a.d, c = a.c, nodes = d / c, n = a.n, t = threadIdx.x;
+#ifdef ORCH_NW_STAMPS
+  uint64_t ts[8];
+  int nts = 0;
+  auto stamp = [&] { if (t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[nts++])); };
+  stamp();
+#else
+  auto stamp = [] {};
+#endif
+  const int lane = t & 31, warp = t >> 5;
+  // ---- volume matrix (topology.cpp:40-53) and the old per-batch arrays
+  for (int i = t; i < d * d; i += kNwThreads) S.V[i] = 0;
+  if (t < d) {
+    S.ocnt[t] = a.bin_count[t];
+    if (a.bin_len) S.olen[t] = a.bin_len[t];
+    if (a.bin_tokens) S.otok[t] = a.bin_tokens[t];
+    if (a.bin_cost) S.ocost[t] = a.bin_cost[t];
+  }
+  if (t <= d) S.ooff[t] = a.bin_offset[t];
+  if (t == 0) {
+    S.visits = 0;
+    S.task_ctr = 0;
+    S.best_task = INT_MAX;
+    S.lock = 0;
+  }
+  __syncthreads();
+  for (int i = t; i < n; i += kNwThreads) {
+    S.members[i] = a.bin_member[i];
+    atomicAdd(&S.V[a.origin[i] * d + a.dest_inst[i]], static_cast<unsigned long long>(a.len[i]));
+  }
+  __syncthreads();
+  stamp();
+  // ---- gains, node totals (topology.cpp:195-262)
+  for (int i = t; i < nodes * d; i += kNwThreads) {
+    const int nd = i / d, b = i % d;
+    int64_t g = 0;
+    for (int r = nd * c; r < (nd + 1) * c; ++r) g += static_cast<int64_t>(S.V[r * d + b]);
+    S.gain[i] = g;
+  }
+  __syncthreads();
+  if (t < nodes) {
+    int64_t tot = 0;
+    for (int b = 0; b < d; ++b) tot += S.gain[t * d + b];
+    S.node_total[t] = tot;
+  }
+  if (t < d) {
+    int64_t top = 0, second = 0;
+    for (int nd = 0; nd < nodes; ++nd) {
+      const int64_t g = S.gain[nd * d + t];
+      if (g > top) {
+        second = top;
+        top = g;
+      } else if (g > second) {
+        second = g;
+      }
+    }
+    S.regret[t] = top - second;
+  }
+  __syncthreads();
+  if (t < d) {  // stable order by descending regret (the reference's insertion sort)
+    int r = 0;
+    for (int b = 0; b < d; ++b)
+      r += S.regret[b] > S.regret[t] || (S.regret[b] == S.regret[t] && b < t);
+    S.order[r] = t;
+    S.ident[t] = t / c;
+  }
+  __syncthreads();
+  if (warp == 0) {  // greedy incumbent: each batch in order to the best node with room
+    int room = lane < nodes ? c : 0;
+    for (int k = 0; k < d; ++k) {
+      const int b = S.order[k];
+      const int pick = warp_argmax_first(room > 0 ? S.gain[lane * d + b] : -1);
+      if (lane == pick) {
+        --room;
+        S.greedy[b] = pick;
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {  // search tables, candidate order per depth
+    for (int k = lane; k < d; k += 32) {
+      const int b = S.order[k];
+      uint8_t* no = S.no + k * nodes;
+      for (int nd = 0; nd < nodes; ++nd) {
+        S.g2[k * nodes + nd] = S.gain[nd * d + b];
+        int j = nd - 1;
+        while (j >= 0 && S.gain[no[j] * d + b] < S.gain[nd * d + b]) {
+          no[j + 1] = no[j];
+          --j;
+        }
+        no[j + 1] = static_cast<uint8_t>(nd);
+      }
+      for (int j = 0; j < nodes; ++j) S.pos[k * nodes + no[j]] = static_cast<uint8_t>(j);
+    }
+  } else if (warp == 2 && lane < nodes) {  // og[k][node][r], deepest level first
+    int64_t top[kNwMaxD];
+    int have = 0;
+    for (int k = d; k >= 0; --k) {
+      if (k < d) {
+        const int64_t g = S.gain[lane * d + S.order[k]];
+        int j = -1;
+        if (have < c) j = have++;
+        else if (top[c - 1] < g) j = c - 1;
+        if (j >= 0) {
+          while (j > 0 && top[j - 1] < g) {
+            top[j] = top[j - 1];
+            --j;
+          }
+          top[j] = g;
+        }
+      }
+      int64_t* og = S.og + (static_cast<size_t>(k) * nodes + lane) * (c + 1);
+      int64_t acc = 0;
+      og[0] = 0;
+      for (int r = 1; r <= c; ++r) {
+        if (r <= have) acc += top[r - 1];
+        og[r] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp < 2) {  // host_value of identity (warp 0) and greedy (warp 1)
+    const int32_t* asg = warp == 0 ? S.ident : S.greedy;
+    int64_t e = INT64_MIN;
+    if (lane < nodes) {
+      e = S.node_total[lane];
+      for (int b = 0; b < d; ++b)
+        if (asg[b] == lane) e -= S.gain[lane * d + b];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int64_t x = __shfl_xor_sync(~0u, e, o);
+      e = x > e ? x : e;
+    }
+    if (lane == 0) S.vals[warp] = e;
+  }
+  __syncthreads();
+  if (t < d) {
+    const bool g_better = S.vals[1] < S.vals[0];  // offer(greedy) only when strictly better
+    S.incumbent[t] = g_better ? S.greedy[t] : S.ident[t];
+  }
+  if (t == 0) {
+    const bool g_better = S.vals[1] < S.vals[0];
+    S.incumbent_value = g_better ? S.vals[1] : S.vals[0];
+    S.best = static_cast<unsigned long long>(S.incumbent_value);
+    // a few prefix tasks per warp: the trees here are small, and a task costs
+    // its prefix decode even when the bound cuts it at once
+    int k0 = 0, tasks = 1;
+    while (k0 < d && tasks < kNwTasks) {
+      tasks *= nodes;
+      ++k0;
+    }
+    S.k0 = k0;
+    S.tasks = tasks;
+    // no leaf can beat the incumbents when the root bound already reaches them
+    int64_t lb = 0;
+    for (int nd = 0; nd < nodes; ++nd) {
+      const int64_t e = S.node_total[nd] - S.og[static_cast<size_t>(nd) * (c + 1) + c];
+      lb = e > lb ? e : lb;
+    }
+    if (lb >= S.incumbent_value) S.tasks = 0;
+  }
+  __syncthreads();
+  stamp();
+  // ---- search: pass 1 finds V*, pass 2 the first V*-leaf in DFS order
+  nw_pass(S, 1, 0, d, c, nodes);
+  __syncthreads();
+  stamp();
+  const int64_t vstar = static_cast<int64_t>(S.best);
+  const bool search2 = vstar < S.incumbent_value;
+  if (t == 0) S.task_ctr = 0;
+  __syncthreads();
+  if (search2) nw_pass(S, 2, vstar, d, c, nodes);
+  __syncthreads();
+  stamp();
+  // ---- hosting, batch -> instance (topology.cpp:283-290), egress figures
+  const bool incumbent = !search2 || S.best_task == INT_MAX;
+  if (t < d) S.a[t] = S.incumbent[t];
+  __syncthreads();
+  if (!incumbent && t < d) S.a[S.order[t]] = S.no[t * nodes + S.best_path[t]];
+  __syncthreads();
+  if (t == 0) {
+    int next[kNwMaxD];
+    for (int nd = 0; nd < nodes; ++nd) next[nd] = nd * c;
+    for (int b = 0; b < d; ++b) {
+      const int nb = next[S.a[b]]++;
+      S.b2i[b] = nb;
+      S.inv[nb] = b;
+    }
+  }
+  __syncthreads();
+  if (t < nodes) {
+    int64_t e = 0, e0 = 0;
+    for (int i = t * c; i < (t + 1) * c; ++i)
+      for (int b = 0; b < d; ++b) {
+        const int64_t v = static_cast<int64_t>(S.V[i * d + b]);
+        if (S.a[b] != t) e += v;
+        if (b / c != t) e0 += v;
+      }
+    S.node_e[t] = e;
+    S.node_e0[t] = e0;
+  }
+  if (t < d) {
+    a.hosting[t] = S.a[t];
+    a.b2i[t] = S.b2i[t];
+  }
+  if (t == 0) {
+    int acc = 0;
+    for (int j = 0; j < d; ++j) {
+      S.noff[j] = acc;
+      acc += S.ocnt[S.inv[j]];
+    }
+    S.noff[d] = acc;
+  }
+  __syncthreads();
+  if (t == 0 && a.info) {
+    int64_t worst = 0, base = 0;
+    for (int nd = 0; nd < nodes; ++nd) {
+      worst = S.node_e[nd] > worst ? S.node_e[nd] : worst;
+      base = S.node_e0[nd] > base ? S.node_e0[nd] : base;
+    }
+    a.info[0] = worst;
+    a.info[1] = base;
+    a.info[2] = incumbent ? 0 : 1;
+    a.info[3] = static_cast<int64_t>(S.visits);
+  }
+  // ---- relabel the balance result: batch b becomes instance b2i[b]
+  if (t < d) {
+    const int b = S.inv[t];
+    a.bin_count[t] = S.ocnt[b];
+    if (a.bin_len) a.bin_len[t] = S.olen[b];
+    if (a.bin_tokens) a.bin_tokens[t] = S.otok[b];
+    if (a.bin_cost) a.bin_cost[t] = S.ocost[b];
+  }
+  if (t <= d) a.bin_offset[t] = S.noff[t];
+  for (int j = 0; j < d; ++j) {
+    const int b = S.inv[j];
+    const int cnt = S.ooff[b + 1] - S.ooff[b];
+    for (int k = t; k < cnt; k += kNwThreads) a.bin_member[S.noff[j] + k] = S.members[S.ooff[b] + k];
+  }
+  for (int i = t; i < n; i += kNwThreads) a.dest_inst[i] = S.b2i[a.dest_inst[i]];
+#ifdef ORCH_NW_STAMPS
+  __syncthreads();
+  stamp();
+  if (t == 0) {
+    static __device__ unsigned calls = 0;
+    if ((atomicAdd(&calls, 1u) % 16) == 15)
+      printf("NWSTAMP d=%d c=%d load %.1f prep %.1f pass1 %.1f pass2 %.1f out %.1f us visits %llu tasks %d\n", d, c,
+             (ts[1] - ts[0]) / 1e3, (ts[2] - ts[1]) / 1e3, (ts[3] - ts[2]) / 1e3, (ts[4] - ts[3]) / 1e3,
+             (ts[5] - ts[4]) / 1e3, S.visits, S.tasks);
+  }
+#endif
+}
+
+bool nodewise_small_fits(int d, int c, int64_t n) {
+  const int nodes = d / c;
+  if (d > kNwMaxD || nodes > kNwMaxD || n > kNwMaxItems) return false;
+  double leaves = 1.0;  // d! / (c!)^nodes
+  for (int i = 2; i <= d; ++i) leaves *= i;
+  double cf = 1.0;
+  for (int i = 2; i <= c; ++i) cf *= i;
+  for (int nd = 0; nd < nodes; ++nd) leaves /= cf;
+  return leaves <= kNwMaxLeaves;
+}
+
 int check_hosting_args(int d, int c) {
   if (d < 1 || c < 1)
     return fail(ORCH_INVALID_ARGUMENT, "topology needs at least one instance and one per node");
@@ -734,6 +1211,41 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
   if (!bal->dest_inst || !bal->bin_count || !bal->bin_offset || !bal->bin_member)
     return fail(ORCH_INVALID_ARGUMENT, "orch_nodewise needs dest_inst, bin_count and the CSR");
   auto st = static_cast<cudaStream_t>(stream);
+  static const bool small_off = getenv("ORCH_NODEWISE_SMALL") && atoi(getenv("ORCH_NODEWISE_SMALL")) == 0;
+  if (!small_off && nodewise_small_fits(d, c, n)) {
+    Plan sp;
+    int32_t *hosting, *b2i;
+    sp.add_or(&hosting, d_hosting, d);
+    sp.add_or(&b2i, d_batch_to_instance, d);
+    rc = sp.commit(ctx, st);
+    if (rc) return rc;
+    NwArgs a{};
+    a.d = d;
+    a.c = c;
+    a.n = static_cast<int>(n);
+    a.len = d_len;
+    a.origin = d_origin;
+    a.dest_inst = bal->dest_inst;
+    a.bin_count = bal->bin_count;
+    a.bin_len = bal->bin_len;
+    a.bin_tokens = bal->bin_tokens;
+    a.bin_cost = bal->bin_cost;
+    a.bin_offset = bal->bin_offset;
+    a.bin_member = bal->bin_member;
+    a.hosting = hosting;
+    a.b2i = b2i;
+    a.info = d_info;
+    static bool configured = false;
+    if (!configured) {
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_nodewise_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(NwSmem))));
+      configured = true;
+    }
+    k_nodewise_small<<<1, kNwThreads, sizeof(NwSmem), st>>>(a);
+    ctx->launches += 1;
+    ORCH_CUDA_TRY(cudaGetLastError());
+    return ORCH_OK;
+  }
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
   Plan plan;
   unsigned long long* V;

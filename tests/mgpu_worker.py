@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 from oracle import Oracle  # noqa: E402
-from paper_2503_23830_b200.capi import Comm, Context, Window  # noqa: E402
+from paper_2503_23830_b200.capi import Comm, Context, GatherWindow, Window  # noqa: E402
 
 
 def main():
@@ -33,6 +33,7 @@ def main():
     P = world
     failures = 0
     cases = 0
+    gwin = GatherWindow(ctx, comm, 300)
     for seed in range(6):
         for kind in (0, 1, 2, 3):
             for R in (32, 8192):
@@ -52,6 +53,16 @@ def main():
                                     torch.from_numpy(O[mine]).cuda(), max_local, n, gl, go)
                 torch.cuda.synchronize()
                 ok = np.array_equal(gl.cpu().numpy(), L) and np.array_equal(go.cpu().numpy(), O)
+                # the same records through peer memory (one window, numbered calls)
+                gl2 = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+                go2 = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+                gst = torch.zeros(1, dtype=torch.int32, device="cuda")
+                ctx.allgather_items_put(gwin, torch.from_numpy(mine.astype(np.int64)).cuda(),
+                                        torch.from_numpy(L[mine]).cuda(),
+                                        torch.from_numpy(O[mine]).cuda(), n, gl2, go2, gst)
+                torch.cuda.synchronize()
+                ok = ok and np.array_equal(gl2.cpu().numpy(), L)
+                ok = ok and np.array_equal(go2.cpu().numpy(), O) and int(gst.item()) == 0
                 bal = ctx.balance(kind, d, gl, go, lam=0.01, v=3)
                 lay = ctx.layout(d, P, gl, go, bal)
                 torch.cuda.synchronize()
@@ -96,6 +107,7 @@ def main():
                           flush=True)
     t = torch.tensor([failures])
     dist.all_reduce(t)
+    gwin.close()
     comm.close()
     if rank == 0:
         print(f"MGPU world={world} cases={cases} failures={int(t.item())}", flush=True)

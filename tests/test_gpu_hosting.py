@@ -139,3 +139,34 @@ def test_solve_hosting_repeated(ctx):
             a = ctx.solve_hosting(64, int(f["c"][k]), f["V"][k])
             np.testing.assert_array_equal(a["hosting"], f["hosting"][k])
             assert a["max_egress"] == f["max_egress"][k]
+
+
+@pytest.mark.parametrize("d,c", [(8, 1), (8, 2), (8, 4), (6, 2), (9, 3), (10, 5), (16, 8),
+                                 (12, 6), (4, 1), (12, 4), (12, 3)])
+def test_nodewise_small_path(ctx, oracle, d, c):
+    """orch_nodewise's one-CTA path (d <= 32, <= 2^18 leaves; (12, 3) takes the
+    multi-CTA path) against the oracle's branch and bound on the volume matrix."""
+    rng = np.random.default_rng(d * 100 + c)
+    for trial in range(12):
+        n = int(rng.integers(d, 400))
+        L, O = random_instance(rng, d, n, 1, int(rng.choice([3, 60, 4000])))
+        kind = int(rng.integers(0, 4))
+        o = oracle.balance(kind, d, L, O, lam=0.01, v=3)
+        V = oracle.volume_matrix(d, L, O, o.dest_inst)
+        h = oracle.solve_hosting(d, c, V)
+        Lt, Ot = torch.from_numpy(L).cuda(), torch.from_numpy(O).cuda()
+        bal = ctx.balance(kind, d, Lt, Ot, lam=0.01, v=3)
+        hosting, b2i, info = ctx.nodewise(d, c, Lt, Ot, bal)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(hosting.cpu().numpy(), h["hosting"])
+        np.testing.assert_array_equal(b2i.cpu().numpy(), h["batch_to_instance"])
+        assert int(info[0]) == h["max_egress"] and int(info[1]) == h["baseline_max"]
+        di = h["batch_to_instance"][o.dest_inst]
+        np.testing.assert_array_equal(bal.dest_inst[:n].cpu().numpy(), di)
+        inv = np.argsort(h["batch_to_instance"])
+        np.testing.assert_array_equal(bal.bin_count.cpu().numpy(), o.bin_count[inv])
+        off = bal.bin_offset.cpu().numpy()
+        mem = bal.bin_member[:n].cpu().numpy()
+        for j in range(d):
+            seg = mem[off[j]:off[j + 1]]
+            assert (di[seg] == j).all() and (o.dest_slot[seg] == np.arange(len(seg))).all()
