@@ -71,6 +71,7 @@ struct HostState {
   int pending;                              // tasks queued or running
   int idle;                                 // warps waiting for work
   int lock;
+  int done_ctas;                            // pass 1 CTAs finished (the last one resets for pass 2)
   int have_best;                            // pass 2: best_path holds a V*-leaf
   uint8_t best_path[kHostMaxD];             // candidate position per depth
   unsigned q_ready[kHostQueue];             // pass << 30 | (index + 1) once published, 0 once read
@@ -78,38 +79,63 @@ struct HostState {
   uint8_t q_path[kHostQueue][kHostMaxD];
 };
 
-__device__ int64_t host_value(const HostState& H, const int32_t* a) {
-  int64_t worst = INT64_MIN;
-  for (int n = 0; n < H.nodes; ++n) {
-    int64_t e = H.node_total[n];
-    for (int b = 0; b < H.d; ++b)
-      if (a[b] == n) e -= H.gain[n * H.d + b];
-    worst = e > worst ? e : worst;
+// ----------------------------------------------------------- preparation
+// gains, node totals, branching order, incumbents and search tables
+// (topology.cpp:195-262), block-wide in shared memory: every global round trip
+// of this latency-bound chain costs microseconds while the row exchange loads
+// the memory system, so nothing here touches global memory.
+template <int MD>
+struct Prep {
+  unsigned long long V[MD * MD];                // [src instance][dest batch]
+  int64_t gain[kHostMaxNodes * MD];             // [node][batch]
+  int64_t g2[MD * kHostMaxNodes];               // [k][node] gain of node for order[k]
+  int64_t og[(MD + 1) * (MD + kHostMaxNodes)];  // [k][node][r], (d+1)*nodes*(c+1) entries
+  int64_t node_total[kHostMaxNodes];
+  int64_t regret[MD];
+  int64_t vals[2];          // host_value of identity, greedy
+  int64_t incumbent_value;
+  int64_t root_lb;          // the bound at the root: no leaf is below it
+  int32_t order[MD], ident[MD], greedy[MD], incumbent[MD];
+  uint8_t no[MD * kHostMaxNodes];   // [k][j] j-th candidate: descending gain, ties by node
+  uint8_t pos[MD * kHostMaxNodes];  // [k][node] inverse of no
+};
+
+// argmax over lanes of v (v >= -1), lowest lane on ties
+__device__ __forceinline__ int warp_argmax_first(int64_t v) {
+  int bl = threadIdx.x & 31;
+  int64_t bv = v;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t ov = __shfl_xor_sync(~0u, bv, o);
+    const int ol = __shfl_xor_sync(~0u, bl, o);
+    if (ov > bv || (ov == bv && ol < bl)) {
+      bv = ov;
+      bl = ol;
+    }
   }
-  return worst;
+  return bl;
 }
 
-// gain, totals, order, incumbents (topology.cpp:195-262): one thread, d <= 64
-__global__ void k_host_prep(int d, int c, const int64_t* __restrict__ V, HostState* H) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int nodes = d / c;
-  H->d = d;
-  H->c = c;
-  H->nodes = nodes;
-  for (int n = 0; n < nodes; ++n) {
-    H->node_total[n] = 0;
-    for (int b = 0; b < d; ++b) H->gain[n * d + b] = 0;
+// S.V must be filled (and a __syncthreads() passed); blockDim.x >= 96 and >= d.
+template <int MD>
+__device__ void prep_run(Prep<MD>& S, int d, int c) {
+  const int nodes = d / c, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int i = t; i < nodes * d; i += blockDim.x) {
+    const int nd = i / d, b = i % d;
+    int64_t g = 0;
+    for (int r = nd * c; r < (nd + 1) * c; ++r) g += static_cast<int64_t>(S.V[r * d + b]);
+    S.gain[i] = g;
   }
-  for (int i = 0; i < d; ++i)
-    for (int b = 0; b < d; ++b) {
-      H->gain[(i / c) * d + b] += V[i * d + b];
-      H->node_total[i / c] += V[i * d + b];
-    }
-  int64_t regret[kHostMaxD];
-  for (int b = 0; b < d; ++b) {
+  __syncthreads();
+  if (t < nodes) {
+    int64_t tot = 0;
+    for (int b = 0; b < d; ++b) tot += S.gain[t * d + b];
+    S.node_total[t] = tot;
+  }
+  if (t < d) {  // top - second gain over the nodes
     int64_t top = 0, second = 0;
-    for (int n = 0; n < nodes; ++n) {
-      const int64_t g = H->gain[n * d + b];
+    for (int nd = 0; nd < nodes; ++nd) {
+      const int64_t g = S.gain[nd * d + t];
       if (g > top) {
         second = top;
         top = g;
@@ -117,77 +143,48 @@ __global__ void k_host_prep(int d, int c, const int64_t* __restrict__ V, HostSta
         second = g;
       }
     }
-    regret[b] = top - second;
-    H->order[b] = b;
+    S.regret[t] = top - second;
   }
-  for (int i = 1; i < d; ++i) {  // stable insertion sort, descending regret
-    const int v = H->order[i];
-    int j = i - 1;
-    while (j >= 0 && regret[H->order[j]] < regret[v]) {
-      H->order[j + 1] = H->order[j];
-      --j;
-    }
-    H->order[j + 1] = v;
+  __syncthreads();
+  if (t < d) {  // stable order by descending regret (the reference's insertion sort)
+    int r = 0;
+    for (int b = 0; b < d; ++b) r += S.regret[b] > S.regret[t] || (S.regret[b] == S.regret[t] && b < t);
+    S.order[r] = t;
+    S.ident[t] = t / c;
   }
-  int32_t ident[kHostMaxD], greedy[kHostMaxD];
-  int room[kHostMaxD];
-  for (int b = 0; b < d; ++b) ident[b] = b / c;
-  for (int n = 0; n < nodes; ++n) room[n] = c;
-  for (int k = 0; k < d; ++k) {
-    const int b = H->order[k];
-    int pick = -1;
-    int64_t pg = -1;
-    for (int n = 0; n < nodes; ++n)
-      if (room[n] > 0 && H->gain[n * d + b] > pg) {
-        pick = n;
-        pg = H->gain[n * d + b];
+  __syncthreads();
+  if (warp == 0) {  // greedy incumbent: each batch in order to the best node with room
+    int room = lane < nodes ? c : 0;
+    for (int k = 0; k < d; ++k) {
+      const int b = S.order[k];
+      const int pick = warp_argmax_first(room > 0 ? S.gain[lane * d + b] : -1);
+      if (lane == pick) {
+        --room;
+        S.greedy[b] = pick;
       }
-    greedy[b] = pick;
-    room[pick] -= 1;
-  }
-  const int64_t vi = host_value(*H, ident), vg = host_value(*H, greedy);
-  const bool g_better = vg < vi;  // offer(greedy) replaces only when strictly better
-  for (int b = 0; b < d; ++b) H->incumbent[b] = g_better ? greedy[b] : ident[b];
-  H->incumbent_value = g_better ? vg : vi;
-  H->best_value = static_cast<unsigned long long>(H->incumbent_value);
-  H->visits = 0;
-  H->overflow = 0;
-  H->have_best = 0;
-  int k0 = 0;
-  long long tasks = 1;
-  while (k0 < d && tasks * nodes <= kHostTasks) {
-    tasks *= nodes;
-    ++k0;
-  }
-  H->k0 = k0;
-  H->tasks = tasks;
-}
-
-// Search tables: thread k < d builds depth k's candidate order (stable sort of
-// the nodes by descending gain for batch order[k]); thread n < nodes builds
-// og[.][n][.] from the deepest level up, keeping its top-c gains sorted.
-__global__ void k_host_tables(HostState* __restrict__ H) {
-  const int d = H->d, c = H->c, nodes = H->nodes, t = threadIdx.x;
-  if (t < d) {
-    const int b = H->order[t];
-    uint8_t* no = H->no + t * nodes;
-    for (int n = 0; n < nodes; ++n) {
-      H->g2[t * nodes + n] = H->gain[n * d + b];
-      int j = n - 1;  // insertion: strictly larger gains first, ties keep node order
-      while (j >= 0 && H->gain[no[j] * d + b] < H->gain[n * d + b]) {
-        no[j + 1] = no[j];
-        --j;
-      }
-      no[j + 1] = static_cast<uint8_t>(n);
+      __syncwarp();
     }
-    for (int j = 0; j < nodes; ++j) H->pos[t * nodes + no[j]] = static_cast<uint8_t>(j);
-  }
-  if (t < nodes) {
-    int64_t top[kHostMaxD];
+  } else if (warp == 1) {  // per depth: candidate nodes by descending gain, ties by node
+    for (int k = lane; k < d; k += 32) {
+      const int b = S.order[k];
+      uint8_t* no = S.no + k * nodes;
+      for (int nd = 0; nd < nodes; ++nd) {
+        S.g2[k * nodes + nd] = S.gain[nd * d + b];
+        int j = nd - 1;
+        while (j >= 0 && S.gain[no[j] * d + b] < S.gain[nd * d + b]) {
+          no[j + 1] = no[j];
+          --j;
+        }
+        no[j + 1] = static_cast<uint8_t>(nd);
+      }
+      for (int j = 0; j < nodes; ++j) S.pos[k * nodes + no[j]] = static_cast<uint8_t>(j);
+    }
+  } else if (warp == 2 && lane < nodes) {  // og[k][node][r], deepest level first
+    int64_t top[MD];
     int have = 0;
     for (int k = d; k >= 0; --k) {
-      if (k < d) {  // insert gain of order[k]
-        const int64_t g = H->gain[t * d + H->order[k]];
+      if (k < d) {
+        const int64_t g = S.gain[lane * d + S.order[k]];
         int j = -1;
         if (have < c) j = have++;
         else if (top[c - 1] < g) j = c - 1;  // else not in the top c (sums unchanged on ties)
@@ -199,7 +196,7 @@ __global__ void k_host_tables(HostState* __restrict__ H) {
           top[j] = g;
         }
       }
-      int64_t* og = H->og + (static_cast<size_t>(k) * nodes + t) * (c + 1);
+      int64_t* og = S.og + (static_cast<size_t>(k) * nodes + lane) * (c + 1);
       int64_t acc = 0;
       og[0] = 0;
       for (int r = 1; r <= c; ++r) {
@@ -208,6 +205,48 @@ __global__ void k_host_tables(HostState* __restrict__ H) {
       }
     }
   }
+  __syncthreads();
+  if (warp < 2) {  // host_value: worst node egress of identity (warp 0) and greedy (warp 1)
+    const int32_t* asg = warp == 0 ? S.ident : S.greedy;
+    int64_t e = INT64_MIN;
+    if (lane < nodes) {
+      e = S.node_total[lane];
+      for (int b = 0; b < d; ++b)
+        if (asg[b] == lane) e -= S.gain[lane * d + b];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int64_t x = __shfl_xor_sync(~0u, e, o);
+      e = x > e ? x : e;
+    }
+    if (lane == 0) S.vals[warp] = e;
+  } else if (warp == 2) {  // lower bound at the root
+    int64_t e = lane < nodes ? S.node_total[lane] - S.og[static_cast<size_t>(lane) * (c + 1) + c] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const int64_t x = __shfl_xor_sync(~0u, e, o);
+      e = x > e ? x : e;
+    }
+    if (lane == 0) S.root_lb = e > 0 ? e : 0;
+  }
+  __syncthreads();
+  const bool g_better = S.vals[1] < S.vals[0];  // offer(greedy) replaces only when strictly better
+  if (t < d) S.incumbent[t] = g_better ? S.greedy[t] : S.ident[t];
+  if (t == 0) S.incumbent_value = g_better ? S.vals[1] : S.vals[0];
+  __syncthreads();
+}
+
+// volume matrix (topology.cpp:40-53) into S.V: from the items, or a given d x d
+template <int MD>
+__device__ void prep_volume(Prep<MD>& S, int d, int64_t n, const int64_t* len, const int32_t* origin,
+                            const int32_t* dest, const int64_t* Vin) {
+  for (int i = threadIdx.x; i < d * d; i += blockDim.x)
+    S.V[i] = Vin ? static_cast<unsigned long long>(Vin[i]) : 0ull;
+  __syncthreads();
+  if (!Vin)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+      atomicAdd(&S.V[origin[i] * d + dest[i]], static_cast<unsigned long long>(len[i]));
+  __syncthreads();
 }
 
 // per warp: choice stack ch[64] (u8), then avail[64] and donated[64] (u32 masks)
@@ -444,25 +483,66 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
   if (lane == 0) atomicAdd(&H.visits, visits & 65535);
 }
 
-// Before each pass. The queue's publish flags are cleared too: the state lives
-// in the reused workspace arena, and a flag left over from an earlier search
-// (same pass, same slot) would let a reader take a path before it is written.
-__global__ void k_host_reset(HostState* __restrict__ H) {
-  for (int i = threadIdx.x; i < kHostQueue; i += blockDim.x) H->q_ready[i] = 0u;
-  if (threadIdx.x == 0) {
+
+// One CTA: volume matrix, preparation, search state of both passes.
+__global__ void __launch_bounds__(1024, 1) k_host_setup(int d, int c, int64_t n,
+                                                        const int64_t* __restrict__ len,
+                                                        const int32_t* __restrict__ origin,
+                                                        const int32_t* __restrict__ dest,
+                                                        const int64_t* __restrict__ Vin,
+                                                        int64_t* __restrict__ Vout, HostState* H) {
+  extern __shared__ __align__(16) unsigned char setup_raw[];
+  Prep<kHostMaxD>& S = *reinterpret_cast<Prep<kHostMaxD>*>(setup_raw);
+  const int nodes = d / c, t = threadIdx.x;
+  prep_volume(S, d, n, len, origin, dest, Vin);
+  if (Vout)
+    for (int i = t; i < d * d; i += blockDim.x) Vout[i] = static_cast<int64_t>(S.V[i]);
+  prep_run(S, d, c);
+  for (int i = t; i < nodes * d; i += blockDim.x) {
+    H->gain[i] = S.gain[i];
+    H->g2[i] = S.g2[i];
+    H->no[i] = S.no[i];
+    H->pos[i] = S.pos[i];
+  }
+  for (int i = t; i < (d + 1) * nodes * (c + 1); i += blockDim.x) H->og[i] = S.og[i];
+  if (t < nodes) H->node_total[t] = S.node_total[t];
+  if (t < d) {
+    H->order[t] = S.order[t];
+    H->incumbent[t] = S.incumbent[t];
+  }
+  for (int i = t; i < kHostQueue; i += blockDim.x) H->q_ready[i] = 0u;
+  if (t == 0) {
+    H->d = d;
+    H->c = c;
+    H->nodes = nodes;
+    H->incumbent_value = S.incumbent_value;
+    H->best_value = static_cast<unsigned long long>(S.incumbent_value);
+    H->visits = 0;
+    H->overflow = 0;
+    H->have_best = 0;
+    int k0 = 0;
+    long long tasks = 1;
+    while (k0 < d && tasks * nodes <= kHostTasks) {
+      tasks *= nodes;
+      ++k0;
+    }
+    if (S.root_lb >= S.incumbent_value) tasks = 0;  // no leaf can beat the incumbents
+    H->k0 = k0;
+    H->tasks = tasks;
     H->task_counter = 0;
     H->q_head = H->q_tail = 0;
-    H->pending = static_cast<int>(H->tasks);
+    H->pending = static_cast<int>(tasks);
     H->idle = 0;
     H->lock = 0;
+    H->done_ctas = 0;
   }
 }
 
 __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restrict__ Hp, int pass) {
   extern __shared__ __align__(16) unsigned char host_raw[];
   HostState& H = *Hp;
-  if (H.overflow) return;
-  if (pass == 2 && static_cast<long long>(H.best_value) >= H.incumbent_value) return;
+  // pass 1 CTAs never leave early: the last one to finish resets the queue
+  if (pass == 2 && (H.overflow || static_cast<long long>(H.best_value) >= H.incumbent_value)) return;
   const HostSmem T = host_load_tables(H, host_raw);
   const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   unsigned char* ws = host_raw + host_table_bytes(H.d, H.c) + warp * kWarpStack;
@@ -510,9 +590,10 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
     int root = 0;
     bool ok = true;
     if (t >= 0) {  // initial prefix: digit k = candidate position among nodes with room
-      long long div = H.tasks / nodes;
+      const int ti = static_cast<int>(t);
+      int div = static_cast<int>(H.tasks) / nodes;
       for (int k = 0; k < k0; ++k) {
-        const int p = static_cast<int>((t / (div > 0 ? div : 1)) % nodes);
+        const int p = (ti / (div > 0 ? div : 1)) % nodes;
         div /= nodes;
         const unsigned pm =
             __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
@@ -566,107 +647,149 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
       atomicSub(&H.pending, 1);
     }
   }
-}
-
-// Final hosting, batch -> instance map, egress figures; then the result remap.
-__global__ void k_host_finish(const HostState* __restrict__ Hp, const int64_t* __restrict__ V,
-                              int32_t* __restrict__ hosting, int32_t* __restrict__ b2i,
-                              int64_t* __restrict__ info) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const HostState& H = *Hp;
-  int32_t a[kHostMaxD];
-  const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value ||
-                         H.overflow || !H.have_best;
-  for (int b = 0; b < H.d; ++b) a[b] = H.incumbent[b];
-  if (!incumbent)
-    for (int l = 0; l < H.d; ++l) a[H.order[l]] = H.no[l * H.nodes + H.best_path[l]];
-  int next[kHostMaxD];
-  for (int n = 0; n < H.nodes; ++n) next[n] = n * H.c;
-  for (int b = 0; b < H.d; ++b) {  // topology.cpp:283-290: ascending batch order in a node
-    hosting[b] = a[b];
-    b2i[b] = next[a[b]]++;
-  }
-  int64_t worst = 0, base = 0;  // inter_node_egress of the solution and of identity hosting
-  for (int n = 0; n < H.nodes; ++n) {
-    int64_t e = 0, e0 = 0;
-    for (int i = n * H.c; i < (n + 1) * H.c; ++i)
-      for (int b = 0; b < H.d; ++b) {
-        if (a[b] != n) e += V[i * H.d + b];
-        if (b / H.c != n) e0 += V[i * H.d + b];
-      }
-    worst = e > worst ? e : worst;
-    base = e0 > base ? e0 : base;
-  }
-  info[0] = worst;
-  info[1] = base;
-  info[2] = H.overflow ? -1 : (incumbent ? 0 : 1);  // -1: visit budget hit, incumbent kept
-  info[3] = static_cast<int64_t>(H.visits);
-#ifdef ORCH_HOST_DEBUG
-  printf("hosting: best %llu inc %lld visits %llu overflow %d k0 %d tasks %lld queued %u\n",
-         H.best_value, (long long)H.incumbent_value, H.visits, H.overflow, H.k0, H.tasks,
-         H.q_tail);
-#endif
-}
-
-// Relabel destination batches: item dest -> b2i[dest]; per-batch arrays and
-// the destination CSR permuted accordingly (contents unchanged).
-__global__ void k_host_remap(int d, int64_t n, const int32_t* __restrict__ b2i,
-                             int32_t* __restrict__ dest_inst, const int32_t* __restrict__ old_cnt,
-                             const int64_t* __restrict__ old_len, const int64_t* __restrict__ old_tok,
-                             const double* __restrict__ old_cost,
-                             const int32_t* __restrict__ old_off,
-                             const int32_t* __restrict__ old_mem, int32_t* __restrict__ bin_count,
-                             int64_t* __restrict__ bin_len, int64_t* __restrict__ bin_tokens,
-                             double* __restrict__ bin_cost, int32_t* __restrict__ bin_offset,
-                             int32_t* __restrict__ bin_member) {
-  __shared__ int32_t inv[kHostMaxD];
-  __shared__ int32_t noff[kHostMaxD + 1];
-  if (threadIdx.x < d) inv[b2i[threadIdx.x]] = threadIdx.x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int j = 0; j < d; ++j) {
-      noff[j] = acc;
-      acc += old_cnt[inv[j]];
+  if (pass == 1) {  // the last CTA out resets the work distribution for pass 2
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&H.done_ctas, 1) == static_cast<int>(gridDim.x) - 1;
     }
-    noff[d] = acc;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      H.task_counter = 0;
+      H.q_head = H.q_tail = 0;
+      H.pending = static_cast<int>(H.tasks);
+      H.idle = 0;
+      H.lock = 0;
+      H.done_ctas = 0;
+      __threadfence();
+    }
   }
-  __syncthreads();
-  if (threadIdx.x < d) {
-    const int j = threadIdx.x, b = inv[j];
-    bin_count[j] = old_cnt[b];
-    if (bin_len) bin_len[j] = old_len[b];
-    if (bin_tokens) bin_tokens[j] = old_tok[b];
-    if (bin_cost) bin_cost[j] = old_cost[b];
-  }
-  if (threadIdx.x <= d) bin_offset[threadIdx.x] = noff[threadIdx.x];
-  for (int j = 0; j < d; ++j) {
-    const int b = inv[j];
-    for (int k = threadIdx.x; k < old_off[b + 1] - old_off[b]; k += blockDim.x)
-      bin_member[noff[j] + k] = old_mem[old_off[b] + k];
-  }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dest_inst[i] = b2i[dest_inst[i]];
 }
 
-__global__ void k_vol(int d, int64_t n, const int64_t* __restrict__ len,
-                      const int32_t* __restrict__ origin, const int32_t* __restrict__ dest,
-                      unsigned long long* __restrict__ V) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&V[static_cast<size_t>(origin[i]) * d + dest[i]],
-              static_cast<unsigned long long>(len[i]));
+
+// Final hosting, batch -> instance map (topology.cpp:283-290), egress figures;
+// with a balance result, its relabelling (batch b becomes instance b2i[b]).
+constexpr int kFinMaxItems = 10240;  // destination CSR members kept in shared memory (static, < 48 KB)
+struct FinSmem {
+  unsigned long long e[kHostMaxNodes], e0[kHostMaxNodes];
+  int32_t a[kHostMaxD], b2i[kHostMaxD], inv[kHostMaxD], noff[kHostMaxD + 1];
+  int32_t ocnt[kHostMaxD], ooff[kHostMaxD + 1];
+  int64_t olen[kHostMaxD], otok[kHostMaxD];
+  double ocost[kHostMaxD];
+  int32_t members[kFinMaxItems];
+};
+
+struct RemapArgs {
+  int64_t n;
+  int32_t* dest_inst;
+  int32_t* bin_count;
+  int64_t* bin_len;
+  int64_t* bin_tokens;
+  double* bin_cost;
+  int32_t* bin_offset;
+  int32_t* bin_member;
+  int32_t* scratch;  // n members when n > kFinMaxItems
+};
+
+__global__ void __launch_bounds__(1024, 1) k_host_finish(const HostState* __restrict__ Hp,
+                                                         const int64_t* __restrict__ V,
+                                                         int32_t* __restrict__ hosting,
+                                                         int32_t* __restrict__ b2i_out,
+                                                         int64_t* __restrict__ info, RemapArgs r) {
+  __shared__ FinSmem F;
+  const HostState& H = *Hp;
+  const int d = H.d, c = H.c, nodes = H.nodes, t = threadIdx.x;
+  const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value || H.overflow ||
+                         !H.have_best;
+  const bool remap = r.dest_inst != nullptr;
+  int32_t* mem = r.n > kFinMaxItems ? r.scratch : F.members;
+  if (remap) {  // the old per-batch arrays and CSR, before anything is overwritten
+    if (t < d) {
+      F.ocnt[t] = r.bin_count[t];
+      if (r.bin_len) F.olen[t] = r.bin_len[t];
+      if (r.bin_tokens) F.otok[t] = r.bin_tokens[t];
+      if (r.bin_cost) F.ocost[t] = r.bin_cost[t];
+    }
+    if (t <= d) F.ooff[t] = r.bin_offset[t];
+    for (int64_t i = t; i < r.n; i += blockDim.x) mem[i] = r.bin_member[i];
+  }
+  if (t < d) F.a[t] = H.incumbent[t];
+  if (t < nodes) F.e[t] = F.e0[t] = 0;
+  __syncthreads();
+  if (!incumbent && t < d) F.a[H.order[t]] = H.no[t * nodes + H.best_path[t]];
+  __syncthreads();
+  if (t == 0) {
+    int next[kHostMaxNodes];
+    for (int nd = 0; nd < nodes; ++nd) next[nd] = nd * c;
+    for (int b = 0; b < d; ++b) {
+      const int nb = next[F.a[b]]++;
+      F.b2i[b] = nb;
+      F.inv[nb] = b;
+    }
+  }
+  for (int i = t; i < d * d; i += blockDim.x) {  // inter_node_egress of the solution and identity
+    const int src = i / d, b = i % d, nd = src / c;
+    const unsigned long long v = static_cast<unsigned long long>(V[i]);
+    if (v) {
+      if (F.a[b] != nd) atomicAdd(&F.e[nd], v);
+      if (b / c != nd) atomicAdd(&F.e0[nd], v);
+    }
+  }
+  __syncthreads();
+  if (t < d) {
+    hosting[t] = F.a[t];
+    b2i_out[t] = F.b2i[t];
+  }
+  if (t == 0) {
+    unsigned long long worst = 0, base = 0;
+    for (int nd = 0; nd < nodes; ++nd) {
+      worst = F.e[nd] > worst ? F.e[nd] : worst;
+      base = F.e0[nd] > base ? F.e0[nd] : base;
+    }
+    info[0] = static_cast<int64_t>(worst);
+    info[1] = static_cast<int64_t>(base);
+    info[2] = H.overflow ? -1 : (incumbent ? 0 : 1);  // -1: visit budget hit, incumbent kept
+    info[3] = static_cast<int64_t>(H.visits);
+    if (remap) {
+      int acc = 0;
+      for (int j = 0; j < d; ++j) {
+        F.noff[j] = acc;
+        acc += F.ocnt[F.inv[j]];
+      }
+      F.noff[d] = acc;
+    }
+  }
+#ifdef ORCH_HOST_DEBUG
+  if (t == 0)
+    printf("hosting: best %llu inc %lld visits %llu overflow %d k0 %d tasks %lld queued %u\n",
+           H.best_value, (long long)H.incumbent_value, H.visits, H.overflow, H.k0, H.tasks, H.q_tail);
+#endif
+  if (!remap) return;
+  __syncthreads();
+  if (t < d) {
+    const int b = F.inv[t];
+    r.bin_count[t] = F.ocnt[b];
+    if (r.bin_len) r.bin_len[t] = F.olen[b];
+    if (r.bin_tokens) r.bin_tokens[t] = F.otok[b];
+    if (r.bin_cost) r.bin_cost[t] = F.ocost[b];
+  }
+  if (t <= d) r.bin_offset[t] = F.noff[t];
+  for (int j = 0; j < d; ++j) {
+    const int b = F.inv[j];
+    const int cnt = F.ooff[b + 1] - F.ooff[b];
+    for (int k = t; k < cnt; k += blockDim.x) r.bin_member[F.noff[j] + k] = mem[F.ooff[b] + k];
+  }
+  for (int64_t i = t; i < r.n; i += blockDim.x) r.dest_inst[i] = F.b2i[r.dest_inst[i]];
 }
 
 // ------------------------------------------------ one-CTA node-wise path
 // For small searches (d <= 32, <= 2^18 leaves, n <= 12288: every C2 shape on
-// 2/4/8 GPUs) the whole of orch_nodewise runs in ONE kernel, in shared memory:
-// volume matrix -> gains, regret order, incumbents, search tables -> two-pass
-// branch and bound (32 warps, lane = node, DFS-ordered prefix tasks) -> hosting,
-// batch_to_instance, egress figures -> relabelling of the balance result.
-// The metadata chain runs beside the NVLink row exchange, where every global
-// round trip costs several microseconds; this path pays about four of them
-// instead of a dozen launches and copies. Same answer as the multi-CTA path
-// (first optimal leaf in DFS order, the incumbents otherwise).
+// 2/4/8 GPUs) the whole of orch_nodewise is ONE kernel in shared memory:
+// volume matrix -> preparation -> two-pass branch and bound (32 warps, lane =
+// node, prefix tasks claimed in DFS order) -> hosting, batch_to_instance,
+// egress figures -> relabelling of the balance result. Same answer as the
+// multi-CTA path (first optimal leaf in DFS order, else the incumbents).
 constexpr int kNwThreads = 1024;
 constexpr int kNwWarps = kNwThreads / 32;
 constexpr int kNwMaxD = 32;
@@ -675,29 +798,18 @@ constexpr int kNwTasks = 64;  // at least two prefix tasks per warp
 constexpr double kNwMaxLeaves = 262144.0;
 
 struct NwSmem {
-  unsigned long long V[kNwMaxD * kNwMaxD];  // [src instance][dest batch]
-  int64_t gain[kNwMaxD * kNwMaxD];          // [node][batch]
-  int64_t g2[kNwMaxD * kNwMaxD];            // [k][node]
-  int64_t og[(kNwMaxD + 1) * 2 * kNwMaxD];  // [k][node][r], (d+1)*nodes*(c+1) <= (d+1)*2d
-  int64_t node_total[kNwMaxD];
-  int64_t regret[kNwMaxD];
+  Prep<kNwMaxD> p;
   int64_t node_e[kNwMaxD], node_e0[kNwMaxD];
-  int64_t incumbent_value;
   unsigned long long best;  // pass 1: best value so far
   unsigned long long visits;
-  int32_t order[kNwMaxD];
-  int32_t ident[kNwMaxD], greedy[kNwMaxD], incumbent[kNwMaxD], a[kNwMaxD];
-  int32_t b2i[kNwMaxD], inv[kNwMaxD], noff[kNwMaxD + 1];
+  int tasks, k0, best_task, lock;
+  unsigned task_ctr;
+  int32_t a[kNwMaxD], b2i[kNwMaxD], inv[kNwMaxD], noff[kNwMaxD + 1];
   int32_t ocnt[kNwMaxD], ooff[kNwMaxD + 1];
   int64_t olen[kNwMaxD], otok[kNwMaxD];
   double ocost[kNwMaxD];
-  uint8_t no[kNwMaxD * kNwMaxD];   // [k][j] j-th candidate node of depth k
-  uint8_t pos[kNwMaxD * kNwMaxD];  // [k][node]
-  uint8_t ch[kNwWarps][kNwMaxD];   // per-warp DFS path (candidate positions)
+  uint8_t ch[kNwWarps][kNwMaxD];  // per-warp DFS path (candidate positions)
   uint8_t best_path[kNwMaxD];
-  int64_t vals[2];
-  int tasks, k0, best_task, lock;
-  unsigned task_ctr;
   int32_t members[kNwMaxItems];
 };
 
@@ -717,30 +829,14 @@ struct NwArgs {
   int64_t* info;
 };
 
-// argmax over lanes of v (v >= -1), lowest lane on ties
-__device__ __forceinline__ int warp_argmax_first(int64_t v) {
-  int lane = threadIdx.x & 31;
-  int64_t bv = v;
-  int bl = lane;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const int64_t ov = __shfl_xor_sync(~0u, bv, o);
-    const int ol = __shfl_xor_sync(~0u, bl, o);
-    if (ov > bv || (ov == bv && ol < bl)) {
-      bv = ov;
-      bl = ol;
-    }
-  }
-  return bl;
-}
-
-// DFS of the subtree below ch[0, root) for one warp (lane = node); the
+// DFS of the subtree below ch[0, root) for one warp (lane = node): the
 // prune rules and visiting order of host_dfs, without donation.
 __device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, int room,
                        int64_t gained, int d, int c, int nodes, uint8_t* ch) {
+  const Prep<kNwMaxD>& T = S.p;
   const int lane = threadIdx.x & 31;
   const bool active = lane < nodes;
-  const int64_t total = active ? S.node_total[lane] : 0;
+  const int64_t total = active ? T.node_total[lane] : 0;
   unsigned long long visits = 0;
   int k = root, jstart = 0;
   bool descend = true;
@@ -751,7 +847,7 @@ __device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, i
           __shfl_sync(~0u, lane == 0 ? *reinterpret_cast<volatile int*>(&S.best_task) : 0, 0) < task)
         break;  // an earlier task already holds a V*-leaf
       const int64_t term =
-          active ? total - gained - S.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room] : 0;
+          active ? total - gained - T.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room] : 0;
       const int64_t lb = warp_max_nonneg(term);
       bool prune;
       if (pass == 1) {
@@ -771,7 +867,8 @@ __device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, i
             }
           __syncwarp();
           __threadfence_block();
-          const int won = __shfl_sync(~0u, lane == 0 ? (task < *reinterpret_cast<volatile int*>(&S.best_task)) : 0, 0);
+          const int won = __shfl_sync(
+              ~0u, lane == 0 ? (task < *reinterpret_cast<volatile int*>(&S.best_task)) : 0, 0);
           if (won) {
             for (int l = lane; l < d; l += 32) S.best_path[l] = ch[l];
             __threadfence_block();
@@ -794,15 +891,15 @@ __device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, i
       if (k == root) break;
       --k;
       const int j = ch[k];
-      const int m = S.no[k * nodes + j];
+      const int m = T.no[k * nodes + j];
       if (lane == m) {
         ++room;
-        gained -= S.g2[k * nodes + m];
+        gained -= T.g2[k * nodes + m];
       }
       jstart = j + 1;
     }
     const unsigned av =
-        __reduce_or_sync(~0u, (active && room > 0) ? (1u << S.pos[k * nodes + lane]) : 0u);
+        __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
     const unsigned pm = jstart >= 32 ? 0u : av & (~0u << jstart);
     if (!pm) {
       descend = false;
@@ -812,10 +909,10 @@ __device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, i
     __syncwarp();
     if (lane == 0) ch[k] = static_cast<uint8_t>(j);
     __syncwarp();
-    const int m = S.no[k * nodes + j];
+    const int m = T.no[k * nodes + j];
     if (lane == m) {
       --room;
-      gained += S.g2[k * nodes + m];
+      gained += T.g2[k * nodes + m];
     }
     ++k;
     descend = true;
@@ -823,8 +920,9 @@ __device__ void nw_dfs(NwSmem& S, int pass, int64_t vstar, int task, int root, i
   if (lane == 0) atomicAdd(&S.visits, visits);
 }
 
-// one pass over the prefix tasks (DFS order), dynamic claiming
+// one pass over the prefix tasks, claimed in DFS order
 __device__ void nw_pass(NwSmem& S, int pass, int64_t vstar, int d, int c, int nodes) {
+  const Prep<kNwMaxD>& T = S.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool active = lane < nodes;
   uint8_t* ch = S.ch[warp];
@@ -835,7 +933,7 @@ __device__ void nw_pass(NwSmem& S, int pass, int64_t vstar, int d, int c, int no
     if (t >= S.tasks) break;
     if (pass == 2 &&
         __shfl_sync(~0u, lane == 0 ? *reinterpret_cast<volatile int*>(&S.best_task) : 0, 0) < t)
-      break;  // tasks are claimed in DFS order: the rest sort after the best leaf
+      break;  // the remaining tasks sort after the best leaf
     int room = active ? c : 0;
     int64_t gained = 0;
     bool ok = true;
@@ -844,7 +942,7 @@ __device__ void nw_pass(NwSmem& S, int pass, int64_t vstar, int d, int c, int no
       const int p = (t / (div > 0 ? div : 1)) % nodes;
       div /= nodes;
       const unsigned pm =
-          __reduce_or_sync(~0u, (active && room > 0) ? (1u << S.pos[k * nodes + lane]) : 0u);
+          __reduce_or_sync(~0u, (active && room > 0) ? (1u << T.pos[k * nodes + lane]) : 0u);
       if (__popc(pm) <= p) {
         ok = false;
         break;
@@ -855,10 +953,10 @@ __device__ void nw_pass(NwSmem& S, int pass, int64_t vstar, int d, int c, int no
       __syncwarp();
       if (lane == 0) ch[k] = static_cast<uint8_t>(j);
       __syncwarp();
-      const int m = S.no[k * nodes + j];
+      const int m = T.no[k * nodes + j];
       if (lane == m) {
         --room;
-        gained += S.g2[k * nodes + m];
+        gained += T.g2[k * nodes + m];
       }
     }
     if (ok) nw_dfs(S, pass, vstar, t, S.k0, room, gained, d, c, nodes, ch);
@@ -868,18 +966,9 @@ __device__ void nw_pass(NwSmem& S, int pass, int64_t vstar, int d, int c, int no
 __global__ void __launch_bounds__(kNwThreads, 1) k_nodewise_small(NwArgs a) {
   extern __shared__ __align__(16) unsigned char nw_raw[];
   NwSmem& S = *reinterpret_cast<NwSmem*>(nw_raw);
+  Prep<kNwMaxD>& T = S.p;
   const int d = a.d, c = a.c, nodes = d / c, n = a.n, t = threadIdx.x;
-#ifdef ORCH_NW_STAMPS
-  uint64_t ts[8];
-  int nts = 0;
-  auto stamp = [&] { if (t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[nts++])); };
-  stamp();
-#else
-  auto stamp = [] {};
-#endif
-  const int lane = t & 31, warp = t >> 5;
-  // ---- volume matrix (topology.cpp:40-53) and the old per-batch arrays
-  for (int i = t; i < d * d; i += kNwThreads) S.V[i] = 0;
+  // the old per-batch arrays and CSR, before anything is overwritten
   if (t < d) {
     S.ocnt[t] = a.bin_count[t];
     if (a.bin_len) S.olen[t] = a.bin_len[t];
@@ -887,166 +976,40 @@ __global__ void __launch_bounds__(kNwThreads, 1) k_nodewise_small(NwArgs a) {
     if (a.bin_cost) S.ocost[t] = a.bin_cost[t];
   }
   if (t <= d) S.ooff[t] = a.bin_offset[t];
+  for (int i = t; i < n; i += kNwThreads) S.members[i] = a.bin_member[i];
   if (t == 0) {
     S.visits = 0;
     S.task_ctr = 0;
     S.best_task = INT_MAX;
     S.lock = 0;
   }
-  __syncthreads();
-  for (int i = t; i < n; i += kNwThreads) {
-    S.members[i] = a.bin_member[i];
-    atomicAdd(&S.V[a.origin[i] * d + a.dest_inst[i]], static_cast<unsigned long long>(a.len[i]));
-  }
-  __syncthreads();
-  stamp();
-  // ---- gains, node totals (topology.cpp:195-262)
-  for (int i = t; i < nodes * d; i += kNwThreads) {
-    const int nd = i / d, b = i % d;
-    int64_t g = 0;
-    for (int r = nd * c; r < (nd + 1) * c; ++r) g += static_cast<int64_t>(S.V[r * d + b]);
-    S.gain[i] = g;
-  }
-  __syncthreads();
-  if (t < nodes) {
-    int64_t tot = 0;
-    for (int b = 0; b < d; ++b) tot += S.gain[t * d + b];
-    S.node_total[t] = tot;
-  }
-  if (t < d) {
-    int64_t top = 0, second = 0;
-    for (int nd = 0; nd < nodes; ++nd) {
-      const int64_t g = S.gain[nd * d + t];
-      if (g > top) {
-        second = top;
-        top = g;
-      } else if (g > second) {
-        second = g;
-      }
-    }
-    S.regret[t] = top - second;
-  }
-  __syncthreads();
-  if (t < d) {  // stable order by descending regret (the reference's insertion sort)
-    int r = 0;
-    for (int b = 0; b < d; ++b)
-      r += S.regret[b] > S.regret[t] || (S.regret[b] == S.regret[t] && b < t);
-    S.order[r] = t;
-    S.ident[t] = t / c;
-  }
-  __syncthreads();
-  if (warp == 0) {  // greedy incumbent: each batch in order to the best node with room
-    int room = lane < nodes ? c : 0;
-    for (int k = 0; k < d; ++k) {
-      const int b = S.order[k];
-      const int pick = warp_argmax_first(room > 0 ? S.gain[lane * d + b] : -1);
-      if (lane == pick) {
-        --room;
-        S.greedy[b] = pick;
-      }
-      __syncwarp();
-    }
-  } else if (warp == 1) {  // search tables, candidate order per depth
-    for (int k = lane; k < d; k += 32) {
-      const int b = S.order[k];
-      uint8_t* no = S.no + k * nodes;
-      for (int nd = 0; nd < nodes; ++nd) {
-        S.g2[k * nodes + nd] = S.gain[nd * d + b];
-        int j = nd - 1;
-        while (j >= 0 && S.gain[no[j] * d + b] < S.gain[nd * d + b]) {
-          no[j + 1] = no[j];
-          --j;
-        }
-        no[j + 1] = static_cast<uint8_t>(nd);
-      }
-      for (int j = 0; j < nodes; ++j) S.pos[k * nodes + no[j]] = static_cast<uint8_t>(j);
-    }
-  } else if (warp == 2 && lane < nodes) {  // og[k][node][r], deepest level first
-    int64_t top[kNwMaxD];
-    int have = 0;
-    for (int k = d; k >= 0; --k) {
-      if (k < d) {
-        const int64_t g = S.gain[lane * d + S.order[k]];
-        int j = -1;
-        if (have < c) j = have++;
-        else if (top[c - 1] < g) j = c - 1;
-        if (j >= 0) {
-          while (j > 0 && top[j - 1] < g) {
-            top[j] = top[j - 1];
-            --j;
-          }
-          top[j] = g;
-        }
-      }
-      int64_t* og = S.og + (static_cast<size_t>(k) * nodes + lane) * (c + 1);
-      int64_t acc = 0;
-      og[0] = 0;
-      for (int r = 1; r <= c; ++r) {
-        if (r <= have) acc += top[r - 1];
-        og[r] = acc;
-      }
-    }
-  }
-  __syncthreads();
-  if (warp < 2) {  // host_value of identity (warp 0) and greedy (warp 1)
-    const int32_t* asg = warp == 0 ? S.ident : S.greedy;
-    int64_t e = INT64_MIN;
-    if (lane < nodes) {
-      e = S.node_total[lane];
-      for (int b = 0; b < d; ++b)
-        if (asg[b] == lane) e -= S.gain[lane * d + b];
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const int64_t x = __shfl_xor_sync(~0u, e, o);
-      e = x > e ? x : e;
-    }
-    if (lane == 0) S.vals[warp] = e;
-  }
-  __syncthreads();
-  if (t < d) {
-    const bool g_better = S.vals[1] < S.vals[0];  // offer(greedy) only when strictly better
-    S.incumbent[t] = g_better ? S.greedy[t] : S.ident[t];
-  }
+  prep_volume(T, d, n, a.len, a.origin, a.dest_inst, nullptr);
+  prep_run(T, d, c);
   if (t == 0) {
-    const bool g_better = S.vals[1] < S.vals[0];
-    S.incumbent_value = g_better ? S.vals[1] : S.vals[0];
-    S.best = static_cast<unsigned long long>(S.incumbent_value);
-    // a few prefix tasks per warp: the trees here are small, and a task costs
-    // its prefix decode even when the bound cuts it at once
-    int k0 = 0, tasks = 1;
+    S.best = static_cast<unsigned long long>(T.incumbent_value);
+    int k0 = 0, tasks = 1;  // a few prefix tasks per warp: these trees are small
     while (k0 < d && tasks < kNwTasks) {
       tasks *= nodes;
       ++k0;
     }
     S.k0 = k0;
-    S.tasks = tasks;
-    // no leaf can beat the incumbents when the root bound already reaches them
-    int64_t lb = 0;
-    for (int nd = 0; nd < nodes; ++nd) {
-      const int64_t e = S.node_total[nd] - S.og[static_cast<size_t>(nd) * (c + 1) + c];
-      lb = e > lb ? e : lb;
-    }
-    if (lb >= S.incumbent_value) S.tasks = 0;
+    S.tasks = T.root_lb >= T.incumbent_value ? 0 : tasks;  // no leaf can beat the incumbents
   }
   __syncthreads();
-  stamp();
   // ---- search: pass 1 finds V*, pass 2 the first V*-leaf in DFS order
   nw_pass(S, 1, 0, d, c, nodes);
   __syncthreads();
-  stamp();
   const int64_t vstar = static_cast<int64_t>(S.best);
-  const bool search2 = vstar < S.incumbent_value;
+  const bool search2 = vstar < T.incumbent_value;
   if (t == 0) S.task_ctr = 0;
   __syncthreads();
   if (search2) nw_pass(S, 2, vstar, d, c, nodes);
   __syncthreads();
-  stamp();
   // ---- hosting, batch -> instance (topology.cpp:283-290), egress figures
   const bool incumbent = !search2 || S.best_task == INT_MAX;
-  if (t < d) S.a[t] = S.incumbent[t];
+  if (t < d) S.a[t] = T.incumbent[t];
   __syncthreads();
-  if (!incumbent && t < d) S.a[S.order[t]] = S.no[t * nodes + S.best_path[t]];
+  if (!incumbent && t < d) S.a[T.order[t]] = T.no[t * nodes + S.best_path[t]];
   __syncthreads();
   if (t == 0) {
     int next[kNwMaxD];
@@ -1062,7 +1025,7 @@ __global__ void __launch_bounds__(kNwThreads, 1) k_nodewise_small(NwArgs a) {
     int64_t e = 0, e0 = 0;
     for (int i = t * c; i < (t + 1) * c; ++i)
       for (int b = 0; b < d; ++b) {
-        const int64_t v = static_cast<int64_t>(S.V[i * d + b]);
+        const int64_t v = static_cast<int64_t>(T.V[i * d + b]);
         if (S.a[b] != t) e += v;
         if (b / c != t) e0 += v;
       }
@@ -1108,17 +1071,6 @@ __global__ void __launch_bounds__(kNwThreads, 1) k_nodewise_small(NwArgs a) {
     for (int k = t; k < cnt; k += kNwThreads) a.bin_member[S.noff[j] + k] = S.members[S.ooff[b] + k];
   }
   for (int i = t; i < n; i += kNwThreads) a.dest_inst[i] = S.b2i[a.dest_inst[i]];
-#ifdef ORCH_NW_STAMPS
-  __syncthreads();
-  stamp();
-  if (t == 0) {
-    static __device__ unsigned calls = 0;
-    if ((atomicAdd(&calls, 1u) % 16) == 15)
-      printf("NWSTAMP d=%d c=%d load %.1f prep %.1f pass1 %.1f pass2 %.1f out %.1f us visits %llu tasks %d\n", d, c,
-             (ts[1] - ts[0]) / 1e3, (ts[2] - ts[1]) / 1e3, (ts[3] - ts[2]) / 1e3, (ts[4] - ts[3]) / 1e3,
-             (ts[5] - ts[4]) / 1e3, S.visits, S.tasks);
-  }
-#endif
 }
 
 bool nodewise_small_fits(int d, int c, int64_t n) {
@@ -1142,22 +1094,23 @@ int check_hosting_args(int d, int c) {
   return ORCH_OK;
 }
 
-int launch_hosting_search(orch_ctx* ctx, int d, int c, const int64_t* V, HostState* H,
-                          cudaStream_t st) {
+// setup + both passes of the multi-CTA search (V from the items, or given)
+int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t* len,
+                          const int32_t* origin, const int32_t* dest, const int64_t* Vin,
+                          int64_t* Vout, HostState* H, cudaStream_t st) {
   const int sm = static_cast<int>(host_smem_bytes(d, c));
   static bool configured = false;
   if (!configured) {
     const int mx = static_cast<int>(host_smem_bytes(kHostMaxD, 2));  // the largest table set
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sizeof(Prep<kHostMaxD>))));
     configured = true;
   }
-  k_host_prep<<<1, 32, 0, st>>>(d, c, V, H);
-  k_host_tables<<<1, kHostMaxD, 0, st>>>(H);
-  k_host_reset<<<1, 1024, 0, st>>>(H);
+  k_host_setup<<<1, 1024, sizeof(Prep<kHostMaxD>), st>>>(d, c, n, len, origin, dest, Vin, Vout, H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
-  k_host_reset<<<1, 1024, 0, st>>>(H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
-  ctx->launches += 6;
+  ctx->launches += 3;
   return ORCH_OK;
 }
 
@@ -1188,9 +1141,9 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
   rc = all.commit(ctx, st);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaMemcpyAsync(V, h_V, sizeof(int64_t) * d * d, cudaMemcpyHostToDevice, st));
-  rc = launch_hosting_search(ctx, d, c, V, H, st);
+  rc = launch_hosting_search(ctx, d, c, 0, nullptr, nullptr, nullptr, V, nullptr, H, st);
   if (rc) return rc;
-  k_host_finish<<<1, 32, 0, st>>>(H, V, hosting, b2i, info);
+  k_host_finish<<<1, 1024, 0, st>>>(H, V, hosting, b2i, info, RemapArgs{});
   ctx->launches += 1;
   ORCH_CUDA_TRY(cudaGetLastError());
   ORCH_CUDA_TRY(cudaMemcpyAsync(h_hosting, hosting, sizeof(int32_t) * d, cudaMemcpyDeviceToHost, st));
@@ -1246,48 +1199,25 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
     ORCH_CUDA_TRY(cudaGetLastError());
     return ORCH_OK;
   }
-  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
   Plan plan;
-  unsigned long long* V;
+  int64_t* V;
   HostState* H;
-  int32_t *hosting, *b2i, *ocnt, *ooff, *omem;
-  int64_t *olen, *otok, *info;
-  double* ocost;
+  int32_t *hosting, *b2i, *scratch = nullptr;
+  int64_t* info;
   plan.add(&V, static_cast<size_t>(d) * d);
   plan.add(&H, 1);
   plan.add_or(&hosting, d_hosting, d);
   plan.add_or(&b2i, d_batch_to_instance, d);
   plan.add_or(&info, d_info, 4);
-  plan.add(&ocnt, d);
-  plan.add(&ooff, d + 1);
-  plan.add(&omem, nn);
-  plan.add(&olen, d);
-  plan.add(&otok, d);
-  plan.add(&ocost, d);
+  if (n > kFinMaxItems) plan.add(&scratch, static_cast<size_t>(n));
   rc = plan.commit(ctx, st);
   if (rc) return rc;
-  ORCH_CUDA_TRY(cudaMemsetAsync(V, 0, sizeof(uint64_t) * d * d, st));
-  if (n > 0)
-    k_vol<<<blocks_for(n, 256), 256, 0, st>>>(d, n, d_len, d_origin, bal->dest_inst, V);
-  const int64_t* dV = reinterpret_cast<const int64_t*>(V);
-  rc = launch_hosting_search(ctx, d, c, dV, H, st);
+  rc = launch_hosting_search(ctx, d, c, n, d_len, d_origin, bal->dest_inst, nullptr, V, H, st);
   if (rc) return rc;
-  k_host_finish<<<1, 32, 0, st>>>(H, dV, hosting, b2i, info);
-  // snapshot the per-batch arrays, then write them back relabelled
-  ORCH_CUDA_TRY(cudaMemcpyAsync(ocnt, bal->bin_count, 4 * d, cudaMemcpyDeviceToDevice, st));
-  ORCH_CUDA_TRY(cudaMemcpyAsync(ooff, bal->bin_offset, 4 * (d + 1), cudaMemcpyDeviceToDevice, st));
-  if (n > 0)
-    ORCH_CUDA_TRY(cudaMemcpyAsync(omem, bal->bin_member, 4 * n, cudaMemcpyDeviceToDevice, st));
-  if (bal->bin_len)
-    ORCH_CUDA_TRY(cudaMemcpyAsync(olen, bal->bin_len, 8 * d, cudaMemcpyDeviceToDevice, st));
-  if (bal->bin_tokens)
-    ORCH_CUDA_TRY(cudaMemcpyAsync(otok, bal->bin_tokens, 8 * d, cudaMemcpyDeviceToDevice, st));
-  if (bal->bin_cost)
-    ORCH_CUDA_TRY(cudaMemcpyAsync(ocost, bal->bin_cost, 8 * d, cudaMemcpyDeviceToDevice, st));
-  k_host_remap<<<1, 256, 0, st>>>(d, n, b2i, bal->dest_inst, ocnt, olen, otok, ocost, ooff, omem,
-                                  bal->bin_count, bal->bin_len, bal->bin_tokens, bal->bin_cost,
-                                  bal->bin_offset, bal->bin_member);
-  ctx->launches += 3;
+  RemapArgs r{n, bal->dest_inst, bal->bin_count, bal->bin_len, bal->bin_tokens, bal->bin_cost,
+              bal->bin_offset, bal->bin_member, scratch};
+  k_host_finish<<<1, 1024, 0, st>>>(H, V, hosting, b2i, info, r);
+  ctx->launches += 1;
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
 }
