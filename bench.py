@@ -225,15 +225,23 @@ def run_b200(args):
         comm_meta = Comm(world, rank, uid[0][0])
         comm_data = Comm(world, rank, uid[0][1])
     # one context (workspace arena) per stream
-    ctx_meta, ctx_data = Context(local), Context(local)
-    gwin = None
+    ctx_data = Context(local)
     P, c, R = world, D_INST // world, CFG["R"]
     batch, phases = build_inputs()
-    if comm_meta is not None and args.gather == "put":
-        gwin = GatherWindow(ctx_meta, comm_meta, max(len(ph[1]) for ph in phases))
-    # the metadata chain is latency-bound and runs beside the row movement:
-    # give its kernels the higher stream priority
-    meta_stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("ORCH_META_PRIO", "-1")))
+    # The metadata chain (gather, balance, hosting, layout) is latency-bound and
+    # runs beside the row movement. Each phase gets its own stream, context and
+    # gather window, so the phases' chains overlap one another (ncclAllGather
+    # on one communicator needs one stream: --gather nccl keeps a single one).
+    per_phase = args.gather == "put" or comm_meta is None
+    prio = int(os.environ.get("ORCH_META_PRIO", "-1"))
+    ms0 = torch.cuda.Stream(device=dev, priority=prio)
+    ctx0 = Context(local)
+    meta_ctx = [Context(local) if per_phase and i else ctx0 for i in range(len(phases))]
+    meta_streams = [torch.cuda.Stream(device=dev, priority=prio) if per_phase and i else ms0
+                    for i in range(len(phases))]
+    gwins = [GatherWindow(meta_ctx[i], comm_meta, len(ph[1]))
+             if comm_meta is not None and args.gather == "put" else None
+             for i, ph in enumerate(phases)]
     data_stream = torch.cuda.Stream(device=dev)
 
     # Per phase: local items (global input positions), and two buffer sets of
@@ -241,7 +249,7 @@ def run_b200(args):
     # on the metadata stream while step i's rows move on the data stream (the
     # paper overlaps the solver with the forward pass).
     st = []
-    for name, L, O, kind, lam, v in phases:
+    for i_ph, (name, L, O, kind, lam, v) in enumerate(phases):
         n = len(L)
         mine = np.nonzero(O // c == rank)[0]
         max_local = int(max(np.bincount(O // c, minlength=P)))
@@ -258,6 +266,7 @@ def run_b200(args):
                          bal=Balance.alloc(D_INST, n, dev), lay=Layout.alloc(P, n, dev),
                          meta_done=torch.cuda.Event(), data_done=torch.cuda.Event())
                     for _ in range(2)]
+        s["ctx"], s["ms"], s["gwin"] = meta_ctx[i_ph], meta_streams[i_ph], gwins[i_ph]
         st.append(s)
 
     meta_marks = []  # ORCH_BENCH_TRACE: events between the metadata sub-steps
@@ -280,9 +289,10 @@ def run_b200(args):
             p1.record(stream)
             probe.append((p0, p1))
         mark(stream)
-        if gwin is not None:  # one single-CTA kernel through peer memory
-            ctx_meta.allgather_items_put(gwin, s["pos"], s["llen"], s["lorg"], s["n"], B["glen"],
-                                         B["gorg"], stream=stream)
+        ctx_meta = s["ctx"]
+        if s["gwin"] is not None:  # one single-CTA kernel through peer memory
+            ctx_meta.allgather_items_put(s["gwin"], s["pos"], s["llen"], s["lorg"], s["n"],
+                                         B["glen"], B["gorg"], stream=stream)
         elif comm_meta is not None:
             ctx_meta.allgather_items(comm_meta, s["pos"], s["llen"], s["lorg"], s["max_local"],
                                      s["n"], B["glen"], B["gorg"], stream=stream)
@@ -340,6 +350,7 @@ def run_b200(args):
         counter[0] += 1
         for s in st:
             B = s["buf"][b]
+            meta_stream = s["ms"]
             meta_stream.wait_event(B["data_done"])  # rows of step i-2 moved: buffers free
             with torch.cuda.stream(meta_stream):
                 if h2d:  # e2e: this step's metadata comes from pinned host memory
@@ -398,20 +409,24 @@ def run_b200(args):
     for _ in range(max(args.warmup, 3)):
         step()
     barrier()
-    launches0 = ctx_meta.launches + ctx_data.launches
+    all_ctx = list({id(x): x for x in meta_ctx}.values()) + [ctx_data]
+    launches0 = sum(x.launches for x in all_ctx)
     with ClockSampler([local]) as clocks:
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(data_stream)
-        meta_stream.wait_event(t0)
+        for ms in meta_streams:
+            ms.wait_event(t0)
         for _ in range(args.steps):
             step(record=True)
         t1.record(data_stream)
         barrier()
-    launches = ctx_meta.launches + ctx_data.launches - launches0
+    launches = sum(x.launches for x in all_ctx) - launches0
     if trace:
-        if gwin is not None:
+        for gwin in gwins:
+            if gwin is None:
+                continue
             stm = gwin.stamps().astype(np.int64)
             for row in stm:
                 if row[0]:
@@ -469,13 +484,14 @@ def run_b200(args):
 
     def e2e_step():
         b = step(h2d=True)
-        with torch.cuda.stream(meta_stream):
-            for s, (hi, hs, hsum) in zip(st, host_out):
+        for s, (hi, hs, hsum) in zip(st, host_out):
+            with torch.cuda.stream(s["ms"]):
                 bal = s["buf"][b]["bal"]
                 hi.copy_(bal.dest_inst[:s["n"]], non_blocking=True)
                 hs.copy_(bal.dest_slot[:s["n"]], non_blocking=True)
                 hsum[:bal.summary_raw.numel()].copy_(bal.summary_raw, non_blocking=True)
-        meta_stream.synchronize()
+        for ms in meta_streams:
+            ms.synchronize()
         data_stream.synchronize()
 
     for _ in range(2):
@@ -561,8 +577,9 @@ def run_b200(args):
         if s.get("win") is not None:
             s["rout"] = None
             s["win"].close()
-    if gwin is not None:
-        gwin.close()
+    for gwin in gwins:
+        if gwin is not None:
+            gwin.close()
     if comm_meta is not None:
         comm_meta.close()
         comm_data.close()
