@@ -13,6 +13,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstring>
 #include <string>
 
 #include "balance_kernels.cuh"
@@ -479,24 +480,21 @@ int orch_balance(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
 
 }  // extern "C"
 
-// Host-buffer variants keep their staging buffers in a second allocation so
-// the pipeline arena can be reserved independently.
+// Host-buffer variants stage through a per-context device buffer and its
+// pinned host mirror with the same layout: inputs | outputs. One H2D copy of
+// the inputs, the pipeline, one D2H copy of the outputs, one synchronize
+// (pageable cudaMemcpyAsync calls cost ~10 us each; a call used to make eight).
 namespace {
 
-struct Staging {
-  void* base = nullptr;
-  size_t cap = 0;
-};
-thread_local Staging g_stage;
-
-int stage_reserve(size_t bytes) {
-  if (bytes <= g_stage.cap) return ORCH_OK;
-  if (g_stage.base) cudaFree(g_stage.base);
-  g_stage.base = nullptr;
+int stage_reserve(orch_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->stage_cap) return ORCH_OK;
+  if (ctx->stage) cudaFree(ctx->stage);
+  ctx->stage = nullptr;
+  ctx->stage_cap = 0;
   size_t cap = 1 << 20;
   while (cap < bytes) cap *= 2;
-  ORCH_CUDA_TRY(cudaMalloc(&g_stage.base, cap));
-  g_stage.cap = cap;
+  ORCH_CUDA_TRY(cudaMalloc(&ctx->stage, cap));
+  ctx->stage_cap = cap;
   return ORCH_OK;
 }
 
@@ -509,54 +507,60 @@ int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n
   ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
   auto al = [](size_t b) { return (b + 255) & ~size_t{255}; };
-  const size_t need = al(nn * 8) + al(nn * 4) + 2 * al(nn * 4) + al(nn * 8) + al(d * 4) +
-                      al(d * 8) + al(sizeof(orch_summary)) + 2 * al(8);
-  int rc = stage_reserve(need);
-  if (rc) return rc;
-  char* p = static_cast<char*>(g_stage.base);
+  // byte offsets of the staged arrays (device buffer and pinned mirror alike)
+  size_t at = 0;
   auto take = [&](size_t b) {
-    char* r = p;
-    p += al(b);
+    const size_t r = at;
+    at += al(b);
     return r;
   };
-  int64_t* len = reinterpret_cast<int64_t*>(take(nn * 8));
-  int32_t* origin = reinterpret_cast<int32_t*>(take(nn * 4));
-  orch_balance_out out{};
-  out.dest_inst = reinterpret_cast<int32_t*>(take(nn * 4));
-  out.dest_slot = reinterpret_cast<int32_t*>(take(nn * 4));
-  out.dst_off = reinterpret_cast<int64_t*>(take(nn * 8));
-  out.bin_count = reinterpret_cast<int32_t*>(take(d * 4));
-  out.bin_cost = reinterpret_cast<double*>(take(d * 8));
-  out.summary = reinterpret_cast<orch_summary*>(take(sizeof(orch_summary)));
-  int64_t* d_bound = reinterpret_cast<int64_t*>(take(8));
-  int32_t* d_probe = reinterpret_cast<int32_t*>(take(8));
-  if (n > 0) {
-    ORCH_CUDA_TRY(cudaMemcpyAsync(len, h_len, n * 8, cudaMemcpyHostToDevice, st));
-    ORCH_CUDA_TRY(cudaMemcpyAsync(origin, h_origin, n * 4, cudaMemcpyHostToDevice, st));
-  }
-  rc = orchb::run_balance(ctx, policy, d, n, len, origin, mode, probe, &out, d_bound, d_probe, st);
+  const size_t o_len = take(nn * 8), o_org = take(nn * 4);
+  const size_t in_bytes = at;
+  const size_t o_di = take(nn * 4), o_ds = take(nn * 4), o_doff = take(nn * 8);
+  const size_t o_bc = take(static_cast<size_t>(d) * 4), o_cost = take(static_cast<size_t>(d) * 8);
+  const size_t o_sum = take(sizeof(orch_summary)), o_bound = take(8), o_probe = take(8);
+  const size_t total = at;
+  int rc = stage_reserve(ctx, total);
   if (rc) return rc;
+  char* hp = static_cast<char*>(orchb::pinned(ctx, total));
+  if (!hp) return orchb::fail(ORCH_CUDA_ERROR, "pinned staging allocation failed");
+  char* dp = static_cast<char*>(ctx->stage);
+  orch_balance_out out{};
+  // only the outputs this mode reads back are written by the pipeline
+  const bool rows = n > 0 && mode < 2;
+  out.dest_inst = reinterpret_cast<int32_t*>(dp + o_di);
+  out.dest_slot = reinterpret_cast<int32_t*>(dp + o_ds);
+  out.dst_off = reinterpret_cast<int64_t*>(dp + o_doff);
+  out.bin_count = reinterpret_cast<int32_t*>(dp + o_bc);
+  out.bin_cost = reinterpret_cast<double*>(dp + o_cost);
+  out.summary = reinterpret_cast<orch_summary*>(dp + o_sum);
+  if (n > 0) {
+    std::memcpy(hp + o_len, h_len, static_cast<size_t>(n) * 8);
+    std::memcpy(hp + o_org, h_origin, static_cast<size_t>(n) * 4);
+    ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
+  }
+  rc = orchb::run_balance(ctx, policy, d, n, reinterpret_cast<int64_t*>(dp + o_len),
+                          reinterpret_cast<int32_t*>(dp + o_org), mode, probe, &out,
+                          reinterpret_cast<int64_t*>(dp + o_bound),
+                          reinterpret_cast<int32_t*>(dp + o_probe), st);
+  if (rc) return rc;
+  // one read-back: the per-item outputs (balance modes) through the probe word
+  const size_t back = rows ? o_di : o_bc;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(hp + back, dp + back, total - back, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
   orch_summary sum;
-  ORCH_CUDA_TRY(cudaMemcpyAsync(&sum, out.summary, sizeof sum, cudaMemcpyDeviceToHost, st));
-  if (n > 0 && mode < 2) {
-    if (h_dest_inst)
-      ORCH_CUDA_TRY(cudaMemcpyAsync(h_dest_inst, out.dest_inst, n * 4, cudaMemcpyDeviceToHost, st));
-    if (h_dest_slot)
-      ORCH_CUDA_TRY(cudaMemcpyAsync(h_dest_slot, out.dest_slot, n * 4, cudaMemcpyDeviceToHost, st));
-    if (h_dst_off)
-      ORCH_CUDA_TRY(cudaMemcpyAsync(h_dst_off, out.dst_off, n * 8, cudaMemcpyDeviceToHost, st));
+  std::memcpy(&sum, hp + o_sum, sizeof sum);
+  if (rows) {
+    if (h_dest_inst) std::memcpy(h_dest_inst, hp + o_di, static_cast<size_t>(n) * 4);
+    if (h_dest_slot) std::memcpy(h_dest_slot, hp + o_ds, static_cast<size_t>(n) * 4);
+    if (h_dst_off) std::memcpy(h_dst_off, hp + o_doff, static_cast<size_t>(n) * 8);
   }
   if (mode < 2) {
-    if (h_bin_count)
-      ORCH_CUDA_TRY(cudaMemcpyAsync(h_bin_count, out.bin_count, d * 4, cudaMemcpyDeviceToHost, st));
-    if (h_bin_cost)
-      ORCH_CUDA_TRY(cudaMemcpyAsync(h_bin_cost, out.bin_cost, d * 8, cudaMemcpyDeviceToHost, st));
+    if (h_bin_count) std::memcpy(h_bin_count, hp + o_bc, static_cast<size_t>(d) * 4);
+    if (h_bin_cost) std::memcpy(h_bin_cost, hp + o_cost, static_cast<size_t>(d) * 8);
   }
-  if (mode == 2 && h_bound)
-    ORCH_CUDA_TRY(cudaMemcpyAsync(h_bound, d_bound, 8, cudaMemcpyDeviceToHost, st));
-  if (mode == 3 && h_probe)
-    ORCH_CUDA_TRY(cudaMemcpyAsync(h_probe, d_probe, 4, cudaMemcpyDeviceToHost, st));
-  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  if (mode == 2 && h_bound) std::memcpy(h_bound, hp + o_bound, 8);
+  if (mode == 3 && h_probe) std::memcpy(h_probe, hp + o_probe, 4);
   if (h_summary) *h_summary = sum;
   if (sum.error) return device_error_message(sum.error, sum.error_index, d, h_len, h_origin);
   return ORCH_OK;

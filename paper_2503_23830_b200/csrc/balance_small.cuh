@@ -75,10 +75,11 @@ struct SmallSmem {
   int32_t ord[NS];
   uint32_t xs[NS];
   uint16_t a_slot[NS];
-  uint16_t id_rank[NS];                   // rank inside its chunk among same-origin items
+  uint16_t id_rank[NS + 1];               // rank inside its chunk among same-origin items
   uint16_t chunk_base[NCH][kSmallMaxD];   // same-origin items in earlier chunks
   uint8_t chunk_cnt[NCH][kSmallMaxD];
   uint8_t a_dest[NS];
+  uint8_t g_bin[NS + 1];  // greedy: bin per sorted position (g_slot = id_rank, g_off = pfx)
   union {
     typename Sort::TempStorage sort;
     typename Scan::TempStorage scan;
@@ -95,17 +96,20 @@ struct SmallSmem {
   int64_t cand[kSmallWarps];
   int feas[kSmallWarps];
   unsigned long long maxlen, total;
-  int bad, unsup, groups, used_identity;
+  int bad, unsup, groups, used_identity, gfirst;
   int64_t lo, hi, bound, rounds;
 };
 
 // Warp 0: round-batched LPT over xs[first, n) (descending). Lane b < d holds
-// bin b: load (optionally pre-seeded) and item count. kWrite: record each
-// item's bin / slot / token offset.
-template <bool kWrite, int W, int ITEMS>
+// bin b: load (optionally pre-seeded) and item count. kWrite: record, per
+// sorted position, the item's bin, slot and token offset (g_bin / g_slot /
+// g_off, plain predicated stores off the round's dependency chain);
+// greedy_scatter() moves them to input positions with the whole block.
+template <bool kWrite, int W, typename Key, int ITEMS>
 __device__ void warp_greedy_w(SmallSmem<ITEMS>& S, int d, int first, int n,
-                              const int64_t* init_load, const int32_t* init_cnt, int64_t* dst_off,
+                              const int64_t* init_load, const int32_t* init_cnt,
                               int64_t* rounds_out) {
+  constexpr Key kKeyMax = ~Key{0};
   const int lane = threadIdx.x & 31;
   int64_t L = 0;
   int32_t cnt = 0;
@@ -117,30 +121,46 @@ __device__ void warp_greedy_w(SmallSmem<ITEMS>& S, int d, int first, int n,
   int64_t rounds = 0;
   while (next < n) {
     const int m = n - next < d ? n - next : d;
-    const uint64_t key = lane < d ? ((static_cast<uint64_t>(L) << 5) | lane) : kU64Max;
-    int rank = 0;
-    uint64_t mn = key;
+    const Key key = lane < d ? ((static_cast<Key>(L) << 5) | lane) : kKeyMax;
+    const uint32_t xv = next + lane < n ? S.xs[next + lane] : 0u;
+    int r0 = 0, r1 = 0;  // two partial counts: half the dependent adds
+    Key mn;
+    if constexpr (sizeof(Key) == 4) {
+      mn = __reduce_min_sync(~0u, key);
 #pragma unroll
-    for (int j = 0; j < W; ++j) {  // W independent shuffles in flight (keys of lanes >= d are MAX)
-      const uint64_t kj = __shfl_sync(~0u, key, j);
-      rank += kj < key;
-      mn = kj < mn ? kj : mn;
+      for (int j = 0; j < W; j += 2) {  // W independent shuffles in flight (keys of lanes >= d are MAX)
+        r0 += __shfl_sync(~0u, key, j) < key;
+        r1 += __shfl_sync(~0u, key, j + 1) < key;
+      }
+    } else {
+      mn = key;
+#pragma unroll
+      for (int j = 0; j < W; j += 2) {
+        const Key k0 = __shfl_sync(~0u, key, j), k1 = __shfl_sync(~0u, key, j + 1);
+        r0 += k0 < key;
+        r1 += k1 < key;
+        mn = k0 < mn ? k0 : mn;
+        mn = k1 < mn ? k1 : mn;
+      }
     }
+    const int rank = r0 + r1;
     const int64_t L0 = static_cast<int64_t>(mn >> 5);
     const bool live = lane < d && rank < m;
-    const int64_t x = live ? static_cast<int64_t>(S.xs[next + rank]) : 0;
+    // x_rank: every lane read xs[next + lane] beside the key shuffles (its
+    // address depends on `next` only); one shuffle by rank replaces a
+    // dependent shared-memory load
+    const uint32_t xr = __shfl_sync(~0u, xv, rank & 31);  // all lanes shuffle
+    const int64_t x = live ? static_cast<int64_t>(xr) : 0;
     const bool c = live && (L - L0 < x);
     const int k = __popc(__ballot_sync(~0u, c));  // c holds exactly for ranks 0..k-1
-    if (c) {
-      if (kWrite) {
-        const int32_t pos = S.ord[next + rank];
-        S.a_dest[pos] = static_cast<uint8_t>(lane);
-        S.a_slot[pos] = static_cast<uint16_t>(cnt);
-        dst_off[pos] = L;
-      }
-      ++cnt;
-      L += x;
+    if (kWrite) {  // unconditional stores (no branch): lanes that take nothing write slot NS
+      const int at = c ? next + rank : SmallSmem<ITEMS>::NS;
+      S.g_bin[at] = static_cast<uint8_t>(lane);
+      S.id_rank[at] = static_cast<uint16_t>(cnt);  // g_slot
+      S.pfx[at] = L;                               // g_off
     }
+    cnt += c ? 1 : 0;
+    L += c ? x : 0;
     next += k;
     ++rounds;
   }
@@ -152,15 +172,36 @@ __device__ void warp_greedy_w(SmallSmem<ITEMS>& S, int d, int first, int n,
   if (rounds_out && lane == 0) *rounds_out = rounds;
 }
 
+// Whole block, after warp_greedy<true>: sorted positions [first, n) to inputs.
+template <int ITEMS>
+__device__ void greedy_scatter(SmallSmem<ITEMS>& S, int first, int n, int64_t* dst_off) {
+  for (int k = first + static_cast<int>(threadIdx.x); k < n; k += kSmallThreads) {
+    const int32_t pos = S.ord[k];
+    S.a_dest[pos] = S.g_bin[k];
+    S.a_slot[pos] = S.id_rank[k];
+    dst_off[pos] = S.pfx[k];
+  }
+}
+
+// Keys (load << 5 | bin) are 32-bit when every load fits 27 bits (loads never
+// exceed the phase's total length): half the shuffles of the 64-bit keys.
 template <bool kWrite, int ITEMS>
 __device__ void warp_greedy(SmallSmem<ITEMS>& S, int d, int first, int n, const int64_t* init_load,
-                            const int32_t* init_cnt, int64_t* dst_off, int64_t* rounds_out) {
-  if (d <= 8)
-    warp_greedy_w<kWrite, 8>(S, d, first, n, init_load, init_cnt, dst_off, rounds_out);
-  else if (d <= 16)
-    warp_greedy_w<kWrite, 16>(S, d, first, n, init_load, init_cnt, dst_off, rounds_out);
-  else
-    warp_greedy_w<kWrite, 32>(S, d, first, n, init_load, init_cnt, dst_off, rounds_out);
+                            const int32_t* init_cnt, int64_t* rounds_out) {
+  if (S.total < (1ull << 27)) {
+    if (d <= 8)
+      warp_greedy_w<kWrite, 8, uint32_t>(S, d, first, n, init_load, init_cnt, rounds_out);
+    else if (d <= 16)
+      warp_greedy_w<kWrite, 16, uint32_t>(S, d, first, n, init_load, init_cnt, rounds_out);
+    else
+      warp_greedy_w<kWrite, 32, uint32_t>(S, d, first, n, init_load, init_cnt, rounds_out);
+  } else if (d <= 8) {
+    warp_greedy_w<kWrite, 8, uint64_t>(S, d, first, n, init_load, init_cnt, rounds_out);
+  } else if (d <= 16) {
+    warp_greedy_w<kWrite, 16, uint64_t>(S, d, first, n, init_load, init_cnt, rounds_out);
+  } else {
+    warp_greedy_w<kWrite, 32, uint64_t>(S, d, first, n, init_load, init_cnt, rounds_out);
+  }
 }
 
 template <int ITEMS>
@@ -324,33 +365,54 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     __syncthreads();
     SMALL_MARK(3);
     if (a.kind == ORCH_GREEDY_UNPADDED) {
-      if (warp == 0) warp_greedy<true>(S, d, 0, n, nullptr, nullptr, a.dst_off, &S.rounds);
+      if (warp == 0) warp_greedy<true>(S, d, 0, n, nullptr, nullptr, &S.rounds);
+      __syncthreads();
+      greedy_scatter(S, 0, n, a.dst_off);
     } else if (a.kind == ORCH_QUADRATIC_TOLERANCE) {
-      if (warp == 0) {  // champion scan (balancers.cpp:223-231) with the batches in lanes
+      if (warp == 0) {
+        // Champion scan (balancers.cpp:223-231): best = 0; for i = 1..d-1:
+        // if less(s[i], s[best]) best = i, with the non-transitive tolerance
+        // comparator less(a, b) = |a.sum - b.sum| < v ? a.sq < b.sq : a.sum < b.sum.
+        // Lane j holds batch j and beats_j, bit i set iff less(s[i], s[j]).
+        // An item changes one batch b, so only row and column b are redone
+        // (one ballot). The scan moves from a champion j to the first later
+        // batch that beats it, nxt_j = lowest bit of beats_j above j.
+        const int64_t v = a.tol_v;
+        const unsigned dmask = d >= 32 ? ~0u : ((1u << d) - 1u);
+        const unsigned above = lane >= 31 ? 0u : (dmask & (~0u << (lane + 1)));
         int64_t qs = 0, qq = 0;
         int32_t cnt = 0;
+        unsigned beats = 0;  // all sums equal and zero: nothing beats anything
+        auto less = [v](int64_t as, int64_t aq, int64_t bs, int64_t bq) {
+          const int64_t df = as - bs;
+          return (df < 0 ? -df : df) < v ? aq < bq : as < bs;
+        };
+        int64_t x_next = n > 0 ? static_cast<int64_t>(S.xs[0]) : 0;
         for (int k = 0; k < n; ++k) {
-          int best = 0;
-          for (;;) {
-            const int64_t bs = __shfl_sync(~0u, qs, best);
-            const int64_t bq = __shfl_sync(~0u, qq, best);
-            const int64_t df = qs - bs;
-            const bool c = lane > best && lane < d &&
-                           ((df < 0 ? -df : df) < a.tol_v ? (qq < bq) : (qs < bs));
-            const unsigned m = __ballot_sync(~0u, c);
-            if (!m) break;
-            best = __ffs(m) - 1;  // the first later batch that beats the champion
-          }
-          if (lane == best) {
-            const int64_t x = S.xs[k];
-            const int32_t pos = S.ord[k];
-            S.a_dest[pos] = static_cast<uint8_t>(best);
-            S.a_slot[pos] = static_cast<uint16_t>(cnt);
-            a.dst_off[pos] = qs;
-            ++cnt;
-            qs += x;
-            qq += x * x;
-          }
+          const int64_t x = x_next;
+          if (k + 1 < n) x_next = static_cast<int64_t>(S.xs[k + 1]);  // off the critical path
+          // the scan's last champion, by pointer jumping along the chain
+          // 0 -> nxt_0 -> ... (a batch nothing later beats points to itself):
+          // ceil(log2 d) dependent shuffles, no branches
+          const int nxt = __ffs(beats & above) - 1;
+          int jump = nxt < 0 ? lane : nxt;
+          for (int span = 1; span < d; span <<= 1) jump = __shfl_sync(~0u, jump, jump);
+          const int best = __shfl_sync(~0u, jump, 0);
+          const bool me = lane == best;
+          const int at = me ? k : SmallSmem<ITEMS>::NS;  // per sorted position, no branch
+          S.g_bin[at] = static_cast<uint8_t>(lane);
+          S.id_rank[at] = static_cast<uint16_t>(cnt);
+          S.pfx[at] = qs;
+          cnt += me ? 1 : 0;
+          qs += me ? x : 0;
+          qq += me ? x * x : 0;
+          const int64_t bs = __shfl_sync(~0u, qs, best);
+          const int64_t bq = __shfl_sync(~0u, qq, best);
+          // column best: does batch `best` beat me; row best: do I beat it
+          const bool b_beats_me = lane != best && less(bs, bq, qs, qq);
+          const bool i_beat_b = lane < d && lane != best && less(qs, qq, bs, bq);
+          const unsigned row = __ballot_sync(~0u, i_beat_b);
+          beats = lane == best ? row : ((beats & ~(1u << best)) | (b_beats_me ? 1u << best : 0u));
         }
         if (lane < d) {
           S.cnt_a[lane] = cnt;
@@ -358,10 +420,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         }
         if (lane == 0) S.rounds = n;
       }
+      __syncthreads();
+      greedy_scatter(S, 0, n, a.dst_off);
     } else if (a.kind == ORCH_CONVTRANSFORMER) {
       if (warp == 0) {
         // bound = greedy objective (balancers.cpp:247-256)
-        warp_greedy<false>(S, d, 0, n, nullptr, nullptr, nullptr, nullptr);
+        warp_greedy<false>(S, d, 0, n, nullptr, nullptr, nullptr);
         int64_t bound = lane < d ? S.tok_a[lane] : 0;
         for (int off = 16; off > 0; off >>= 1) {
           const int64_t o = __shfl_xor_sync(~0u, bound, off);
@@ -414,8 +478,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
           S.bound = bound;
         }
         __syncwarp();
-        warp_greedy<true>(S, d, k, n, S.seed_load, S.seed_cnt, a.dst_off, &S.rounds);
+        warp_greedy<true>(S, d, k, n, S.seed_load, S.seed_cnt, &S.rounds);
+        if (lane == 0) S.gfirst = k;
       }
+      __syncthreads();
+      greedy_scatter(S, S.gfirst, n, a.dst_off);
     } else {  // BinaryPadded: k-ary search over the ascending lengths in smem
       {
         int64_t v[ITEMS];  // prefix of ascending lengths (token offsets in groups)

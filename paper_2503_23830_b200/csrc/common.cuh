@@ -42,6 +42,9 @@ struct orch_ctx {
   // Pinned host staging for small device->host reads.
   void* pinned = nullptr;
   size_t pinned_cap = 0;
+  // Device staging of the host-buffer (_host) entry points, mirrored in `pinned`.
+  void* stage = nullptr;
+  size_t stage_cap = 0;
   int64_t launches = 0;
 };
 

@@ -97,6 +97,7 @@ void orch_ctx_destroy(orch_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->arena.base) cudaFree(ctx->arena.base);
+  if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;
 }
