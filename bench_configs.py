@@ -2,7 +2,7 @@
 """Per-config evidence for BASELINE.json configs C1..C5 on one B200 (not the
 driver's bench line; see bench.py for that). For every config and phase:
 GPU balance time (device-resident inputs, CUDA events, median of reps),
-host-buffer C-ABI time (orch_balance_host, synchronous), the reference's own
+host-buffer C-ABI time (orch_balance_host through ctypes, synchronous, median), the reference's own
 balance() time on the host (oracle/_ref), bit-exact parity of the assignment
 and objective against the reference, and for the dispatched configs the
 token-row movement time and HBM GB/s.
@@ -101,9 +101,13 @@ def main():
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1) * 1e3)
             gpu_us = statistics.median(times)
-            t0 = time.perf_counter()
-            hr = ctx.balance_host(kind, d, L, O, lam=lam, v=v)
-            host_us = (time.perf_counter() - t0) * 1e6
+            hr = ctx.balance_host(kind, d, L, O, lam=lam, v=v)  # warm (staging sized)
+            hts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                hr = ctx.balance_host(kind, d, L, O, lam=lam, v=v)
+                hts.append((time.perf_counter() - t0) * 1e6)
+            host_us = statistics.median(hts)
             s = bal.summary()
             rec = dict(config=cname, phase=pname, policy=kind, d=d, n=n, tokens=int(L.sum()),
                        gpu_balance_us=round(gpu_us, 1), host_abi_balance_us=round(host_us, 1),

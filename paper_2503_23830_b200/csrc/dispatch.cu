@@ -122,52 +122,60 @@ __global__ void k_rank_offsets(int64_t n, const int32_t* __restrict__ origin,
   }
 }
 
-// Within each destination batch (slot order), the running row offset of the
-// item among items from the same ORIGIN RANK (warp per batch, P <= 8 lanes of
-// warp scans per 32 items), plus per-(batch, origin rank) totals W.
+// Within destination batch j (slot order), the running row offset of each
+// item among items from the same ORIGIN RANK (P <= 8 lanes of warp scans per
+// 32 items), plus the per-(batch, origin rank) totals W[j*P + q]. One warp.
+__device__ __forceinline__ void pair_within_batch(int j, int P, int c,
+                                                  const int32_t* __restrict__ bin_offset,
+                                                  const int32_t* __restrict__ bin_member,
+                                                  const int64_t* __restrict__ len,
+                                                  const int32_t* __restrict__ origin,
+                                                  int64_t* __restrict__ pair_off, int64_t* W) {
+  const int lane = threadIdx.x & 31;
+  int64_t run[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int beg = bin_offset[j], end = bin_offset[j + 1];
+  for (int base = beg; base < end; base += 32) {
+    const int k = base + lane;
+    int32_t pos = 0, r = -1;
+    int64_t l = 0;
+    if (k < end) {
+      pos = bin_member[k];
+      l = len[pos];
+      r = origin[pos] / c;
+    }
+    int64_t mine = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q >= P) break;
+      int64_t v = r == q ? l : 0;
+      int64_t incl = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t o = __shfl_up_sync(~0u, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (r == q) mine = run[q] + incl - v;
+      run[q] += __shfl_sync(~0u, incl, 31);
+    }
+    if (k < end) pair_off[pos] = mine;
+  }
+  if (lane < P) {
+    int64_t v = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q == lane) v = run[q];
+    W[j * P + lane] = v;
+  }
+}
+
 __global__ void k_pair_within(int d, int P, const int32_t* __restrict__ bin_offset,
                               const int32_t* __restrict__ bin_member,
                               const int64_t* __restrict__ len, const int32_t* __restrict__ origin,
                               int64_t* __restrict__ pair_off, int64_t* __restrict__ W) {
-  const int lane = threadIdx.x & 31;
   const int c = d / P;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < d; j += warps) {
-    int64_t run[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const int beg = bin_offset[j], end = bin_offset[j + 1];
-    for (int base = beg; base < end; base += 32) {
-      const int k = base + lane;
-      int32_t pos = 0, r = -1;
-      int64_t l = 0;
-      if (k < end) {
-        pos = bin_member[k];
-        l = len[pos];
-        r = origin[pos] / c;
-      }
-      int64_t mine = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (q >= P) break;
-        int64_t v = r == q ? l : 0;
-        int64_t incl = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int64_t o = __shfl_up_sync(~0u, incl, off);
-          if (lane >= off) incl += o;
-        }
-        if (r == q) mine = run[q] + incl - v;
-        run[q] += __shfl_sync(~0u, incl, 31);
-      }
-      if (k < end) pair_off[pos] = mine;
-    }
-    if (lane < P) {
-      int64_t v = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == lane) v = run[q];
-      W[j * P + lane] = v;
-    }
-  }
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < d; j += warps)
+    pair_within_batch(static_cast<int>(j), P, c, bin_offset, bin_member, len, origin, pair_off, W);
 }
 
 // Segment bases: for dest rank q and origin rank r, the rows from r into the
@@ -208,6 +216,75 @@ __global__ void k_pair_apply(int64_t n, int d, int P, const int32_t* __restrict_
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     pair_off[i] += Wbase[static_cast<int64_t>(dest[i]) * P + origin[i] / c];
+}
+
+// The whole layout of a small phase in one CTA (n <= kLayoutSmallItems,
+// d <= kLayoutSmallD): the six kernels above with their intermediates in
+// shared memory. The metadata chain of C1-C3 and C5 is latency-bound; this
+// saves five launches and the three memsets.
+constexpr int kLayoutSmallItems = 16384;
+constexpr int kLayoutSmallD = 256;
+constexpr int kLayoutSmallThreads = 1024;
+
+__global__ void __launch_bounds__(kLayoutSmallThreads, 1)
+    k_layout_small(int n, int d, int P, const int64_t* __restrict__ len,
+                   const int32_t* __restrict__ origin, orch_balance_out bal, orch_layout_out L) {
+  __shared__ unsigned long long inst_in[kLayoutSmallD], inst_out[kLayoutSmallD];
+  __shared__ int64_t base_in[kLayoutSmallD], base_out[kLayoutSmallD];
+  __shared__ int64_t W[kLayoutSmallD * 8], Wbase[kLayoutSmallD * 8];
+  const int t = threadIdx.x, c = d / P;
+  if (t == 0) *L.status = 0;
+  for (int i = t; i < d; i += blockDim.x) inst_in[i] = inst_out[i] = 0;
+  __syncthreads();
+  for (int i = t; i < n; i += blockDim.x) {  // k_inst_rows
+    const unsigned long long l = static_cast<unsigned long long>(len[i]);
+    atomicAdd(&inst_in[origin[i]], l);
+    atomicAdd(&inst_out[bal.dest_inst[i]], l);
+  }
+  __syncthreads();
+  if (t < P) {  // k_inst_bases
+    int64_t a = 0, b = 0;
+    for (int i = t * c; i < (t + 1) * c; ++i) {
+      base_in[i] = a;
+      base_out[i] = b;
+      a += static_cast<int64_t>(inst_in[i]);
+      b += static_cast<int64_t>(inst_out[i]);
+    }
+    L.in_rows[t] = a;
+    L.out_rows[t] = b;
+  }
+  // k_pair_within: warp per destination batch (reads only the balance outputs)
+  for (int j = t >> 5; j < d; j += blockDim.x >> 5)
+    pair_within_batch(j, P, c, bal.bin_offset, bal.bin_member, len, origin, L.pair_off, W);
+  __syncthreads();
+  if (t < P * P) {  // k_pair_bases
+    const int q = t / P, r = t % P;
+    int64_t acc = 0;
+    for (int j = q * c; j < (q + 1) * c; ++j) {
+      Wbase[j * P + r] = acc;
+      acc += W[j * P + r];
+    }
+    L.send_rows[r * P + q] = acc;
+  }
+  __syncthreads();
+  if (t < P) {
+    int64_t a = 0;
+    for (int q = 0; q < P; ++q) {
+      L.send_displ[t * P + q] = q == t ? 0 : a;
+      if (q != t) a += L.send_rows[t * P + q];
+    }
+    int64_t b = 0;
+    for (int r = 0; r < P; ++r) {
+      L.recv_displ[t * P + r] = r == t ? 0 : b;
+      if (r != t) b += L.send_rows[r * P + t];
+    }
+  }
+  for (int i = t; i < n; i += blockDim.x) {  // k_rank_offsets + k_pair_apply
+    const int o = origin[i], de = bal.dest_inst[i];
+    L.rank_src_off[i] = base_in[o] + bal.src_off[i];
+    L.rank_dst_off[i] = base_out[de] + bal.dst_off[i];
+    L.pair_off[i] += Wbase[de * P + o / c];
+  }
 }
 
 // ---------------------------------------------------------------- movement
@@ -740,6 +817,15 @@ int orch_layout(orch_ctx* ctx, int32_t d, int32_t P, int64_t n, const int64_t* d
   if (!bal->dest_inst || !bal->src_off || !bal->dst_off || !bal->bin_offset || !bal->bin_member)
     return fail(ORCH_INVALID_ARGUMENT, "orch_layout needs dest_inst, src_off, dst_off, bin_offset, bin_member");
   auto st = static_cast<cudaStream_t>(stream);
+  if (!L->status) return fail(ORCH_INVALID_ARGUMENT, "layout->status is required");
+  if (n <= kLayoutSmallItems && d <= kLayoutSmallD) {
+    launch(ctx, [&] {
+      k_layout_small<<<1, kLayoutSmallThreads, 0, st>>>(static_cast<int>(n), d, P, d_len, d_origin,
+                                                        *bal, *L);
+    });
+    ORCH_CUDA_TRY(cudaGetLastError());
+    return ORCH_OK;
+  }
   Plan plan;
   unsigned long long *inst_in, *inst_out;
   int64_t *base_in, *base_out, *W, *Wbase;

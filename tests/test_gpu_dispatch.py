@@ -54,6 +54,25 @@ def test_layout_matches_oracle(ctx, oracle, P):
                                               e["send_tokens"])
 
 
+@pytest.mark.parametrize("P,d,n", [(1, 320, 3000), (4, 64, 20000), (8, 512, 30000)])
+def test_layout_multi_kernel_path(ctx, oracle, P, d, n):
+    """Beyond the single-CTA layout (n > 16384 or d > 256): the six-kernel path."""
+    rng = np.random.default_rng(7 * P + d)
+    length, origin = make_case(rng, d, n, hi=300)
+    o = oracle.balance(0, d, length, origin)
+    L, O = to_dev(length, np.int64), to_dev(origin, np.int32)
+    bal = ctx.balance(0, d, L, O)
+    lay = ctx.layout(d, P, L, O, bal)
+    torch.cuda.synchronize()
+    e = expected_layout(oracle, d, P, length, origin, o)
+    np.testing.assert_array_equal(lay.rank_src_off[:n].cpu().numpy(), e["rank_src_off"])
+    np.testing.assert_array_equal(lay.rank_dst_off[:n].cpu().numpy(), e["rank_dst_off"])
+    np.testing.assert_array_equal(lay.out_rows.cpu().numpy(), e["out_tokens"])
+    if P > 1:
+        np.testing.assert_array_equal(lay.pair_off[:n].cpu().numpy(), e["pair_off"])
+        np.testing.assert_array_equal(lay.send_rows.cpu().numpy().reshape(P, P), e["send_tokens"])
+
+
 def test_volume_matrix(ctx, oracle):
     rng = np.random.default_rng(3)
     for d in (1, 3, 8, 64, 300):
