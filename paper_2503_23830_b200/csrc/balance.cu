@@ -146,7 +146,11 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
 
-  if (mode <= 1 && d <= kSmallMaxD && n <= kSmallMaxItems) {
+  // quadratic tolerance and ConvTransformer keep one batch per lane (d <= 32)
+  const int small_max_d =
+      !identity_only && (kind == ORCH_QUADRATIC_TOLERANCE || kind == ORCH_CONVTRANSFORMER) ? 32
+                                                                                          : kSmallMaxD;
+  if (mode <= 1 && d <= small_max_d && n <= kSmallMaxItems) {
     Plan sp;
     SmallArgs a{};
     const size_t nn1 = static_cast<size_t>(n > 0 ? n : 1);

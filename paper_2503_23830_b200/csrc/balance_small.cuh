@@ -33,7 +33,7 @@ __device__ long long g_small_prof[16];
 
 constexpr int kSmallThreads = 256;
 constexpr int kSmallWarps = kSmallThreads / 32;
-constexpr int kSmallMaxD = 32;
+constexpr int kSmallMaxD = 64;       // greedy, padded, identity; quadtol / conv: 32
 constexpr int kSmallMaxItems = 4096;
 
 struct SmallArgs {
@@ -172,6 +172,71 @@ __device__ void warp_greedy_w(SmallSmem<ITEMS>& S, int d, int first, int n,
   if (rounds_out && lane == 0) *rounds_out = rounds;
 }
 
+// Warp 0, 32 < d <= 64 (greedy only): the same rounds with two bins per lane,
+// b = lane and b = lane + 32; keys (load << 6 | bin).
+template <bool kWrite, typename Key, int ITEMS>
+__device__ void warp_greedy_w64(SmallSmem<ITEMS>& S, int d, int n, int64_t* rounds_out) {
+  constexpr Key kKeyMax = ~Key{0};
+  const int lane = threadIdx.x & 31;
+  const int b1 = lane + 32;
+  int64_t LA = 0, LB = 0;
+  int32_t cA = 0, cB = 0;
+  int next = 0;
+  int64_t rounds = 0;
+  while (next < n) {
+    const int m = n - next < d ? n - next : d;
+    const Key kA = (static_cast<Key>(LA) << 6) | lane;
+    const Key kB = b1 < d ? ((static_cast<Key>(LB) << 6) | b1) : kKeyMax;
+    const uint32_t xa = next + lane < n ? S.xs[next + lane] : 0u;
+    const uint32_t xb = next + b1 < n ? S.xs[next + b1] : 0u;
+    int rA = 0, rB = 0, sA = 0, sB = 0;
+    Key mn = kA < kB ? kA : kB;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {  // all 64 keys against both of mine (keys are distinct)
+      const Key ja = __shfl_sync(~0u, kA, j), jb = __shfl_sync(~0u, kB, j);
+      rA += ja < kA;
+      sA += jb < kA;
+      rB += ja < kB;
+      sB += jb < kB;
+      mn = ja < mn ? ja : mn;
+      mn = jb < mn ? jb : mn;
+    }
+    const int rankA = rA + sA, rankB = rB + sB;
+    const int64_t L0 = static_cast<int64_t>(mn >> 6);
+    const uint32_t xA0 = __shfl_sync(~0u, xa, rankA & 31), xA1 = __shfl_sync(~0u, xb, rankA & 31);
+    const uint32_t xB0 = __shfl_sync(~0u, xa, rankB & 31), xB1 = __shfl_sync(~0u, xb, rankB & 31);
+    const bool liveA = rankA < m, liveB = b1 < d && rankB < m;
+    const int64_t xA = liveA ? static_cast<int64_t>(rankA < 32 ? xA0 : xA1) : 0;
+    const int64_t xB = liveB ? static_cast<int64_t>(rankB < 32 ? xB0 : xB1) : 0;
+    const bool tA = liveA && (LA - L0 < xA), tB = liveB && (LB - L0 < xB);
+    const int k = __popc(__ballot_sync(~0u, tA)) + __popc(__ballot_sync(~0u, tB));
+    if (kWrite) {  // unconditional stores: lanes that take nothing write slot NS
+      const int atA = tA ? next + rankA : SmallSmem<ITEMS>::NS;
+      S.g_bin[atA] = static_cast<uint8_t>(lane);
+      S.id_rank[atA] = static_cast<uint16_t>(cA);
+      S.pfx[atA] = LA;
+      const int atB = tB ? next + rankB : SmallSmem<ITEMS>::NS;
+      S.g_bin[atB] = static_cast<uint8_t>(b1);
+      S.id_rank[atB] = static_cast<uint16_t>(cB);
+      S.pfx[atB] = LB;
+    }
+    cA += tA ? 1 : 0;
+    LA += tA ? xA : 0;
+    cB += tB ? 1 : 0;
+    LB += tB ? xB : 0;
+    next += k;
+    ++rounds;
+  }
+  S.cnt_a[lane] = cA;
+  S.tok_a[lane] = LA;
+  if (b1 < d) {
+    S.cnt_a[b1] = cB;
+    S.tok_a[b1] = LB;
+  }
+  __syncwarp();
+  if (rounds_out && lane == 0) *rounds_out = rounds;
+}
+
 // Whole block, after warp_greedy<true>: sorted positions [first, n) to inputs.
 template <int ITEMS>
 __device__ void greedy_scatter(SmallSmem<ITEMS>& S, int first, int n, int64_t* dst_off) {
@@ -188,6 +253,13 @@ __device__ void greedy_scatter(SmallSmem<ITEMS>& S, int first, int n, int64_t* d
 template <bool kWrite, int ITEMS>
 __device__ void warp_greedy(SmallSmem<ITEMS>& S, int d, int first, int n, const int64_t* init_load,
                             const int32_t* init_cnt, int64_t* rounds_out) {
+  if (d > 32) {  // greedy only (the caller keeps quadtol / conv at d <= 32)
+    if (S.total < (1ull << 26))
+      warp_greedy_w64<kWrite, uint32_t>(S, d, n, rounds_out);
+    else
+      warp_greedy_w64<kWrite, uint64_t>(S, d, n, rounds_out);
+    return;
+  }
   if (S.total < (1ull << 27)) {
     if (d <= 8)
       warp_greedy_w<kWrite, 8, uint32_t>(S, d, first, n, init_load, init_cnt, rounds_out);
@@ -202,6 +274,26 @@ __device__ void warp_greedy(SmallSmem<ITEMS>& S, int d, int first, int n, const 
   } else {
     warp_greedy_w<kWrite, 32, uint64_t>(S, d, first, n, init_load, init_cnt, rounds_out);
   }
+}
+
+// Warp 0: exclusive scan of cnt[0..d) into off[0..d], off[d] = total (d <= 64:
+// lane holds elements lane and lane + 32).
+__device__ __forceinline__ void warp_offsets64(const int32_t* cnt, int32_t* off, int d, int total) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = lane < d ? cnt[lane] : 0;
+  const int c1 = lane + 32 < d ? cnt[lane + 32] : 0;
+  int i0 = c0, i1 = c1;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u0 = __shfl_up_sync(~0u, i0, o), u1 = __shfl_up_sync(~0u, i1, o);
+    if (lane >= o) {
+      i0 += u0;
+      i1 += u1;
+    }
+  }
+  const int half = __shfl_sync(~0u, i0, 31);
+  if (lane < d) off[lane] = i0 - c0;
+  if (lane + 32 < d) off[lane + 32] = half + i1 - c1;
+  if (lane == 0) off[d] = total;
 }
 
 template <int ITEMS>
@@ -282,6 +374,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     const unsigned peers = __match_any_sync(~0u, o);
     if (i < n) S.id_rank[i] = static_cast<uint16_t>(__popc(peers & ((1u << lane) - 1u)));
     if (lane < d) S.chunk_cnt[c][lane] = 0;
+    if (lane + 32 < d) S.chunk_cnt[c][lane + 32] = 0;
     __syncwarp();
     if (i < n && (__ffs(peers) - 1) == lane) S.chunk_cnt[c][o] = static_cast<uint8_t>(__popc(peers));
   }
@@ -295,16 +388,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     S.cnt_id[tid] = run;
   }
   __syncthreads();
-  if (warp == 0) {  // offsets of the origin batches
-    const int c = lane < d ? S.cnt_id[lane] : 0;
-    int incl = c;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int o = __shfl_up_sync(~0u, incl, off);
-      if (lane >= off) incl += o;
-    }
-    if (lane < d) S.off_id[lane] = incl - c;
-    if (lane == 0) S.off_id[d] = n;
-  }
+  if (warp == 0) warp_offsets64(S.cnt_id, S.off_id, d, n);  // offsets of the origin batches
   __syncthreads();
   for (int i = tid; i < n; i += kSmallThreads) {
     const int o = S.org[i];
@@ -552,8 +636,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       __syncthreads();
       const int G = S.groups;
       for (int k = tid; k < n; k += kSmallThreads) {
-        int g = 0;
-        while (g + 1 < G && S.starts[g + 1] <= k) ++g;
+        int g = 0, hi = G - 1;  // last group whose start is <= k
+        while (g < hi) {
+          const int mid = (g + hi + 1) >> 1;
+          if (S.starts[mid] <= k) g = mid; else hi = mid - 1;
+        }
         const int32_t pos = S.ord[k];
         S.a_dest[pos] = static_cast<uint8_t>(g);
         S.a_slot[pos] = static_cast<uint16_t>(k - S.starts[g]);
@@ -564,16 +651,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     __syncthreads();
     SMALL_MARK(4);
     // ---- algorithm CSR (balancers.cpp:43-60 assemble: slot = position in bin)
-    if (warp == 0) {
-      const int c = lane < d ? S.cnt_a[lane] : 0;
-      int incl = c;
-      for (int off = 1; off < 32; off <<= 1) {
-        const int o = __shfl_up_sync(~0u, incl, off);
-        if (lane >= off) incl += o;
-      }
-      if (lane < d) S.off_a[lane] = incl - c;
-      if (lane == 0) S.off_a[d] = n;
-    }
+    if (warp == 0) warp_offsets64(S.cnt_a, S.off_a, d, n);
     __syncthreads();
     for (int i = tid; i < n; i += kSmallThreads) {
       const int b = S.a_dest[i];

@@ -89,6 +89,20 @@ def test_random_medium_large_d(ctx, oracle, kind):
         run_case(ctx, oracle, kind, d, length, origin, lam=1e-4, v=int(rng.choice([0, 64, 2048])))
 
 
+@pytest.mark.parametrize("kind", KINDS)
+def test_random_fused_d33_64(ctx, oracle, kind):
+    """33 <= d <= 64, n <= 4096: the single-CTA kernel with two batches per lane
+    (greedy, padded; quadtol / conv take the multi-kernel path). Large lengths
+    push the phase total past 2^26 (64-bit greedy keys)."""
+    rng = np.random.default_rng(2500 + kind)
+    for trial in range(40):
+        d = int(rng.integers(33, 65))
+        n = int(rng.integers(1, 4097))
+        hi = int(rng.choice([2, 50, 4096, 1 << 20]))
+        length, origin = random_instance(rng, d, n, 1, hi, rng.choice(["random", "zero", "rr"]))
+        run_case(ctx, oracle, kind, d, length, origin, lam=1e-4, v=int(rng.choice([0, 64])))
+
+
 def test_heavy_ties(ctx, oracle):
     """All-equal lengths: every argmin is a tie broken by the lowest index."""
     for d in (2, 7, 31, 32, 33, 64, 257):
