@@ -382,7 +382,10 @@ def run_b200(args):
                 ctx_data.put(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
                              s["win"], comm_data, stream=data_stream)
                 if s is st[-1]:
-                    ctx_data.barrier(comm_data, stream=data_stream)
+                    if args.barrier == "window":  # peer-memory flags (one 1-warp kernel)
+                        ctx_data.window_barrier(s["win"], stream=data_stream)
+                    elif args.barrier == "nccl":
+                        ctx_data.barrier(comm_data, stream=data_stream)
             else:
                 ctx_data.dispatch(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
                                   s["rout"], s["send"], s["recv"], comm_data, stream=data_stream)
@@ -600,6 +603,9 @@ def main():
                     help="N>1: skip the GPU-wise hosting of destination batches")
     ap.add_argument("--gather", default="put", choices=["put", "nccl"],
                     help="N>1 lengths all-gather: peer-memory kernel (default) or ncclAllGather")
+    ap.add_argument("--barrier", default="window", choices=["window", "nccl", "none"],
+                    help="N>1 put: the per-step barrier through the window's peer memory "
+                         "(default), a 1-int ncclAllReduce, or none (diagnostics only)")
     ap.add_argument("--exchange", default="put", choices=["put", "nccl"],
                     help="N>1: fused pack+put over NVLink (default) or NCCL send/recv")
     args = ap.parse_args()

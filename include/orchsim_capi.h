@@ -315,6 +315,13 @@ int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window
 void* orch_window_ptr(const orch_window* w);
 size_t orch_window_bytes(const orch_window* w);
 int orch_window_destroy(orch_window* w); /* collective */
+/* Barrier through the window's peer memory (one 1-warp kernel, no NCCL):
+ * lane q stores this rank's call count into rank q's flag slot with a
+ * system-scope release, then waits for every rank's store into its own slots
+ * (acquire). Everything earlier on `stream` (e.g. this step's puts) is visible
+ * to every rank once its barrier returns. Collective: every rank calls it the
+ * same number of times on the same window. Replaces orch_barrier after puts. */
+int orch_window_barrier(orch_ctx* ctx, orch_window* w, void* stream);
 
 /* Fused pack + put exchange: every item's rows are
  * read once from this rank's d_in and stored directly at their final

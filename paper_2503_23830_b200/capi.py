@@ -31,7 +31,7 @@ EXPORTED = [
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
     "orch_solve_hosting_host", "orch_nodewise", "orch_rearrange", "orch_backbone_targets",
     "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
-    "orch_window_destroy", "orch_dispatch_put", "orch_put",
+    "orch_window_destroy", "orch_window_barrier", "orch_dispatch_put", "orch_put",
     "orch_gather_window_create", "orch_gather_window_destroy", "orch_allgather_items_put",
     "orch_gather_window_stamps",
 ]
@@ -491,6 +491,10 @@ class Context:
     @staticmethod
     def barrier(comm: Comm, stream=None):
         _check(lib().orch_barrier(comm.h, _stream(stream)))
+
+    def window_barrier(self, window: "Window", stream=None):
+        """orch_window_barrier: flag barrier through the window's peer memory."""
+        _check(lib().orch_window_barrier(self.h, window.h, _stream(stream)))
 
     def allgather_items_put(self, gwin: GatherWindow, local_pos, local_len, local_origin, n,
                             out_len, out_origin, status=None, stream=None):

@@ -31,6 +31,8 @@ struct orch_window {
   orch_comm* comm = nullptr;
   char* base = nullptr;
   size_t bytes = 0;
+  size_t flags_off = 0;           // [P] uint64 barrier slots after the rows (IPC-shared)
+  uint64_t epoch = 0;             // orch_window_barrier calls so far (equal on every rank)
   std::vector<char*> peers;       // host copy, peers[rank] == base
   char** peers_dev = nullptr;     // device copy [P]
 };
@@ -285,6 +287,28 @@ __global__ void __launch_bounds__(kLayoutSmallThreads, 1)
     L.rank_dst_off[i] = base_out[de] + bal.dst_off[i];
     L.pair_off[i] += Wbase[de * P + o / c];
   }
+}
+
+// Window barrier: lane q publishes this rank's epoch in rank q's slot [me]
+// (release, system scope: the stream's earlier kernels -- the puts into the
+// peers' windows -- are complete, and the fence orders them before the flag),
+// then waits until rank q's epoch is in this rank's slot [q] (acquire).
+__global__ void k_window_barrier(char* const* __restrict__ peers, size_t flags_off, int me, int P,
+                                 uint64_t epoch) {
+  const int q = threadIdx.x;
+  if (q < P) {
+    __threadfence_system();
+    uint64_t* slot = reinterpret_cast<uint64_t*>(peers[q] + flags_off) + me;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
+    const uint64_t* mine = reinterpret_cast<const uint64_t*>(peers[me] + flags_off) + q;
+    uint64_t v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- movement
@@ -1351,11 +1375,13 @@ int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window
   w->comm = comm;
   w->bytes = bytes;
   w->peers.assign(P, nullptr);
-  cudaError_t e = cudaMalloc(&w->base, bytes);
+  w->flags_off = (bytes + 255) & ~size_t{255};
+  cudaError_t e = cudaMalloc(&w->base, w->flags_off + 256);
   if (e != cudaSuccess) {
     delete w;
     return fail(ORCH_CUDA_ERROR, std::string("window allocation: ") + cudaGetErrorString(e));
   }
+  ORCH_CUDA_TRY(cudaMemset(w->base + w->flags_off, 0, 256));
   cudaIpcMemHandle_t mine;
   ORCH_CUDA_TRY(cudaIpcGetMemHandle(&mine, w->base));
   char* dev = nullptr;
@@ -1382,6 +1408,18 @@ int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window
   ORCH_CUDA_TRY(cudaMemcpy(w->peers_dev, w->peers.data(), sizeof(char*) * P,
                            cudaMemcpyHostToDevice));
   *out = w;
+  return ORCH_OK;
+}
+
+int orch_window_barrier(orch_ctx* ctx, orch_window* w, void* stream) {
+  if (!ctx || !w) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  const int P = w->comm->size;
+  ++w->epoch;
+  launch(ctx, [&] {
+    k_window_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        w->peers_dev, w->flags_off, w->comm->rank, P, w->epoch);
+  });
+  ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
 }
 

@@ -99,6 +99,17 @@ def main():
                 ok = ok and int(lay.status.item()) == 0
                 k = len(outs[rank])
                 ok = ok and torch.equal(wv[:k].cpu(), torch.from_numpy(outs[rank]))
+                # put + the window's peer-memory barrier, twice (epochs 1, 2): the
+                # rows are complete as soon as this rank's barrier returns on its stream
+                for _ in range(2):
+                    wv.zero_()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    ctx.put(d, gl, go, bal, lay, R, rin, win, comm)
+                    ctx.window_barrier(win)
+                    ok = ok and torch.equal(wv[:k].cpu(), torch.from_numpy(outs[rank]))
+                    torch.cuda.synchronize()
+                    dist.barrier()
                 win.close()
                 cases += 1
                 if not ok:
