@@ -315,13 +315,109 @@ __device__ __forceinline__ int64_t warp_next_start(const uint32_t* __restrict__ 
   return hi;
 }
 
+// One thread: next_start from p with a guess h of the group size. Probe
+// t = p + h - 1: if cond(t) is false the boundary is beyond t (gallop from t),
+// else it is in (p, t] (bisect). Sizes change slowly along ascending lengths,
+// so the guess is usually within a step or two.
+__device__ __forceinline__ int64_t thread_next_start_hint(const uint32_t* a, int64_t n, int64_t p,
+                                                          int64_t b, int64_t h) {
+  auto cond = [&](int64_t t) { return t >= n || (t - p + 1) * static_cast<int64_t>(a[t]) > b; };
+  int64_t lo = p, hi;
+  const int64_t g = h > 1 ? p + h - 1 : p + 1;
+  if (cond(g)) {
+    hi = g;
+    if (g - 1 > p && !cond(g - 1)) return g;  // the guess was exact
+  } else {
+    lo = g;
+    int64_t k = 1;
+    for (;; k <<= 1) {
+      const int64_t t = g + k;
+      if (cond(t)) {
+        hi = t < n ? t : n;
+        break;
+      }
+      lo = t;
+    }
+  }
+  while (hi - lo > 1) {  // cond(lo) false (lo == p or probed), cond(hi) true
+    const int64_t t = lo + ((hi - lo) >> 1);
+    if (cond(t)) hi = t;
+    else lo = t;
+  }
+  return hi;
+}
+
+// One thread: is bound b feasible (at most d groups)?
+__device__ __forceinline__ bool thread_feasible(const uint32_t* a, int64_t n, int d, int64_t b) {
+  int64_t p = 0, size = 0;
+  for (int groups = 0; p < n; ++groups) {
+    if (groups == d) return false;
+    const int64_t q = thread_next_start_hint(a, n, p, b, size);
+    size = q - p;
+    p = q;
+  }
+  return true;
+}
+
+// warp_next_start with a guess of the group size (the previous group's: sizes
+// change slowly along ascending lengths). One ballot over the 32 starts
+// around the guess settles most groups; otherwise the boundary is bracketed by
+// the window and finished by 32-ary search (or the plain gallop).
+__device__ __forceinline__ int64_t warp_next_start_hint(const uint32_t* __restrict__ a, int64_t n,
+                                                        int64_t p, int64_t b, int lane,
+                                                        int64_t size_hint) {
+  if (size_hint <= 16) return warp_next_start(a, n, p, b, lane);
+  const int64_t base = p + size_hint - 16;  // > p
+  const int64_t t = base + lane;
+  const bool c = t >= n || (t - p + 1) * static_cast<int64_t>(a[t]) > b;
+  const unsigned m = __ballot_sync(~0u, c);
+  int64_t lo, hi;
+  if (m & 1u) {  // boundary in (p, base]: cond(p) false, cond(base) true
+    lo = p;
+    hi = base;
+  } else if (m) {
+    return base + (__ffs(m) - 1);  // cond(base + f - 1) false, cond(base + f) true
+  } else {  // past the window: gallop from base + 31 (false)
+    lo = base + 31;
+    int64_t step = 1;
+    for (;;) {
+      const int64_t tt = lo + step * (lane + 1);
+      const bool cc = tt >= n || (tt - p + 1) * static_cast<int64_t>(a[tt]) > b;
+      const unsigned mm = __ballot_sync(~0u, cc);
+      if (mm) {
+        const int f = __ffs(mm) - 1;
+        hi = lo + step * (f + 1);
+        if (hi > n) hi = n;
+        lo = lo + step * f;
+        break;
+      }
+      lo = lo + step * 32;
+      step *= 32;
+    }
+  }
+  while (hi - lo > 1) {  // invariant: cond(lo) false, cond(hi) true
+    const int64_t span = hi - lo;
+    const int64_t st = (span + 31) / 32;
+    const int64_t tt = lo + st * (lane + 1);
+    const bool cc = tt >= hi || (tt - p + 1) * static_cast<int64_t>(a[tt]) > b;
+    const unsigned mm = __ballot_sync(~0u, cc);
+    const int f = __ffs(mm) - 1;
+    const int64_t nhi = lo + st * (f + 1);
+    hi = nhi < hi ? nhi : hi;
+    lo = lo + st * f;
+  }
+  return hi;
+}
+
 __device__ __forceinline__ bool warp_feasible(const uint32_t* __restrict__ a, int64_t n, int d,
                                               int64_t b, int lane) {
-  int64_t p = 0;
+  int64_t p = 0, size = 0;
   int groups = 0;
   while (p < n) {
     if (++groups > d) return false;
-    p = warp_next_start(a, n, p, b, lane);
+    const int64_t q = warp_next_start_hint(a, n, p, b, lane, size);
+    size = q - p;
+    p = q;
   }
   return true;
 }

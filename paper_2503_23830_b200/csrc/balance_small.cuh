@@ -27,8 +27,10 @@ namespace {
 #ifdef ORCH_SMALL_PROFILE
 __device__ long long g_small_prof[16];
 #define SMALL_MARK(i) do { __syncthreads(); if (threadIdx.x == 0) g_small_prof[i] = clock64(); } while (0)
+#define SMALL_SUB(i) do { if (threadIdx.x == 0) g_small_prof[i] = clock64(); } while (0)
 #else
 #define SMALL_MARK(i) do { } while (0)
+#define SMALL_SUB(i) do { } while (0)
 #endif
 
 constexpr int kSmallThreads = 256;
@@ -76,8 +78,9 @@ struct SmallSmem {
   uint32_t xs[NS];
   uint16_t a_slot[NS];
   uint16_t id_rank[NS + 1];               // rank inside its chunk among same-origin items
-  uint16_t chunk_base[NCH][kSmallMaxD];   // same-origin items in earlier chunks
-  uint8_t chunk_cnt[NCH][kSmallMaxD];
+  // origin-major, so a warp scans one origin's chunk counts conflict-free
+  uint16_t chunk_base[kSmallMaxD][NCH + 2];  // same-origin items in earlier chunks (rows padded:
+  uint8_t chunk_cnt[kSmallMaxD][NCH + 4];    // lanes of one chunk hit different banks)
   uint8_t a_dest[NS];
   uint8_t g_bin[NS + 1];  // greedy: bin per sorted position (g_slot = id_rank, g_off = pfx)
   union {
@@ -93,8 +96,7 @@ struct SmallSmem {
   int64_t b_len[2][kSmallMaxD], b_tok[2][kSmallMaxD];
   double b_cost[2][kSmallMaxD];
   int64_t starts[kSmallMaxD + 2];
-  int64_t cand[kSmallWarps];
-  int feas[kSmallWarps];
+  unsigned long long nhi, nlo;  // padded search: min feasible / max infeasible + 1 this round
   unsigned long long maxlen, total;
   int bad, unsup, groups, used_identity, gfirst;
   int64_t lo, hi, bound, rounds;
@@ -368,35 +370,67 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   SMALL_MARK(1);
   // ---- S2: identity grouping (batches_from_items, core.cpp:183-199): the
   // source slot of an item is the number of earlier items with its origin.
+  // Same-origin lanes of a 32-item chunk by one ballot per origin bit (d <= 64:
+  // at most 6), cheaper than __match_any_sync.
+  const int obits = d > 1 ? 32 - __clz(d - 1) : 0;
+#pragma unroll 2
   for (int c = warp; c < nch; c += kSmallWarps) {
     const int i = c * 32 + lane;
-    const int o = i < n ? S.org[i] : kSmallMaxD + lane;  // padding never matches
-    const unsigned peers = __match_any_sync(~0u, o);
-    if (i < n) S.id_rank[i] = static_cast<uint16_t>(__popc(peers & ((1u << lane) - 1u)));
-    if (lane < d) S.chunk_cnt[c][lane] = 0;
-    if (lane + 32 < d) S.chunk_cnt[c][lane + 32] = 0;
-    __syncwarp();
-    if (i < n && (__ffs(peers) - 1) == lane) S.chunk_cnt[c][o] = static_cast<uint8_t>(__popc(peers));
-  }
-  __syncthreads();
-  if (tid < d) {  // running count of each origin over the chunks
-    int run = 0;
-    for (int c = 0; c < nch; ++c) {
-      S.chunk_base[c][tid] = static_cast<uint16_t>(run);
-      run += S.chunk_cnt[c][tid];
+    const int o = i < n ? S.org[i] : 0;
+    unsigned peers = __ballot_sync(~0u, i < n);
+    for (int bit = 0; bit < obits; ++bit) {
+      const bool set = (o >> bit) & 1;
+      const unsigned m = __ballot_sync(~0u, set);
+      peers &= set ? m : ~m;
     }
-    S.cnt_id[tid] = run;
+    if (i < n) S.id_rank[i] = static_cast<uint16_t>(__popc(peers & ((1u << lane) - 1u)));
+    if (lane < d) S.chunk_cnt[lane][c] = 0;
+    if (lane + 32 < d) S.chunk_cnt[lane + 32][c] = 0;
+    __syncwarp();
+    if (i < n && (__ffs(peers) - 1) == lane) S.chunk_cnt[o][c] = static_cast<uint8_t>(__popc(peers));
   }
   __syncthreads();
+  SMALL_SUB(10);
+  {  // running count of each origin over the chunks: warp per origin, lane per
+     // ceil(NCH / 32) consecutive chunks, one warp scan
+    constexpr int PER = (SS::NCH + 31) / 32;
+    for (int o = warp; o < d; o += kSmallWarps) {
+      int c[PER], tot = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int ch = lane * PER + j;
+        c[j] = ch < nch ? S.chunk_cnt[o][ch] : 0;
+        tot += c[j];
+      }
+      int incl = tot;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(~0u, incl, off);
+        if (lane >= off) incl += u;
+      }
+      int run = incl - tot;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        const int ch = lane * PER + j;
+        if (ch < nch) S.chunk_base[o][ch] = static_cast<uint16_t>(run);
+        run += c[j];
+      }
+      if (lane == 31) S.cnt_id[o] = incl;
+    }
+  }
+  __syncthreads();
+  SMALL_SUB(11);
   if (warp == 0) warp_offsets64(S.cnt_id, S.off_id, d, n);  // offsets of the origin batches
   __syncthreads();
+  SMALL_SUB(12);
   for (int i = tid; i < n; i += kSmallThreads) {
     const int o = S.org[i];
-    const int slot = S.chunk_base[i >> 5][o] + S.id_rank[i];
+    const int slot = S.chunk_base[o][i >> 5] + S.id_rank[i];
     a.src_slot[i] = slot;
     S.ord_id[S.off_id[o] + slot] = i;
+    S.a_slot[i] = static_cast<uint16_t>(S.off_id[o] + slot);  // identity position (a_slot is free here)
   }
   __syncthreads();
+  SMALL_SUB(13);
   {
     int64_t v[ITEMS];
 #pragma unroll
@@ -411,12 +445,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     if (tid == 0) S.pfx[SS::NS] = agg;
   }
   __syncthreads();
-  for (int k = tid; k < n; k += kSmallThreads) {
-    const int32_t pos = S.ord_id[k];
-    const int st = S.off_id[S.org[pos]];
-    a.src_off[pos] = S.pfx[k] - S.pfx[st];
-    a.src_member[k] = pos;
-  }
+  SMALL_SUB(14);
+  for (int i = tid; i < n; i += kSmallThreads)  // by input position: coalesced org / a_slot reads
+    a.src_off[i] = S.pfx[S.a_slot[i]] - S.pfx[S.off_id[S.org[i]]];
+  for (int k = tid; k < n; k += kSmallThreads) a.src_member[k] = S.ord_id[k];
   if (tid <= d) a.src_offset[tid] = S.off_id[tid];
 
   SMALL_MARK(2);
@@ -589,42 +621,50 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         S.hi = max_len * (n / d + 1);
       }
       __syncthreads();
-      constexpr int W = kSmallWarps;
+#ifdef ORCH_SMALL_PROFILE
+      if (tid == 0) g_small_prof[8] = clock64();
+#endif
+      // k-ary search with one candidate bound per thread (256 per round; the
+      // answer is the minimal feasible bound whatever the probe order)
       while (true) {
         const int64_t lo = S.lo, hi = S.hi;
         if (lo >= hi) break;
         const int64_t span = hi - lo;
-        const int64_t c = span <= W ? lo + warp : lo + (span * warp) / W;
-        bool f = true;
-        if (c < hi) f = warp_feasible(S.xs, n, d, c, lane);
-        if (lane == 0) {
-          S.cand[warp] = c;
-          S.feas[warp] = f;
+        const int64_t c = span <= kSmallThreads ? lo + tid : lo + (span * tid) / kSmallThreads;
+        __syncthreads();  // every thread has read lo / hi
+        if (tid == 0) {
+          S.nhi = static_cast<unsigned long long>(hi);
+          S.nlo = static_cast<unsigned long long>(lo);
+        }
+        __syncthreads();
+        if (c < hi) {
+          if (thread_feasible(S.xs, n, d, c))
+            atomicMin(&S.nhi, static_cast<unsigned long long>(c));
+          else
+            atomicMax(&S.nlo, static_cast<unsigned long long>(c + 1));
         }
         __syncthreads();
         if (tid == 0) {
-          int64_t nhi = hi, nlo = lo;
-          for (int w = 0; w < W; ++w) {
-            if (S.cand[w] >= hi) continue;
-            if (S.feas[w]) {
-              if (S.cand[w] < nhi) nhi = S.cand[w];
-            } else if (S.cand[w] + 1 > nlo) {
-              nlo = S.cand[w] + 1;
-            }
-          }
+          const int64_t nhi = static_cast<int64_t>(S.nhi), nlo = static_cast<int64_t>(S.nlo);
           S.hi = nhi;
           S.lo = nlo < nhi ? nlo : nhi;
         }
         __syncthreads();
       }
+#ifdef ORCH_SMALL_PROFILE
+      if (tid == 0) g_small_prof[9] = clock64();
+#endif
       if (warp == 0) {
         const int64_t bound = S.hi;
         int64_t p = 0;
         int g = 0;
+        int64_t size = 0;
         while (p < n) {
           if (lane == 0) S.starts[g] = p;
           ++g;
-          p = warp_next_start(S.xs, n, p, bound, lane);
+          const int64_t q = warp_next_start_hint(S.xs, n, p, bound, lane, size);
+          size = q - p;
+          p = q;
         }
         if (lane == 0) {
           S.starts[g] = n;
@@ -666,50 +706,79 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   }
 
   SMALL_MARK(5);
-  // ---- S6: batch costs (core.cpp:91-118): warp w -> algorithm batch w, identity batch w
-  for (int task = warp; task < 2 * d; task += kSmallWarps) {
-    const int side = task < d ? 0 : 1;  // 0 algorithm, 1 identity
-    const int b = side ? task - d : task;
-    if (side == 0 && a.identity_only) continue;
-    const int beg = side ? S.off_id[b] : S.off_a[b];
-    const int end = side ? S.off_id[b + 1] : S.off_a[b + 1];
-    int64_t s = 0, mx = 0;
-    unsigned long long sq = 0;
-    bool inexact = false;
-    for (int k = beg + lane; k < end; k += 32) {
-      const int32_t pos = side ? S.ord_id[k] : S.ord[k];
-      const int64_t l = S.len[pos];
-      s += l;
-      mx = l > mx ? l : mx;
-      if (l >= (1ll << 26)) inexact = true;
-      sq += static_cast<unsigned long long>(l) * static_cast<unsigned long long>(l);
-      if (sq >= (1ull << 53)) inexact = true;
+  // ---- S6: batch costs (core.cpp:91-118), algorithm batches then identity batches.
+  // Integer sums are exact; Sum l^2 is replayed as the reference's sequential
+  // double loop when a partial sum could reach 2^53.
+  const orch_cost_model& model = a.model;
+  auto finish_batch = [&](int side, int b, int beg, int end, int64_t s, int64_t mx, double sqd) {
+    const int64_t cnt = end - beg;
+    S.b_cnt[side][b] = static_cast<int32_t>(cnt);
+    S.b_tok[side][b] = s;
+    S.b_len[side][b] = model.padded ? cnt * mx : s;
+    S.b_cost[side][b] = batch_cost(model, cnt, s, mx, sqd);
+  };
+  auto replay_sq = [&](int side, int beg, int end) {
+    double acc = 0.0;
+    for (int k = beg; k < end; ++k) {
+      const double l = static_cast<double>(S.len[side ? S.ord_id[k] : S.ord[k]]);
+      acc = rn_add(acc, rn_mul(l, l));
     }
-    for (int off = 16; off > 0; off >>= 1) {
-      s += __shfl_xor_sync(~0u, s, off);
-      const int64_t om = __shfl_xor_sync(~0u, mx, off);
-      mx = om > mx ? om : mx;
-      sq += __shfl_xor_sync(~0u, sq, off);
+    return acc;
+  };
+  const bool quad_unpadded = model.variant == ORCH_TRANSFORMER_QUADRATIC && !model.padded;
+  if (d >= 32) {  // many short batches: a thread per batch
+    for (int task = tid; task < 2 * d; task += kSmallThreads) {
+      const int side = task < d ? 0 : 1;  // 0 algorithm, 1 identity
+      const int b = side ? task - d : task;
+      if (side == 0 && a.identity_only) continue;
+      const int beg = side ? S.off_id[b] : S.off_a[b];
+      const int end = side ? S.off_id[b + 1] : S.off_a[b + 1];
+      int64_t sm = 0, mx = 0;
+      unsigned long long sq = 0;
+      bool inexact = false;
+      for (int k = beg; k < end; ++k) {
+        const int64_t l = S.len[side ? S.ord_id[k] : S.ord[k]];
+        sm += l;
+        mx = l > mx ? l : mx;
+        if (l >= (1ll << 26)) inexact = true;
+        sq += static_cast<unsigned long long>(l) * static_cast<unsigned long long>(l);
+        if (sq >= (1ull << 53)) inexact = true;
+      }
+      finish_batch(side, b, beg, end, sm, mx,
+                   inexact && quad_unpadded ? replay_sq(side, beg, end) : static_cast<double>(sq));
     }
-    inexact = __any_sync(~0u, inexact) || sq >= (1ull << 53);
-    // the identity side is scored under the policy cost model too
-    const orch_cost_model& m = a.model;
-    double sqd = static_cast<double>(sq);
-    if (inexact && m.variant == ORCH_TRANSFORMER_QUADRATIC && !m.padded) {
-      double acc = 0.0;
-      if (lane == 0)
-        for (int k = beg; k < end; ++k) {
-          const double l = static_cast<double>(S.len[side ? S.ord_id[k] : S.ord[k]]);
-          acc = rn_add(acc, rn_mul(l, l));
-        }
-      sqd = __shfl_sync(~0u, acc, 0);
-    }
-    if (lane == 0) {
-      const int64_t cnt = end - beg;
-      S.b_cnt[side][b] = static_cast<int32_t>(cnt);
-      S.b_tok[side][b] = s;
-      S.b_len[side][b] = m.padded ? cnt * mx : s;
-      S.b_cost[side][b] = batch_cost(m, cnt, s, mx, sqd);
+  } else {  // few long batches: a warp per batch
+    for (int task = warp; task < 2 * d; task += kSmallWarps) {
+      const int side = task < d ? 0 : 1;
+      const int b = side ? task - d : task;
+      if (side == 0 && a.identity_only) continue;
+      const int beg = side ? S.off_id[b] : S.off_a[b];
+      const int end = side ? S.off_id[b + 1] : S.off_a[b + 1];
+      int64_t sm = 0, mx = 0;
+      unsigned long long sq = 0;
+      bool inexact = false;
+      for (int k = beg + lane; k < end; k += 32) {
+        const int64_t l = S.len[side ? S.ord_id[k] : S.ord[k]];
+        sm += l;
+        mx = l > mx ? l : mx;
+        if (l >= (1ll << 26)) inexact = true;
+        sq += static_cast<unsigned long long>(l) * static_cast<unsigned long long>(l);
+        if (sq >= (1ull << 53)) inexact = true;
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        sm += __shfl_xor_sync(~0u, sm, off);
+        const int64_t om = __shfl_xor_sync(~0u, mx, off);
+        mx = om > mx ? om : mx;
+        sq += __shfl_xor_sync(~0u, sq, off);
+      }
+      inexact = __any_sync(~0u, inexact) || sq >= (1ull << 53);
+      double sqd = static_cast<double>(sq);
+      if (inexact && quad_unpadded) {
+        double acc = 0.0;
+        if (lane == 0) acc = replay_sq(side, beg, end);
+        sqd = __shfl_sync(~0u, acc, 0);
+      }
+      if (lane == 0) finish_batch(side, b, beg, end, sm, mx, sqd);
     }
   }
   __syncthreads();
