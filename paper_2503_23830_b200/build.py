@@ -112,10 +112,23 @@ def build_ref_tests(force=False):
     return out
 
 
+def build_cpp_api_bench(force=False):
+    """scripts/cpp_api_bench.cpp against the B200 C++ API (timing tool)."""
+    out = os.path.join(LIB, "cpp_api_bench_b200")
+    src = os.path.join(ROOT, "scripts", "cpp_api_bench.cpp")
+    host = os.path.join(LIB, "liborchsim_b200_host.so")
+    if not force and not _stale(out, [src, host]):
+        return out
+    _run([CXX, "-std=c++20", "-O2", "-Wall", "-I", INCLUDE, "-o", out, src, "-L", LIB,
+          "-l:liborchsim_b200_host.so", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_all(force=False):
     build_cuda(force)
     build_host(force)
     build_ref_tests(force)
+    build_cpp_api_bench(force)
 
 
 if __name__ == "__main__":

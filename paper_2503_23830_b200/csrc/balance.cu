@@ -179,13 +179,14 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
     a.origin = origin;
     a.s = S;
     auto run_small = [&](auto kern, int sm) -> int {
-      static int configured[3] = {0, 0, 0};  // per instantiation, once per process
+      static PerDeviceOnce configured[3];  // per instantiation
       const int slot = sm == static_cast<int>(sizeof(SmallSmem<2>)) ? 0
                        : sm == static_cast<int>(sizeof(SmallSmem<4>)) ? 1 : 2;
-      if (!configured[slot]) {
+      const int rc_attr = configured[slot]([&]() -> int {
         ORCH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        configured[slot] = 1;
-      }
+        return ORCH_OK;
+      });
+      if (rc_attr) return rc_attr;
       launch(ctx, [&] { kern<<<1, kSmallThreads, sm, st>>>(a); });
       return ORCH_OK;
     };
@@ -338,16 +339,17 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
     ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, asc_len, asc_prefix, (int)n + 1, st));
     const bool use_nx = n <= kNxMax;
     const int nx_smem = static_cast<int>(n) * 2;
-    static bool pad_configured = false;
-    if (!pad_configured) {
+    static PerDeviceOnce pad_configured;
+    const int rc_attr = pad_configured([&]() -> int {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_pad_eval_nx, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kNxMax * 2));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_pad_starts_nx,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kNxMax * 2));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_padded_search,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      pad_configured = true;
-    }
+      return ORCH_OK;
+    });
+    if (rc_attr) return rc_attr;
     if (mode == 3) {  // one feasibility probe
       if (use_nx) {
         launch(ctx, [&] {

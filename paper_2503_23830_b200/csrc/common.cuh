@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -57,6 +58,22 @@ void arena_reset(orch_ctx* ctx);
 // Make sure the arena can hold `bytes` without reallocation.
 int arena_reserve(orch_ctx* ctx, size_t bytes, cudaStream_t stream);
 void* pinned(orch_ctx* ctx, size_t bytes);
+
+// Runs f() once per device (function attributes such as the dynamic shared
+// memory limit are per-device state; a process may drive several devices).
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> done{0};
+  template <class F>
+  int operator()(F&& f) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return ORCH_OK;
+    const int rc = f();
+    if (rc == ORCH_OK) done.fetch_or(bit, std::memory_order_acq_rel);
+    return rc;
+  }
+};
 
 inline unsigned ceil_log2(unsigned long long x) {
   unsigned b = 0;

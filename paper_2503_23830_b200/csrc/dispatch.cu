@@ -974,15 +974,16 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
     const bool fat = mode == kPut && free_sms > 0;
     const int tma_grid = fat ? kSMs - free_sms : kSMs * ctas_per_sm;
     const int sm_req = fat ? 227 * 1024 - static_cast<int>(sizeof(TmaTable)) - 64 : sm;
-    static bool attr_done = false;
-    if (!attr_done) {
+    static PerDeviceOnce attr_done;
+    const int rc_attr = attr_done([&]() -> int {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kUnpack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          free_sms > 0 ? sm_req : sm));
-      attr_done = true;
-    }
+      return ORCH_OK;
+    });
+    if (rc_attr) return rc_attr;
     launch(ctx, [&] {
       if (mode == kLocal)
         k_move_tma<kLocal><<<tma_grid, 32, sm, st>>>(a);

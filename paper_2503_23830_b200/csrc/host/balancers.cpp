@@ -40,12 +40,20 @@ BalanceResult run(const BalancePolicy& policy, int d, const std::vector<SeqItem>
     r.new_batches[i].padding_mode = native_mode(policy.kind);
     r.new_batches[i].items.resize(static_cast<std::size_t>(count[i]));
   }
-  std::map<SlotRef, SlotRef> moves;
-  std::vector<int> next(static_cast<std::size_t>(d), 0);  // source slots (index_sources)
+  // moves keyed by (origin, source slot): inserted in key order (a stable
+  // counting sort by origin) so every insert is a hinted append
+  std::vector<std::size_t> obase(static_cast<std::size_t>(d) + 1, 0);
   for (std::size_t i = 0; i < items.size(); ++i) {
     r.new_batches[dest[i]].items[slot[i]] = items[i];
-    moves.emplace(SlotRef{origin[i], next[origin[i]]++}, SlotRef{dest[i], slot[i]});
+    ++obase[static_cast<std::size_t>(origin[i]) + 1];
   }
+  for (int i = 0; i < d; ++i) obase[i + 1] += obase[i];
+  std::vector<int32_t> by_src(items.size());
+  for (std::size_t i = 0; i < items.size(); ++i) by_src[obase[origin[i]]++] = static_cast<int32_t>(i);
+  std::map<SlotRef, SlotRef> moves;
+  std::vector<int> next(static_cast<std::size_t>(d), 0);  // source slots (index_sources)
+  for (const int32_t i : by_src)
+    moves.emplace_hint(moves.end(), SlotRef{origin[i], next[origin[i]]++}, SlotRef{dest[i], slot[i]});
   r.rearrangement = Rearrangement(d, std::move(moves));
   return r;
 }

@@ -1099,14 +1099,15 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
                           const int32_t* origin, const int32_t* dest, const int64_t* Vin,
                           int64_t* Vout, HostState* H, cudaStream_t st) {
   const int sm = static_cast<int>(host_smem_bytes(d, c));
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceOnce configured;
+  const int rc_attr = configured([&]() -> int {
     const int mx = static_cast<int>(host_smem_bytes(kHostMaxD, 2));  // the largest table set
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(Prep<kHostMaxD>))));
-    configured = true;
-  }
+    return ORCH_OK;
+  });
+  if (rc_attr) return rc_attr;
   k_host_setup<<<1, 1024, sizeof(Prep<kHostMaxD>), st>>>(d, c, n, len, origin, dest, Vin, Vout, H);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
@@ -1188,12 +1189,13 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
     a.hosting = hosting;
     a.b2i = b2i;
     a.info = d_info;
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceOnce configured;
+    const int rc_attr = configured([&]() -> int {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_nodewise_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sizeof(NwSmem))));
-      configured = true;
-    }
+      return ORCH_OK;
+    });
+    if (rc_attr) return rc_attr;
     k_nodewise_small<<<1, kNwThreads, sizeof(NwSmem), st>>>(a);
     ctx->launches += 1;
     ORCH_CUDA_TRY(cudaGetLastError());
