@@ -31,3 +31,41 @@ def test_reference_unit_tests_against_reference_library():
     r = subprocess.run([REF_BIN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0
     assert "32 passed | 0 failed" in r.stdout
+
+
+CPP_B200 = os.path.join(ROOT, "paper_2503_23830_b200", "lib", "cpp_api_bench_b200")
+CPP_REF = os.path.join(ROOT, "oracle", "_ref", "cpp_api_bench_ref")
+
+
+@pytest.mark.gpu
+def test_cpp_api_matches_reference_on_baseline_phases(tmp_path):
+    """orchsim::balance(policy, d, items) through the B200 C++ API and through
+    the unmodified reference, on C2, C3, C4x30 and C5 phases at their full
+    BASELINE sizes: same objective and same new_batches contents."""
+    import json
+    import sys
+
+    import numpy as np
+    if not (os.path.exists(CPP_B200) and os.path.exists(CPP_REF)):
+        pytest.skip("cpp_api_bench binaries not built (needs /root/reference at build time)")
+    sys.path.insert(0, ROOT)
+    import bench_configs as bc
+    files = []
+    for cname in ("C2", "C3", "C4x30", "C5"):
+        cfg = bc.CONFIGS[cname]
+        for i, (_, L, O, kind, lam, v) in enumerate(cfg["phases"]()):
+            f = tmp_path / f"{cname}_{i}.bin"
+            with open(f, "wb") as fh:
+                np.array([len(L), cfg["d"], kind, v], np.int64).tofile(fh)
+                np.array([lam], np.float64).tofile(fh)
+                L.astype(np.int64).tofile(fh)
+                O.astype(np.int32).tofile(fh)
+            files.append(str(f))
+    out = {}
+    for name, exe in (("b200", CPP_B200), ("ref", CPP_REF)):
+        r = subprocess.run([exe, *files], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[name] = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(out["b200"]) == len(out["ref"]) == len(files)
+    for a, b in zip(out["b200"], out["ref"]):
+        assert a["checksum"] == b["checksum"] and a["objective"] == b["objective"], (a, b)
