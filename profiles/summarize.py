@@ -2,6 +2,7 @@
 
     python profiles/summarize.py launches <launches.csv> <out.md>
     python profiles/summarize.py full <report.ncu-rep> <out.md>
+    python profiles/summarize.py balance <kprof dir> <out.md>   (scripts/kprof.sh output)
 """
 import collections
 import csv
@@ -65,5 +66,40 @@ def full(path, out):
             f.write("\n")
 
 
+def balance(d, out):
+    """Per-kernel device time of one warm balance call per config phase."""
+    import glob
+    import os
+    names = {"C3": ["vision", "audio", "llm"], "C4x30": ["vision", "audio", "llm"],
+             "C4x64": ["vision", "audio", "llm"]}
+    with open(out, "w") as f:
+        f.write("# Balance kernels per launch\n\n`scripts/kprof.sh`: `ncu --profile-from-start off "
+                "--metrics gpu__time_duration.sum --clock-control none` around the third (warm) "
+                "`ctx.balance` call of each phase (cold-cache, serialised launches). C3 = DP=64 "
+                "(single-CTA kernel), C4 = DP=2560 (30 and 64 examples per instance); vision and "
+                "LLM phases GreedyUnpadded, audio BinaryPadded.\n\n")
+        for path in sorted(glob.glob(os.path.join(d, "C*_[0-9].csv"))):
+            cfg, ph = os.path.basename(path)[:-4].rsplit("_", 1)
+            rows = list(csv.reader(open(path)))
+            hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+            hdr = rows[hi]
+            ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+            agg = collections.OrderedDict()
+            for r in rows[hi + 1:]:
+                k = r[ki].split("(")[0].replace("void ", "")
+                k = k.split("::")[-1] if "orchb" in k else k[:60]
+                a = agg.setdefault(k, [0, 0.0])
+                a[0] += 1
+                a[1] += float(r[vi].replace(",", ""))
+            tot = sum(v for _, v in agg.values())
+            n = sum(c for c, _ in agg.values())
+            name = names.get(cfg, [ph] * 3)[int(ph)]
+            f.write(f"## {cfg} {name}: {tot / 1e3:.1f} us device time over {n} launches\n\n"
+                    "| us | launches | kernel |\n|---:|---:|---|\n")
+            for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1])[:8]:
+                f.write(f"| {v / 1e3:.1f} | {c} | `{k}` |\n")
+            f.write("\n")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "balance": balance}[sys.argv[1]](sys.argv[2], sys.argv[3])

@@ -103,6 +103,19 @@ def test_random_fused_d33_64(ctx, oracle, kind):
         run_case(ctx, oracle, kind, d, length, origin, lam=1e-4, v=int(rng.choice([0, 64])))
 
 
+def test_quadtol_single_thread_and_warp_scans(ctx, oracle):
+    """QuadraticTolerance in the single-CTA kernel: d <= 8 scans in one thread,
+    9 <= d <= 32 on the warp (cached beat masks + pointer jumping)."""
+    rng = np.random.default_rng(4242)
+    for trial in range(60):
+        d = int(rng.integers(1, 9)) if trial % 2 else int(rng.integers(9, 33))
+        n = int(rng.integers(1, 3000))
+        hi = int(rng.choice([4, 300, 40000]))
+        length, origin = random_instance(rng, d, n, 1, hi, rng.choice(["random", "zero", "rr"]))
+        v = int(rng.choice([0, 1, 8, 2048, 1 << 40]))
+        run_case(ctx, oracle, 2, d, length, origin, lam=float(rng.choice([0.0, 1e-5, 0.3])), v=v)
+
+
 def test_heavy_ties(ctx, oracle):
     """All-equal lengths: every argmin is a tie broken by the lowest index."""
     for d in (2, 7, 31, 32, 33, 64, 257):
