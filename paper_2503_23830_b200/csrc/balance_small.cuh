@@ -484,51 +484,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       if (warp == 0) warp_greedy<true>(S, d, 0, n, nullptr, nullptr, &S.rounds);
       __syncthreads();
       greedy_scatter(S, 0, n, a.dst_off);
-    } else if (a.kind == ORCH_QUADRATIC_TOLERANCE && d <= 8) {
-      // d <= 8 (C5): the champion scan in one thread, batches in registers --
-      // seven dependent comparator steps per item beat the warp's shuffle /
-      // ballot latencies at this width
-      if (tid == 0) {
-        const int64_t v = a.tol_v;
-        int64_t qs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, qq[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int k = 0; k < n; ++k) {
-          const int64_t x = static_cast<int64_t>(S.xs[k]);
-          int best = 0;
-          int64_t bs = qs[0], bq = qq[0];
-#pragma unroll
-          for (int i = 1; i < 8; ++i) {
-            if (i < d) {
-              const int64_t df = qs[i] - bs;
-              const bool c = (df < 0 ? -df : df) < v ? qq[i] < bq : qs[i] < bs;
-              best = c ? i : best;
-              bs = c ? qs[i] : bs;
-              bq = c ? qq[i] : bq;
-            }
-          }
-          int32_t cb = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool me = i == best;
-            cb = me ? cnt[i] : cb;
-            cnt[i] += me ? 1 : 0;
-            qs[i] += me ? x : 0;
-            qq[i] += me ? x * x : 0;
-          }
-          S.g_bin[k] = static_cast<uint8_t>(best);
-          S.id_rank[k] = static_cast<uint16_t>(cb);
-          S.pfx[k] = bs;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (i < d) {
-            S.cnt_a[i] = cnt[i];
-            S.tok_a[i] = qs[i];
-          }
-        S.rounds = n;
-      }
-      __syncthreads();
-      greedy_scatter(S, 0, n, a.dst_off);
     } else if (a.kind == ORCH_QUADRATIC_TOLERANCE) {
       if (warp == 0) {
         // Champion scan (balancers.cpp:223-231): best = 0; for i = 1..d-1:

@@ -103,9 +103,9 @@ def test_random_fused_d33_64(ctx, oracle, kind):
         run_case(ctx, oracle, kind, d, length, origin, lam=1e-4, v=int(rng.choice([0, 64])))
 
 
-def test_quadtol_single_thread_and_warp_scans(ctx, oracle):
-    """QuadraticTolerance in the single-CTA kernel: d <= 8 scans in one thread,
-    9 <= d <= 32 on the warp (cached beat masks + pointer jumping)."""
+def test_quadtol_warp_scan(ctx, oracle):
+    """QuadraticTolerance in the single-CTA kernel (d <= 32): the warp scan with
+    cached beat masks and pointer jumping, narrow and wide d."""
     rng = np.random.default_rng(4242)
     for trial in range(60):
         d = int(rng.integers(1, 9)) if trial % 2 else int(rng.integers(9, 33))
