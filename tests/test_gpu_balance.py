@@ -116,6 +116,18 @@ def test_quadtol_warp_scan(ctx, oracle):
         run_case(ctx, oracle, 2, d, length, origin, lam=float(rng.choice([0.0, 1e-5, 0.3])), v=v)
 
 
+@pytest.mark.parametrize("kind", KINDS)
+def test_path_thresholds(ctx, oracle, kind):
+    """Either side of every switch between kernels: the single-CTA kernel's
+    item-count instantiations (512 / 1024 / 4096 items) and width limits
+    (32 for quadtol / conv, 64 otherwise) against the multi-kernel path."""
+    rng = np.random.default_rng(31 + kind)
+    for n in (512, 513, 1024, 1025, 4096, 4097):
+        for d in (8, 32, 33, 64, 65):
+            length, origin = random_instance(rng, d, n, 1, 3000, "random")
+            run_case(ctx, oracle, kind, d, length, origin, lam=2e-5, v=256)
+
+
 def test_heavy_ties(ctx, oracle):
     """All-equal lengths: every argmin is a tie broken by the lowest index."""
     for d in (2, 7, 31, 32, 33, 64, 257):

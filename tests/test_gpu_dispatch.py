@@ -54,9 +54,10 @@ def test_layout_matches_oracle(ctx, oracle, P):
                                               e["send_tokens"])
 
 
-@pytest.mark.parametrize("P,d,n", [(1, 320, 3000), (4, 64, 20000), (8, 512, 30000)])
+@pytest.mark.parametrize("P,d,n", [(1, 320, 3000), (4, 64, 20000), (8, 512, 30000),
+                                   (2, 256, 16384), (2, 256, 16385), (8, 256, 500), (1, 257, 500)])
 def test_layout_multi_kernel_path(ctx, oracle, P, d, n):
-    """Beyond the single-CTA layout (n > 16384 or d > 256): the six-kernel path."""
+    """Either side of the single-CTA layout limits (n <= 16384, d <= 256)."""
     rng = np.random.default_rng(7 * P + d)
     length, origin = make_case(rng, d, n, hi=300)
     o = oracle.balance(0, d, length, origin)
