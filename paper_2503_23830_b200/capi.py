@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "liborchsim_b200.so")
+LIB_PATH = os.environ.get("ORCH_LIB_PATH") or os.path.join(PKG, "lib", "liborchsim_b200.so")
 
 GREEDY_UNPADDED, BINARY_PADDED, QUADRATIC_TOLERANCE, CONVTRANSFORMER = 0, 1, 2, 3
 LINEAR_ONLY, TRANSFORMER_QUADRATIC, CONV_TRANSFORMER_PADDED = 0, 1, 2

@@ -465,12 +465,20 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
 // ------------------------------------------------------------ TMA movement
 // Rows of >= 8 KiB move with bulk async copies (cp.async.bulk, SASS UBLKCP):
 // global -> shared stage -> global, one warp per SM. The iteration buffer is
-// cut into 32 KiB chunks (chunk c -> CTA c % grid); each chunk is at most
+// cut into 32 KiB chunks claimed 32 at a time; each chunk is at most
 // kTmaMaxPieces contiguous item pieces. The 32 lanes decode 32 chunks' pieces
-// in parallel into a shared table, lane 0 streams them through a 3-stage ring:
-// loads of two chunks in flight while the oldest chunk is stored.
-constexpr int kTmaStages = 3;
-constexpr int kTmaChunk = 32768;
+// in parallel into a shared table, lane 0 streams them through a 4-stage ring:
+// loads of three chunks in flight while the oldest chunk is stored (4 stages
+// beat 3 by ~1% on one GPU; 6 stages and 48 KiB chunks gain nothing more, and
+// the NVLink put is at its push ceiling either way).
+#ifndef ORCH_TMA_STAGES
+#define ORCH_TMA_STAGES 4
+#endif
+#ifndef ORCH_TMA_CHUNK
+#define ORCH_TMA_CHUNK 32768
+#endif
+constexpr int kTmaStages = ORCH_TMA_STAGES;
+constexpr int kTmaChunk = ORCH_TMA_CHUNK;
 constexpr int kTmaMaxPieces = 6;
 constexpr int64_t kTmaMinRow = 8192;
 
