@@ -7,7 +7,7 @@ balance() time on the host (oracle/_ref), bit-exact parity of the assignment
 and objective against the reference, and for the dispatched configs the
 token-row movement time and HBM GB/s.
 
-    python bench_configs.py [--out profiles/r01_configs.jsonl]
+    python bench_configs.py [--sweep] [--only C3,C4x30] [--out profiles/r01_configs.jsonl]
 """
 from __future__ import annotations
 
@@ -68,6 +68,10 @@ CONFIGS = {
     "C4x64": dict(d=2560, R=None, phases=lambda: mci_phases(2560, 64, 7)),
     "C5": dict(d=8, R=16384, phases=c5_phases),
 }
+# C4's balancer scaling sweep: d in {8, 64, 256, 1024}
+# at 30 examples per instance, three modalities (d = 2560 is C4x30 above)
+SWEEP = {f"C4sweep_d{d}": dict(d=d, R=None, phases=(lambda d=d: mci_phases(d, 30, 7)))
+         for d in (8, 64, 256, 1024)}
 
 
 def main():
@@ -78,11 +82,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.jsonl"))
     ap.add_argument("--only", default="")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also C4's balancer sweep over d in {8, 64, 256, 1024}")
     args = ap.parse_args()
+    configs = dict(CONFIGS, **SWEEP) if args.sweep else CONFIGS
     ref = RefLib() if RefLib.available() else None
     ctx = Context(0)
     lines = []
-    for cname, cfg in CONFIGS.items():
+    for cname, cfg in configs.items():
         if args.only and cname not in args.only.split(","):
             continue
         d = cfg["d"]

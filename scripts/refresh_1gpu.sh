@@ -8,7 +8,7 @@ python bench.py > $o/bench_1gpu.json 2> $o/bench_1gpu.err
 python bench.py --impl reference --steps 3 --warmup 1 > $o/bench_ref.json 2> $o/bench_ref.err
 python bench.py --config C3 --no-cpu-baseline --steps 10 --warmup 3 > $o/bench_c3.json 2> $o/bench_c3.err
 python bench.py --config C5 --no-cpu-baseline --steps 10 --warmup 3 > $o/bench_c5.json 2> $o/bench_c5.err
-python bench_configs.py --out $o/configs.jsonl > $o/configs.log 2>&1
+python bench_configs.py --sweep --out $o/configs.jsonl > $o/configs.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/launches.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $o/ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_move_tma -s 8 -c 2 \
