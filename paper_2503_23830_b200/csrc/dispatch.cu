@@ -469,15 +469,24 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
 // kTmaMaxPieces contiguous item pieces. The 32 lanes decode 32 chunks' pieces
 // in parallel into a shared table, lane 0 streams them through a 4-stage ring:
 // loads of three chunks in flight while the oldest chunk is stored (4 stages
-// beat 3 by ~1% on one GPU; 6 stages and 48 KiB chunks gain nothing more, and
-// the NVLink put is at its push ceiling either way).
+// beat 3 by ~1% on one GPU; 6 stages and 48 KiB chunks gain nothing more).
 #ifndef ORCH_TMA_STAGES
 #define ORCH_TMA_STAGES 4
+#endif
+#ifndef ORCH_TMA_PUT_STAGES
+#define ORCH_TMA_PUT_STAGES 3
 #endif
 #ifndef ORCH_TMA_CHUNK
 #define ORCH_TMA_CHUNK 32768
 #endif
+// HBM moves use 4 stages; the NVLink put keeps 3 (it is at the push ceiling
+// either way, and the smaller ring leaves shared memory for the next step's
+// metadata kernels that run beside it: C3 / C5 on 4 GPUs lose ~2% with 4)
 constexpr int kTmaStages = ORCH_TMA_STAGES;
+constexpr int kTmaPutStages = ORCH_TMA_PUT_STAGES;
+static_assert(kTmaPutStages <= kTmaStages, "TmaTable is sized by kTmaStages");
+template <int MODE>
+__host__ __device__ constexpr int tma_stages() { return MODE == kPut ? kTmaPutStages : kTmaStages; }
 constexpr int kTmaChunk = ORCH_TMA_CHUNK;
 constexpr int kTmaMaxPieces = 6;
 constexpr int64_t kTmaMinRow = 8192;
@@ -499,7 +508,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 template <int MODE>
 __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
-  extern __shared__ __align__(128) unsigned char ring[];  // kTmaStages * kTmaChunk
+  constexpr int kS = tma_stages<MODE>();
+  extern __shared__ __align__(128) unsigned char ring[];  // kS * kTmaChunk
   __shared__ TmaTable T;
   const int lane = threadIdx.x;
   const int64_t total = a.iter_rows[a.me];
@@ -525,16 +535,16 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
   unsigned long long* claim = a.chunk_counter;
   const int64_t beg = a.offs[a.lo_idx], end = a.offs[a.hi_idx];
   if (lane == 0) {
-    for (int s = 0; s < kTmaStages; ++s)
+    for (int s = 0; s < kS; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&T.bar[s])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
   uint32_t phases = 0;  // lane 0: parity bit per stage
-  int64_t fed = 0;      // lane 0: chunks issued so far (stage = fed % kTmaStages)
+  int64_t fed = 0;      // lane 0: chunks issued so far (stage = fed % kS)
 
   auto retire = [&](int64_t r) {  // lane 0: wait chunk r's loads, store its pieces
-    const int s = static_cast<int>(r % kTmaStages);
+    const int s = static_cast<int>(r % kS);
     const uint32_t ph = (phases >> s) & 1u;
     asm volatile(
         "{\n .reg .pred p;\n W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -629,10 +639,10 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
       for (int j = 0; j < cnt; ++j) {
         const int pn = T.np[j];
         if (pn == 0) continue;  // nothing to move in this chunk
-        if (fed >= kTmaStages - 1) retire(fed - (kTmaStages - 1));
-        if (fed >= kTmaStages)  // stage of chunk fed-3 is free once its store has read smem
+        if (fed >= kS - 1) retire(fed - (kS - 1));
+        if (fed >= kS)  // stage of chunk fed-3 is free once its store has read smem
           asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        const int s = static_cast<int>(fed % kTmaStages);
+        const int s = static_cast<int>(fed % kS);
         uint32_t tot = 0;
         for (int p = 0; p < pn; ++p) tot += T.bytes[j][p];
         const uint32_t bar = smem_u32(&T.bar[s]);
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
     __syncwarp();
   }
   if (lane == 0) {
-    for (int64_t r = fed - (kTmaStages - 1) > 0 ? fed - (kTmaStages - 1) : 0; r < fed; ++r)
+    for (int64_t r = fed - (kS - 1) > 0 ? fed - (kS - 1) : 0; r < fed; ++r)
       retire(r);
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (MODE == kPut) {
@@ -981,14 +991,15 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
     }();
     const bool fat = mode == kPut && free_sms > 0;
     const int tma_grid = fat ? kSMs - free_sms : kSMs * ctas_per_sm;
-    const int sm_req = fat ? 227 * 1024 - static_cast<int>(sizeof(TmaTable)) - 64 : sm;
+    const int sm_put = kTmaPutStages * kTmaChunk;
+    const int sm_req = fat ? 227 * 1024 - static_cast<int>(sizeof(TmaTable)) - 64 : sm_put;
     static PerDeviceOnce attr_done;
     const int rc_attr = attr_done([&]() -> int {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kLocal>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kUnpack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         free_sms > 0 ? sm_req : sm));
+                                         sm_req));
       return ORCH_OK;
     });
     if (rc_attr) return rc_attr;
