@@ -505,6 +505,12 @@ def run_b200(args):
         e2e_step()
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - w0)
+    if os.environ.get("ORCH_BENCH_TRACE"):  # the metadata sub-steps of the last e2e steps
+        mm = meta_marks[-5 * 2 * len(st):]
+        for i in range(0, len(mm), 5):
+            g = [mm[i].elapsed_time(mm[i + j]) for j in range(1, 5)]
+            print(f"[trace r{rank}] e2e meta allgather {g[0]:.3f} balance {g[1] - g[0]:.3f} "
+                  f"nodewise {g[2] - g[1]:.3f} layout {g[3] - g[2]:.3f} ms", file=sys.stderr)
 
     # load balance (stats_of max/mean, orchestrator.cpp:91-102)
     imb = {}

@@ -184,6 +184,7 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
                        : sm == static_cast<int>(sizeof(SmallSmem<4>)) ? 1 : 2;
       const int rc_attr = configured[slot]([&]() -> int {
         ORCH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        ORCH_CUDA_TRY(max_carveout(kern));
         return ORCH_OK;
       });
       if (rc_attr) return rc_attr;

@@ -861,6 +861,12 @@ int orch_layout(orch_ctx* ctx, int32_t d, int32_t P, int64_t n, const int64_t* d
   auto st = static_cast<cudaStream_t>(stream);
   if (!L->status) return fail(ORCH_INVALID_ARGUMENT, "layout->status is required");
   if (n <= kLayoutSmallItems && d <= kLayoutSmallD) {
+    static PerDeviceOnce configured;
+    const int rc_attr = configured([&]() -> int {
+      ORCH_CUDA_TRY(max_carveout(k_layout_small));
+      return ORCH_OK;
+    });
+    if (rc_attr) return rc_attr;
     launch(ctx, [&] {
       k_layout_small<<<1, kLayoutSmallThreads, 0, st>>>(static_cast<int>(n), d, P, d_len, d_origin,
                                                         *bal, *L);
@@ -1000,6 +1006,10 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kUnpack>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_move_tma<kPut>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sm_req));
+      ORCH_CUDA_TRY(max_carveout(k_move_tma<kLocal>));
+      ORCH_CUDA_TRY(max_carveout(k_move_tma<kPack>));
+      ORCH_CUDA_TRY(max_carveout(k_move_tma<kUnpack>));
+      ORCH_CUDA_TRY(max_carveout(k_move_tma<kPut>));
       return ORCH_OK;
     });
     if (rc_attr) return rc_attr;
@@ -1560,6 +1570,12 @@ int orch_allgather_items_put(orch_ctx* ctx, orch_gather_window* g, int64_t local
   a.status = d_status;
   a.stamps = g->stamps;
   auto st = static_cast<cudaStream_t>(stream);
+  static PerDeviceOnce configured;
+  const int rc_attr = configured([&]() -> int {
+    ORCH_CUDA_TRY(max_carveout(k_gather_put));
+    return ORCH_OK;
+  });
+  if (rc_attr) return rc_attr;
   launch(ctx, [&] { k_gather_put<<<1, 1024, 0, st>>>(a); });
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;

@@ -1105,6 +1105,8 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(Prep<kHostMaxD>))));
+    ORCH_CUDA_TRY(max_carveout(k_host_bb));
+    ORCH_CUDA_TRY(max_carveout(k_host_setup));
     return ORCH_OK;
   });
   if (rc_attr) return rc_attr;
@@ -1193,6 +1195,7 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
     const int rc_attr = configured([&]() -> int {
       ORCH_CUDA_TRY(cudaFuncSetAttribute(k_nodewise_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sizeof(NwSmem))));
+      ORCH_CUDA_TRY(max_carveout(k_nodewise_small));
       return ORCH_OK;
     });
     if (rc_attr) return rc_attr;
