@@ -139,6 +139,14 @@ int orch_balance(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
                  const int64_t* d_len, const int32_t* d_origin, int32_t identity_only,
                  const orch_balance_out* out, void* stream);
 
+/* orch_balance followed by orch_layout for one rank (P = 1), in one launch when
+ * the phase fits the single-CTA balance kernel (n <= 4096, d <= 64), else the
+ * two calls. Same outputs as the pair. Every layout array is required. */
+int orch_balance_layout1(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                         const int64_t* d_len, const int32_t* d_origin, int32_t identity_only,
+                         const orch_balance_out* out, const orch_layout_out* layout,
+                         void* stream);
+
 /* Host-buffer variant: copies h_len/h_origin in, runs orch_balance, copies
  * the flat result out (any h_ output may be NULL) and synchronises. Returns
  * the reference's error class. */

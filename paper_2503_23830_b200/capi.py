@@ -22,7 +22,7 @@ CUDA_ERROR, NCCL_ERROR, UNSUPPORTED = 10, 11, 12
 
 EXPORTED = [
     "orch_ctx_create", "orch_ctx_destroy", "orch_last_error", "orch_version",
-    "orch_ctx_launches", "orch_balance", "orch_balance_host",
+    "orch_ctx_launches", "orch_balance", "orch_balance_layout1", "orch_balance_host",
     "orch_min_feasible_padded_bound_host", "orch_padded_bound_feasible_host",
     "orch_oracle_optimal_host",
     "orch_batch_costs", "orch_batch_costs_host", "orch_volume_matrix_host", "orch_group_by_origin", "orch_encode_lengths", "orch_volume_matrix",
@@ -296,6 +296,20 @@ class Context:
                                   _ptr(origin), C.c_int32(1 if identity_only else 0), C.byref(s),
                                   _stream(stream)))
         return out
+
+    def balance_layout1(self, kind, d, length, origin, lam=0.0, v=0, identity_only=False,
+                        out=None, layout=None, stream=None):
+        """orch_balance_layout1: balance + the single-rank layout (fused when small)."""
+        n = int(length.numel())
+        out = out or Balance.alloc(d, n, length.device)
+        layout = layout or Layout.alloc(1, n, length.device)
+        pol = Policy(kind, 0, v, lam)
+        _check(lib().orch_balance_layout1(self.h, C.byref(pol), C.c_int32(d), C.c_int64(n),
+                                          _ptr(length), _ptr(origin),
+                                          C.c_int32(1 if identity_only else 0),
+                                          C.byref(out.struct()), C.byref(layout.struct()),
+                                          _stream(stream)))
+        return out, layout
 
     def balance_host(self, kind, d, length, origin, lam=0.0, v=0, identity_only=False):
         """numpy in / numpy out through orch_balance_host (synchronous)."""

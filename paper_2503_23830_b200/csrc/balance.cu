@@ -134,7 +134,9 @@ int check_policy_args(const orch_policy* p, int d, int64_t n, int identity_only)
 // mode: 0 balance, 1 identity only, 2 padded search only, 3 padded feasibility probe
 int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const int64_t* len,
                 const int32_t* origin, int mode, int64_t probe, const orch_balance_out* out,
-                int64_t* d_bound_out, int32_t* d_probe_out, cudaStream_t st) {
+                int64_t* d_bound_out, int32_t* d_probe_out, cudaStream_t st,
+                const orch_layout_out* lay1 = nullptr, bool* lay1_done = nullptr) {
+  if (lay1_done) *lay1_done = false;
   const int identity_only = mode == 1;
   if (!out || !out->summary) return fail(ORCH_INVALID_ARGUMENT, "orch_balance: summary required");
   orch_summary* S = out->summary;
@@ -178,6 +180,11 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
     a.len = len;
     a.origin = origin;
     a.s = S;
+    if (lay1) {  // the single-rank layout in the same launch
+      a.with_layout = 1;
+      a.lay = *lay1;
+      if (lay1_done) *lay1_done = true;
+    }
     auto run_small = [&](auto kern, int sm) -> int {
       static PerDeviceOnce configured[3];  // per instantiation
       const int slot = sm == static_cast<int>(sizeof(SmallSmem<2>)) ? 0
@@ -483,6 +490,29 @@ int orch_balance(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
   ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
   return orchb::run_balance(ctx, policy, d, n, d_len, d_origin, identity_only ? 1 : 0, 0, out,
                             nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int orch_balance_layout1(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
+                         const int64_t* d_len, const int32_t* d_origin, int32_t identity_only,
+                         const orch_balance_out* out, const orch_layout_out* layout,
+                         void* stream) {
+  if (!ctx) return orchb::fail(ORCH_INVALID_ARGUMENT, "null context");
+  if (!layout || !layout->status || !layout->rank_src_off || !layout->rank_dst_off ||
+      !layout->pair_off || !layout->send_rows || !layout->send_displ || !layout->recv_displ ||
+      !layout->in_rows || !layout->out_rows)
+    return orchb::fail(ORCH_INVALID_ARGUMENT, "orch_balance_layout1: every layout array is required");
+  if (!out || !out->dest_inst || !out->src_off || !out->dst_off || !out->bin_offset ||
+      !out->bin_member)
+    return orchb::fail(ORCH_INVALID_ARGUMENT,
+                       "orch_balance_layout1 needs dest_inst, src_off, dst_off, bin_offset, bin_member");
+  int rc = orchb::check_policy_args(policy, d, n, identity_only);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
+  bool fused = false;
+  rc = orchb::run_balance(ctx, policy, d, n, d_len, d_origin, identity_only ? 1 : 0, 0, out,
+                          nullptr, nullptr, static_cast<cudaStream_t>(stream), layout, &fused);
+  if (rc || fused) return rc;
+  return orch_layout(ctx, d, 1, n, d_len, d_origin, out, layout, stream);
 }
 
 }  // extern "C"

@@ -62,6 +62,9 @@ struct SmallArgs {
   int32_t* src_offset;
   int32_t* src_member;
   orch_summary* s;
+  // optional: the single-rank layout (orch_layout with P = 1), fused
+  int with_layout;
+  orch_layout_out lay;
 };
 
 template <int ITEMS>
@@ -840,6 +843,47 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       a.bin_member[i] = S.ord_id[i];
     }
     if (tid <= d) a.bin_offset[tid] = S.off_id[tid];
+  }
+  if (a.with_layout) {
+    // orch_layout for one rank (k_layout_small with P = 1): every instance on
+    // rank 0, origin batches in instance order in the input buffer, destination
+    // batches in instance order in the output buffer; the (0 -> 0) segment is
+    // the whole output, so pair_off = rank_dst_off.
+    __syncthreads();  // the identity epilogue's dst_off stores
+    if (warp == 0) {  // instance bases: exclusive scans over d <= 64 batch totals
+      for (int side = 0; side < 2; ++side) {
+        const int64_t* tok = side ? S.b_tok[w] : S.b_tok[1];
+        int64_t* base = side ? S.tok_a : S.seed_load;  // free here
+        const int64_t t0 = lane < d ? tok[lane] : 0, t1 = lane + 32 < d ? tok[lane + 32] : 0;
+        int64_t i0 = t0, i1 = t1;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t u0 = __shfl_up_sync(~0u, i0, o), u1 = __shfl_up_sync(~0u, i1, o);
+          if (lane >= o) {
+            i0 += u0;
+            i1 += u1;
+          }
+        }
+        const int64_t half = __shfl_sync(~0u, i0, 31);
+        if (lane < d) base[lane] = i0 - t0;
+        if (lane + 32 < d) base[lane + 32] = half + i1 - t1;
+        if (side == 1 && lane == 0) {
+          const int64_t total = static_cast<int64_t>(S.total);
+          a.lay.in_rows[0] = total;
+          a.lay.out_rows[0] = total;
+          a.lay.send_rows[0] = total;
+          a.lay.send_displ[0] = 0;
+          a.lay.recv_displ[0] = 0;
+          *a.lay.status = 0;
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += kSmallThreads) {
+      const int64_t rd = a.dst_off[i] + S.tok_a[w ? S.org[i] : S.a_dest[i]];
+      a.lay.rank_src_off[i] = a.src_off[i] + S.seed_load[S.org[i]];
+      a.lay.rank_dst_off[i] = rd;
+      a.lay.pair_off[i] = rd;
+    }
   }
   SMALL_MARK(7);
 }

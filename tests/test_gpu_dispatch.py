@@ -74,6 +74,29 @@ def test_layout_multi_kernel_path(ctx, oracle, P, d, n):
         np.testing.assert_array_equal(lay.send_rows.cpu().numpy().reshape(P, P), e["send_tokens"])
 
 
+def test_balance_layout1_matches_the_pair(ctx, oracle):
+    """orch_balance_layout1 (balance + single-rank layout in one launch when small,
+    else the two calls) equals orch_balance followed by orch_layout(P = 1)."""
+    rng = np.random.default_rng(1234)
+    cases = [(int(rng.integers(1, 65)), int(rng.integers(1, 4097))) for _ in range(24)]
+    cases += [(8, 301), (64, 4096), (65, 500), (8, 4097), (300, 6000)]
+    for t, (d, n) in enumerate(cases):
+        kind = t % 4
+        length, origin = make_case(rng, d, n, hi=int(rng.choice([3, 900, 70000])), kind=kind)
+        L, O = to_dev(length, np.int64), to_dev(origin, np.int32)
+        for ident in (False, True):
+            b1 = ctx.balance(kind, d, L, O, lam=1e-4, v=64, identity_only=ident)
+            l1 = ctx.layout(d, 1, L, O, b1)
+            b2, l2 = ctx.balance_layout1(kind, d, L, O, lam=1e-4, v=64, identity_only=ident)
+            torch.cuda.synchronize()
+            for k in ("dest_inst", "dest_slot", "src_off", "dst_off"):
+                assert torch.equal(getattr(b1, k)[:n], getattr(b2, k)[:n]), (d, n, kind, k)
+            for k in ("rank_src_off", "rank_dst_off", "pair_off"):
+                assert torch.equal(getattr(l1, k)[:n], getattr(l2, k)[:n]), (d, n, kind, ident, k)
+            for k in ("send_rows", "send_displ", "recv_displ", "in_rows", "out_rows", "status"):
+                assert torch.equal(getattr(l1, k), getattr(l2, k)), (d, n, kind, ident, k)
+
+
 def test_volume_matrix(ctx, oracle):
     rng = np.random.default_rng(3)
     for d in (1, 3, 8, 64, 300):
