@@ -1,4 +1,4 @@
-"""World-size-2 gloo test of the N>1 host logic (CPU): local shards by origin
+"""World-size-2 and -4 gloo tests of the N>1 host logic (CPU): local shards by origin
 rank, the length all-gather (records scattered back into input order), and the
 rank-level exchange layout (send/recv displacements, pair offsets) realised
 with gloo send/recv on host buffers -- the same protocol orch_allgather_items /
@@ -122,11 +122,12 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_exchange_protocol_gloo():
+@pytest.mark.parametrize("world", [2, 4])
+def test_exchange_protocol_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]
