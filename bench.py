@@ -329,13 +329,23 @@ def run_b200(args):
         s["moved_rows"] = out_rows  # every row of this rank's output is written once
         s["send_rows"] = int(S[rank].sum() - S[rank, rank])
         s["recv_rows"] = int(S[:, rank].sum() - S[rank, rank])
-        s["win"] = None
-        if P > 1 and args.exchange == "put":
-            wrows = int(lay.out_rows.max().item())
-            s["win"] = Window(ctx_data, comm_data, max(wrows, 1) * R)
-            s["rout"] = s["win"].tensor_view(dev)
-        else:
-            s["rout"] = torch.empty(max(out_rows, 1) * R, dtype=torch.uint8, device=dev)
+        s["wrows"] = max(int(lay.out_rows.max().item()), 1)
+    # N>1 put: the phases of a step share one window (one barrier, one release),
+    # each phase's output at its own offset
+    win = None
+    if P > 1 and args.exchange == "put":
+        off = 0
+        for s in st:
+            s["win_off"] = off
+            off += s["wrows"] * R
+        win = Window(ctx_data, comm_data, off)
+        wview = win.tensor_view(dev)
+        for s in st:
+            s["rout"] = wview[s["win_off"]:s["win_off"] + s["wrows"] * R]
+    else:
+        for s in st:
+            s["rout"] = torch.empty(max(s["buf"][0]["lay"].out_rows[rank].item(), 1) * R,
+                                    dtype=torch.uint8, device=dev)
     rin = torch.randint(0, 255, (max(max(s["in_rows"] for s in st), 1) * R,), dtype=torch.uint8,
                         device=dev)
     send = recv = None
@@ -386,12 +396,16 @@ def run_b200(args):
                 e0.record(data_stream)
             if os.environ.get("ORCH_BENCH_NOMOVE"):  # diagnostics only: metadata alone
                 pass
-            elif s["win"] is not None:  # one barrier per step closes both phases' puts
+            elif win is not None:  # one barrier per step closes both phases' puts
                 ctx_data.put(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
-                             s["win"], comm_data, stream=data_stream)
+                             win, comm_data, offset=s["win_off"], stream=data_stream)
                 if s is st[-1]:
                     if args.barrier == "window":  # peer-memory flags (one 1-warp kernel)
-                        ctx_data.window_barrier(s["win"], stream=data_stream)
+                        ctx_data.window_barrier(win, stream=data_stream)
+                        # the consumer of the rows (the encoder / LLM forward) runs
+                        # here; then the window is released, which the next step's
+                        # puts on every rank wait for (write-after-read guard)
+                        ctx_data.window_release(win, stream=data_stream)
                     elif args.barrier == "nccl":
                         ctx_data.barrier(comm_data, stream=data_stream)
             else:
@@ -604,10 +618,11 @@ def run_b200(args):
                                                        f"{host_bytes / 1e9:.0f} GB"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    for s in st:
-        if s.get("win") is not None:
+    if win is not None:
+        for s in st:
             s["rout"] = None
-            s["win"].close()
+        wview = None
+        win.close()
     for gwin in gwins:
         if gwin is not None:
             gwin.close()

@@ -56,7 +56,11 @@ extern "C" {
 #define ORCH_MAX_ITEMS 16777215        /* n < 2^24                                */
 #define ORCH_MAX_LENGTH 4294967295LL   /* per-item length < 2^32                  */
 
-typedef struct orch_ctx orch_ctx;   /* per-device workspace; not thread-safe, one per host thread */
+/* Per-device context. Device-pointer calls on different streams get separate
+ * workspaces, so one context may feed several streams (16 at a time; a call on
+ * a 17th stream first synchronises the device and recycles a workspace). A
+ * context is used by one host thread at a time (not thread-safe). */
+typedef struct orch_ctx orch_ctx;
 typedef struct orch_comm orch_comm; /* NCCL communicator over the ranks of one box               */
 
 /* BalancePolicy (balancers.hpp:14-18). */
@@ -207,11 +211,11 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_pa
 /* solve_hosting (topology.hpp:71, topology.cpp:179-265) on a host volume
  * matrix h_V[d*d] with c instances per node: exact (the reference's answer,
  * including its tie-breaking) by a parallel two-pass branch and bound on the
- * device; ORCH_UNSUPPORTED when d > 64 or d/c > 32 nodes. A search that
- * exceeds 2^31 visited nodes keeps the incumbent (info[2] = -1 below). */
+ * device; ORCH_UNSUPPORTED when d > 64 or d/c > 32 nodes. h_info (optional,
+ * [4]) as orch_nodewise's d_info below. A search that exceeds 2^31 visited
+ * nodes returns ORCH_UNSUPPORTED (h_hosting then holds the incumbent). */
 int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
-                            int32_t* h_hosting, int64_t* h_max_egress, int64_t* h_baseline_max,
-                            void* stream);
+                            int32_t* h_hosting, int64_t* h_info, void* stream);
 
 /* nodewise_rearrange (topology.hpp:87, topology.cpp:267-303) applied in place
  * to a balance result: volume matrix of the result, optimal hosting, then
@@ -220,7 +224,9 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
  * rank per node this is the GPU-wise hosting that cuts NVLink egress.
  * d_info = {max_egress, baseline_max_egress (identity hosting), leaf_used
  * (1: a search leaf beat the identity/greedy incumbents, 0: incumbent,
- * -1: visit budget exhausted, incumbent kept), nodes visited}. */
+ * -1: visit budget exhausted, incumbent kept), nodes visited by the device
+ * search (its parallel order prunes differently from the reference's
+ * sequential DFS, so this is not the reference's count)}. */
 int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t* d_len,
                   const int32_t* d_origin, const orch_balance_out* bal, int32_t* d_hosting,
                   int32_t* d_batch_to_instance, int64_t* d_info, void* stream);
@@ -263,6 +269,48 @@ int orch_volume_matrix(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len
 int orch_volume_matrix_host(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* h_len,
                             const int32_t* h_origin, const int32_t* h_dest_inst, int64_t* h_V,
                             void* stream);
+
+/* ExchangeCostReport (exchange.hpp:27-35) without its per-node vector. */
+typedef struct {
+  double modeled_time;
+  int64_t total_inter_volume;
+  int64_t total_intra_volume;
+  int64_t local_volume;
+  int64_t peak_resident_volume;
+  int32_t bottleneck; /* Bottleneck (exchange.hpp:25): 0 None, 1 IntraNode, 2 InterNode */
+  int32_t stale;      /* 1: d_V is not the volume matrix of the given items */
+} orch_exchange_cost;
+
+/* simulate_exchange's cost report (exchange.cpp:64-111) as one device
+ * reduction over the volume matrix d_V[d*d] (src-major; the plan's
+ * per_pair_volumes) for c instances per node: inter / intra / local volume,
+ * per-node egress (d_per_node_egress[d/c]), peak resident volume, modeled time
+ * (alltoall_constant x the slowest instance's inter/inter_bw + intra/intra_bw,
+ * mode 0 = AllToAll) or the ring bound (d-1) max L / inter_bw (mode 1 =
+ * AllGather, needs d_batch_len[d] = batch_length of the input batches) and
+ * the bottleneck, bit-identical to the reference. With items (n >= 0, d_len,
+ * d_src_inst, d_dst_inst: the plan's rearrangement) the plan is also checked
+ * against their volume matrix (exchange.cpp:57-60): d_report->stale.
+ * Topology errors as validate_topology (topology.cpp:12-22). */
+int orch_exchange_report(orch_ctx* ctx, int32_t d, int32_t c, double intra_bw, double inter_bw,
+                         double alltoall_constant, int32_t mode, const int64_t* d_V,
+                         const int64_t* d_batch_len, int64_t n, const int64_t* d_len,
+                         const int32_t* d_src_inst, const int32_t* d_dst_inst,
+                         int64_t* d_per_node_egress, orch_exchange_cost* d_report, void* stream);
+/* Host-buffer variant (synchronous): a stale plan returns ORCH_INVALID_ARGUMENT
+ * with the reference's message. */
+int orch_exchange_report_host(orch_ctx* ctx, int32_t d, int32_t c, double intra_bw,
+                              double inter_bw, double alltoall_constant, int32_t mode,
+                              const int64_t* h_V, const int64_t* h_batch_len, int64_t n,
+                              const int64_t* h_len, const int32_t* h_src_inst,
+                              const int32_t* h_dst_inst, int64_t* h_per_node_egress,
+                              orch_exchange_cost* h_report, void* stream);
+/* make_exchange_plan's AllGather volumes (exchange.cpp:17-28):
+ * V[i][j] = batch_len[i] for j != i, 0 on the diagonal. */
+int orch_allgather_volumes(orch_ctx* ctx, int32_t d, const int64_t* d_batch_len, int64_t* d_V,
+                           void* stream);
+int orch_allgather_volumes_host(orch_ctx* ctx, int32_t d, const int64_t* h_batch_len,
+                                int64_t* h_V, void* stream);
 
 /* Send/recv layout of the exchange (make_exchange_plan, exchange.cpp:10-32,
  * realised on ranks): offsets, per-pair counts. Needs the balance result's
@@ -317,35 +365,76 @@ int orch_barrier(orch_comm* comm, void* stream);
 
 /* A row buffer every rank can store into over NVLink (cudaMalloc + CUDA IPC
  * handles exchanged over the communicator). Collective: every rank calls it
- * with the same size. */
+ * with the same size; the sizes are exchanged with the handles and a mismatch
+ * fails on every rank (ORCH_INVALID_ARGUMENT) before any peer is mapped.
+ *
+ * One step of a put exchange, on every rank (the protocol INTEGRATION.md 2
+ * spells out):
+ *   orch_put / orch_put_at      (any number, into disjoint window ranges)
+ *   orch_window_barrier         every rank's puts of the step have landed here
+ *   ... consumers read this rank's window ...
+ *   orch_window_release         after the last consumer kernel (stream order)
+ * The first put after the e-th barrier (per stream) is preceded by a one-warp
+ * kernel that waits, on the device, until every rank has released e steps, so
+ * the next step's puts never overwrite rows a peer is still reading
+ * (write-after-read); the wait holds one warp, not the put's CTAs, so the
+ * consumers keep the SMs they need. Waits give up after ~4 s: the barrier or
+ * the acquire sets the window status, and a put whose acquire timed out sets
+ * layout->status to ORCH_CUDA_ERROR and stores nothing. */
 typedef struct orch_window orch_window;
 int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out);
 void* orch_window_ptr(const orch_window* w);
 size_t orch_window_bytes(const orch_window* w);
 int orch_window_destroy(orch_window* w); /* collective */
 /* Barrier through the window's peer memory (one 1-warp kernel, no NCCL):
- * lane q stores this rank's call count into rank q's flag slot with a
+ * lane q stores this rank's call count into rank q's arrival slot with a
  * system-scope release, then waits for every rank's store into its own slots
  * (acquire). Everything earlier on `stream` (e.g. this step's puts) is visible
  * to every rank once its barrier returns. Collective: every rank calls it the
- * same number of times on the same window. Replaces orch_barrier after puts. */
+ * same number of times on the same window. */
 int orch_window_barrier(orch_ctx* ctx, orch_window* w, void* stream);
+/* The rows of the oldest unreleased barrier-closed step have been consumed on
+ * this rank (everything earlier on `stream` is done reading the window): one
+ * 1-warp kernel stores the release count into every rank's window. */
+int orch_window_release(orch_ctx* ctx, orch_window* w, void* stream);
+/* 0, or ORCH_CUDA_ERROR when a barrier on this window timed out (synchronous
+ * read; call after the streams that used the window have been synchronised). */
+int orch_window_status(const orch_window* w, int32_t* h_status);
 
 /* Fused pack + put exchange: every item's rows are
  * read once from this rank's d_in and stored directly at their final
  * destination-slot offset in the destination rank's window (TMA bulk stores
- * over NVLink to peer memory); a communicator barrier on the stream then
- * publishes the windows. Same result bytes as orch_dispatch. */
+ * over NVLink to peer memory); orch_window_barrier on the stream then
+ * publishes the windows. Same result bytes as orch_dispatch. The caller
+ * releases the window (orch_window_release) once the rows are consumed. */
 int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
                       const int32_t* d_origin, const orch_balance_out* bal,
                       const orch_layout_out* layout, size_t row_bytes, const void* d_in,
                       int64_t in_cap, orch_window* out_win, void* stream);
 /* The put alone (no barrier): several exchanges (e.g. the phases of one
- * iteration) can share one orch_barrier. */
+ * iteration) can share one window barrier. orch_put_at stores this exchange's
+ * output at byte offset win_offset (a multiple of 16) of every rank's window,
+ * so the phases of a step share one window, one barrier and one release. */
 int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
              const int32_t* d_origin, const orch_balance_out* bal,
              const orch_layout_out* layout, size_t row_bytes, const void* d_in, int64_t in_cap,
              orch_window* out_win, void* stream);
+int orch_put_at(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                const int32_t* d_origin, const orch_balance_out* bal,
+                const orch_layout_out* layout, size_t row_bytes, const void* d_in,
+                int64_t in_cap, orch_window* out_win, size_t win_offset, void* stream);
+
+/* ------------------------------------------ single-process rank emulation */
+/* P ranks in one process on one device (tests and single-GPU integration
+ * checks): a loopback communicator carries rank and size but no NCCL (the
+ * NCCL entry points refuse it), and orch_window_create_local makes the P
+ * windows of such communicators at once, each rank's peers being the other
+ * windows' device buffers. Puts, window barriers, releases and the gather
+ * window then run the same kernels as across GPUs; each emulated rank needs
+ * its own stream (a barrier waits for the other ranks' kernels). */
+int orch_comm_create_local(int32_t nranks, int32_t rank, orch_comm** out);
+int orch_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t nranks, size_t bytes,
+                             orch_window** out /* [nranks] */);
 
 /* gather_lengths (exchange.cpp:34-47) realised as ncclAllGather: every rank
  * contributes its local items (global input position, length, origin) and
@@ -370,6 +459,9 @@ typedef struct orch_gather_window orch_gather_window;
 int orch_gather_window_create(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
                               orch_gather_window** out); /* collective */
 int orch_gather_window_destroy(orch_gather_window* g);   /* collective */
+/* P gather windows of loopback communicators (see orch_window_create_local). */
+int orch_gather_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t nranks,
+                                    int64_t max_n, orch_gather_window** out /* [nranks] */);
 /* Diagnostics: %globaltimer (ns) at the stages of the last 8 calls, [epoch % 8][k]:
  * k = 0 start, 1 window free, 2 records stored + fenced, 3 all ranks arrived, 4 end. */
 int orch_gather_window_stamps(const orch_gather_window* g, uint64_t* h_out64);

@@ -39,7 +39,8 @@ def _nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu", "exhaustive.cu", "hosting.cu", "compose.cu"]
+CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu", "exhaustive.cu", "hosting.cu", "compose.cu",
+              "exchange.cu"]
 HOST_SOURCES = ["host/core.cpp", "host/balancers.cpp", "host/topology.cpp", "host/exchange.cpp",
                 "host/runtime.cpp"]
 
@@ -113,15 +114,18 @@ def build_ref_tests(force=False):
 
 
 def build_cpp_api_bench(force=False):
-    """scripts/cpp_api_bench.cpp against the B200 C++ API (timing tool)."""
-    out = os.path.join(LIB, "cpp_api_bench_b200")
-    src = os.path.join(ROOT, "scripts", "cpp_api_bench.cpp")
+    """scripts/cpp_api_{bench,exchange}.cpp against the B200 C++ API (timing and
+    parity tools; the same sources are built against the reference by oracle/Makefile)."""
     host = os.path.join(LIB, "liborchsim_b200_host.so")
-    if not force and not _stale(out, [src, host]):
-        return out
-    _run([CXX, "-std=c++20", "-O2", "-Wall", "-I", INCLUDE, "-o", out, src, "-L", LIB,
-          "-l:liborchsim_b200_host.so", "-Wl,-rpath,$ORIGIN"])
-    return out
+    outs = []
+    for name in ("cpp_api_bench", "cpp_api_exchange"):
+        out = os.path.join(LIB, f"{name}_b200")
+        src = os.path.join(ROOT, "scripts", f"{name}.cpp")
+        if force or _stale(out, [src, host]):
+            _run([CXX, "-std=c++20", "-O2", "-Wall", "-I", INCLUDE, "-o", out, src, "-L", LIB,
+                  "-l:liborchsim_b200_host.so", "-Wl,-rpath,$ORIGIN"])
+        outs.append(out)
+    return outs
 
 
 def build_all(force=False):

@@ -33,7 +33,10 @@ EXPORTED = [
     "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
     "orch_window_destroy", "orch_window_barrier", "orch_dispatch_put", "orch_put",
     "orch_gather_window_create", "orch_gather_window_destroy", "orch_allgather_items_put",
-    "orch_gather_window_stamps",
+    "orch_gather_window_stamps", "orch_window_release", "orch_window_status", "orch_put_at",
+    "orch_comm_create_local", "orch_window_create_local", "orch_gather_window_create_local",
+    "orch_exchange_report", "orch_exchange_report_host", "orch_allgather_volumes",
+    "orch_allgather_volumes_host",
 ]
 
 
@@ -105,6 +108,14 @@ def _check(rc):
 
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _on(stream):
+    """Allocate a call's outputs on the stream the call runs on, so the caching
+    allocator never hands them to other work while the call's kernels still
+    write them (outputs a caller drops are recycled in stream order)."""
+    import contextlib
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
 
 
 def _stream(stream=None):
@@ -191,11 +202,22 @@ class Layout:
 
 
 class Comm:
-    def __init__(self, nranks: int, rank: int, uid: bytes):
+    def __init__(self, nranks: int, rank: int, uid: bytes | None):
+        """NCCL communicator; uid=None makes a loopback one (rank emulation in
+        one process, orch_comm_create_local)."""
         self.h = C.c_void_p()
-        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
-        _check(lib().orch_comm_create(C.c_int32(nranks), C.c_int32(rank), buf, C.byref(self.h)))
+        if uid is None:
+            _check(lib().orch_comm_create_local(C.c_int32(nranks), C.c_int32(rank),
+                                                C.byref(self.h)))
+        else:
+            buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+            _check(lib().orch_comm_create(C.c_int32(nranks), C.c_int32(rank), buf,
+                                          C.byref(self.h)))
         self.rank, self.size = rank, nranks
+
+    @staticmethod
+    def local_group(nranks: int) -> list["Comm"]:
+        return [Comm(nranks, r, None) for r in range(nranks)]
 
     @staticmethod
     def unique_id() -> bytes:
@@ -212,11 +234,29 @@ class Comm:
 class Window:
     """orch_window: an IPC-shared row buffer of one rank (collective create)."""
 
-    def __init__(self, ctx: "Context", comm: Comm, nbytes: int):
+    def __init__(self, ctx: "Context", comm: Comm, nbytes: int, _handle=None):
         self.h = C.c_void_p()
-        _check(lib().orch_window_create(ctx.h, comm.h, C.c_size_t(nbytes), C.byref(self.h)))
+        if _handle is not None:
+            self.h = _handle
+        else:
+            _check(lib().orch_window_create(ctx.h, comm.h, C.c_size_t(nbytes),
+                                            C.byref(self.h)))
         self.nbytes = nbytes
         self.ptr = lib().orch_window_ptr(self.h)
+
+    @staticmethod
+    def local_group(ctx: "Context", comms: list[Comm], nbytes: int) -> list["Window"]:
+        """The windows of P loopback ranks in this process (orch_window_create_local)."""
+        P = len(comms)
+        hs = (C.c_void_p * P)()
+        cs = (C.c_void_p * P)(*[c.h.value for c in comms])
+        _check(lib().orch_window_create_local(ctx.h, cs, C.c_int32(P), C.c_size_t(nbytes), hs))
+        return [Window(ctx, comms[r], nbytes, _handle=C.c_void_p(hs[r])) for r in range(P)]
+
+    def status(self) -> int:
+        out = C.c_int32(0)
+        _check(lib().orch_window_status(self.h, C.byref(out)))
+        return out.value
 
     def tensor_view(self, device):
         """A uint8 torch view of this rank's window (no copy)."""
@@ -232,10 +272,23 @@ class Window:
 class GatherWindow:
     """orch_gather_window: peer-memory all-gather of item records (collective)."""
 
-    def __init__(self, ctx: "Context", comm: Comm, max_n: int):
+    def __init__(self, ctx: "Context", comm: Comm, max_n: int, _handle=None):
         self.h = C.c_void_p()
-        _check(lib().orch_gather_window_create(ctx.h, comm.h, C.c_int64(max_n), C.byref(self.h)))
+        if _handle is not None:
+            self.h = _handle
+        else:
+            _check(lib().orch_gather_window_create(ctx.h, comm.h, C.c_int64(max_n),
+                                                   C.byref(self.h)))
         self.max_n = max_n
+
+    @staticmethod
+    def local_group(ctx: "Context", comms: list[Comm], max_n: int) -> list["GatherWindow"]:
+        P = len(comms)
+        hs = (C.c_void_p * P)()
+        cs = (C.c_void_p * P)(*[c.h.value for c in comms])
+        _check(lib().orch_gather_window_create_local(ctx.h, cs, C.c_int32(P), C.c_int64(max_n),
+                                                     hs))
+        return [GatherWindow(ctx, comms[r], max_n, _handle=C.c_void_p(hs[r])) for r in range(P)]
 
     def stamps(self):
         """[8][8] %globaltimer ns of the last 8 calls' stages (diagnostics)."""
@@ -289,7 +342,8 @@ class Context:
                 stream=None) -> Balance:
         """length int64 / origin int32 CUDA tensors, input order."""
         n = int(length.numel())
-        out = out or Balance.alloc(d, n, length.device)
+        with _on(stream):
+            out = out or Balance.alloc(d, n, length.device)
         pol = Policy(kind, 0, v, lam)
         s = out.struct()
         _check(lib().orch_balance(self.h, C.byref(pol), C.c_int32(d), C.c_int64(n), _ptr(length),
@@ -301,8 +355,9 @@ class Context:
                         out=None, layout=None, stream=None):
         """orch_balance_layout1: balance + the single-rank layout (fused when small)."""
         n = int(length.numel())
-        out = out or Balance.alloc(d, n, length.device)
-        layout = layout or Layout.alloc(1, n, length.device)
+        with _on(stream):
+            out = out or Balance.alloc(d, n, length.device)
+            layout = layout or Layout.alloc(1, n, length.device)
         pol = Policy(kind, 0, v, lam)
         _check(lib().orch_balance_layout1(self.h, C.byref(pol), C.c_int32(d), C.c_int64(n),
                                           _ptr(length), _ptr(origin),
@@ -353,7 +408,8 @@ class Context:
     # ---- composed delivery
     def rearrange(self, d, length, src_inst, src_slot, dst_inst, dst_slot, stream=None):
         n = int(length.numel())
-        out = Balance.alloc(d, n, length.device)
+        with _on(stream):
+            out = Balance.alloc(d, n, length.device)
         b = out.struct()
         _check(lib().orch_rearrange(self.h, C.c_int32(d), C.c_int64(n), _ptr(length),
                                     _ptr(src_inst), _ptr(src_slot), _ptr(dst_inst),
@@ -364,8 +420,9 @@ class Context:
                          stream=None):
         E = part_offset.numel() - 1
         n = item_part.numel()
-        di = torch.empty(max(n, 1), dtype=torch.int32, device=part_offset.device)
-        ds = torch.empty(max(n, 1), dtype=torch.int32, device=part_offset.device)
+        with _on(stream):
+            di = torch.empty(max(n, 1), dtype=torch.int32, device=part_offset.device)
+            ds = torch.empty(max(n, 1), dtype=torch.int32, device=part_offset.device)
         _check(lib().orch_backbone_targets(self.h, C.c_int32(d), C.c_int64(E), _ptr(llm.dest_inst),
                                            _ptr(llm.bin_offset), _ptr(llm.bin_member),
                                            _ptr(part_offset), _ptr(interleave_pos),
@@ -378,20 +435,22 @@ class Context:
         import numpy as np
         V = np.ascontiguousarray(V, dtype=np.int64).reshape(-1)
         hosting = np.zeros(d, np.int32)
-        mx, base = C.c_int64(), C.c_int64()
+        info = np.zeros(4, np.int64)
         _check(lib().orch_solve_hosting_host(self.h, C.c_int32(d), C.c_int32(c),
                                              V.ctypes.data_as(C.c_void_p),
-                                             hosting.ctypes.data_as(C.c_void_p), C.byref(mx),
-                                             C.byref(base), _stream()))
-        return dict(hosting=hosting, max_egress=mx.value, baseline_max=base.value)
+                                             hosting.ctypes.data_as(C.c_void_p),
+                                             info.ctypes.data_as(C.c_void_p), _stream()))
+        return dict(hosting=hosting, max_egress=int(info[0]), baseline_max=int(info[1]),
+                    leaf_used=int(info[2]), visited=int(info[3]))
 
     def nodewise(self, d, c, length, origin, bal: "Balance", stream=None):
         """Relabels bal's destination batches in place; returns device tensors
         (hosting[d], batch_to_instance[d], info[4])."""
         dev = length.device
-        hosting = torch.empty(d, dtype=torch.int32, device=dev)
-        b2i = torch.empty(d, dtype=torch.int32, device=dev)
-        info = torch.empty(4, dtype=torch.int64, device=dev)
+        with _on(stream):
+            hosting = torch.empty(d, dtype=torch.int32, device=dev)
+            b2i = torch.empty(d, dtype=torch.int32, device=dev)
+            info = torch.empty(4, dtype=torch.int64, device=dev)
         b = bal.struct()
         _check(lib().orch_nodewise(self.h, C.c_int32(d), C.c_int32(c), C.c_int64(length.numel()),
                                    _ptr(length), _ptr(origin), C.byref(b), _ptr(hosting),
@@ -401,8 +460,9 @@ class Context:
     # ---- cost model
     def batch_costs(self, alpha, beta, padded, variant, batch_padded, d, length, bin_offset,
                     bin_member, stream=None):
-        cost = torch.empty(d, dtype=torch.float64, device=length.device)
-        stats = torch.empty(3, dtype=torch.float64, device=length.device)
+        with _on(stream):
+            cost = torch.empty(d, dtype=torch.float64, device=length.device)
+            stats = torch.empty(3, dtype=torch.float64, device=length.device)
         m = CostModel(alpha, beta, padded, variant)
         _check(lib().orch_batch_costs(self.h, C.byref(m), C.c_int32(batch_padded), C.c_int32(d),
                                       C.c_int64(length.numel()), _ptr(length), _ptr(bin_offset),
@@ -411,8 +471,9 @@ class Context:
 
     def group_by_origin(self, d, origin, stream=None):
         n = origin.numel()
-        off = torch.empty(d + 1, dtype=torch.int32, device=origin.device)
-        mem = torch.empty(max(n, 1), dtype=torch.int32, device=origin.device)
+        with _on(stream):
+            off = torch.empty(d + 1, dtype=torch.int32, device=origin.device)
+            mem = torch.empty(max(n, 1), dtype=torch.int32, device=origin.device)
         _check(lib().orch_group_by_origin(self.h, C.c_int32(d), C.c_int64(n), _ptr(origin),
                                           _ptr(off), _ptr(mem), _stream(stream)))
         return off, mem[:n]
@@ -421,8 +482,9 @@ class Context:
         import numpy as np
         E = part_offset.numel() - 1
         rates = np.ascontiguousarray(rates, dtype=np.int64)
-        enc = torch.empty_like(meta_len)
-        inter = torch.empty(max(E, 1), dtype=torch.int64, device=meta_len.device)
+        with _on(stream):
+            enc = torch.empty_like(meta_len)
+            inter = torch.empty(max(E, 1), dtype=torch.int64, device=meta_len.device)
         _check(lib().orch_encode_lengths(self.h, C.c_int64(E), _ptr(part_offset), _ptr(modality),
                                          _ptr(meta_len), C.c_int32(len(rates)),
                                          rates.ctypes.data_as(C.c_void_p), _ptr(enc),
@@ -431,7 +493,8 @@ class Context:
 
     # ---- layout / movement
     def volume_matrix(self, d, length, origin, dest_inst, stream=None):
-        V = torch.empty(d * d, dtype=torch.int64, device=length.device)
+        with _on(stream):
+            V = torch.empty(d * d, dtype=torch.int64, device=length.device)
         _check(lib().orch_volume_matrix(self.h, C.c_int32(d), C.c_int64(length.numel()),
                                         _ptr(length), _ptr(origin), _ptr(dest_inst), _ptr(V),
                                         _stream(stream)))
@@ -440,7 +503,8 @@ class Context:
     def layout(self, d, P, length, origin, bal: Balance, out: Layout | None = None,
                stream=None) -> Layout:
         n = length.numel()
-        out = out or Layout.alloc(P, n, length.device)
+        with _on(stream):
+            out = out or Layout.alloc(P, n, length.device)
         b, lo = bal.struct(), out.struct()
         _check(lib().orch_layout(self.h, C.c_int32(d), C.c_int32(P), C.c_int64(n), _ptr(length),
                                  _ptr(origin), C.byref(b), C.byref(lo), _stream(stream)))
@@ -493,14 +557,19 @@ class Context:
                                        _stream(stream)))
 
     def put(self, d, length, origin, bal: Balance, lay: Layout, row_bytes, rows_in,
-            window: "Window", comm: Comm, stream=None):
-        """Fused pack+put without the closing barrier (call barrier() after)."""
+            window: "Window", comm: Comm, offset=0, stream=None):
+        """Fused pack+put without the closing barrier (window_barrier() after),
+        into byte `offset` of every rank's window (orch_put_at)."""
         b, lo = bal.struct(), lay.struct()
         R = row_bytes
-        _check(lib().orch_put(self.h, comm.h, C.c_int32(d), C.c_int64(length.numel()),
-                              _ptr(length), _ptr(origin), C.byref(b), C.byref(lo), C.c_size_t(R),
-                              _ptr(rows_in), C.c_int64(self._rows(rows_in, R)), window.h,
-                              _stream(stream)))
+        _check(lib().orch_put_at(self.h, comm.h, C.c_int32(d), C.c_int64(length.numel()),
+                                 _ptr(length), _ptr(origin), C.byref(b), C.byref(lo),
+                                 C.c_size_t(R), _ptr(rows_in), C.c_int64(self._rows(rows_in, R)),
+                                 window.h, C.c_size_t(offset), _stream(stream)))
+
+    def window_release(self, window: "Window", stream=None):
+        """orch_window_release: this rank has consumed the window's current step."""
+        _check(lib().orch_window_release(self.h, window.h, _stream(stream)))
 
     @staticmethod
     def barrier(comm: Comm, stream=None):

@@ -523,18 +523,6 @@ int orch_balance_layout1(orch_ctx* ctx, const orch_policy* policy, int32_t d, in
 // (pageable cudaMemcpyAsync calls cost ~10 us each; a call used to make eight).
 namespace {
 
-int stage_reserve(orch_ctx* ctx, size_t bytes) {
-  if (bytes <= ctx->stage_cap) return ORCH_OK;
-  if (ctx->stage) cudaFree(ctx->stage);
-  ctx->stage = nullptr;
-  ctx->stage_cap = 0;
-  size_t cap = 1 << 20;
-  while (cap < bytes) cap *= 2;
-  ORCH_CUDA_TRY(cudaMalloc(&ctx->stage, cap));
-  ctx->stage_cap = cap;
-  return ORCH_OK;
-}
-
 int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
                   const int64_t* h_len, const int32_t* h_origin, int mode, int64_t probe,
                   int32_t* h_dest_inst, int32_t* h_dest_slot, int64_t* h_dst_off,
@@ -557,11 +545,9 @@ int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n
   const size_t o_bc = take(static_cast<size_t>(d) * 4), o_cost = take(static_cast<size_t>(d) * 8);
   const size_t o_sum = take(sizeof(orch_summary)), o_bound = take(8), o_probe = take(8);
   const size_t total = at;
-  int rc = stage_reserve(ctx, total);
+  char *hp, *dp;
+  int rc = orchb::host_stage(ctx, total, &hp, &dp);
   if (rc) return rc;
-  char* hp = static_cast<char*>(orchb::pinned(ctx, total));
-  if (!hp) return orchb::fail(ORCH_CUDA_ERROR, "pinned staging allocation failed");
-  char* dp = static_cast<char*>(ctx->stage);
   orch_balance_out out{};
   // only the outputs this mode reads back are written by the pipeline
   const bool rows = n > 0 && mode < 2;

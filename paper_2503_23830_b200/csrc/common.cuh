@@ -14,6 +14,7 @@
 namespace orchb {
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+constexpr int kMaxCtxStreams = 16;  // distinct streams one orch_ctx serves
 
 // Thread-local message for orch_last_error().
 void set_error(const std::string& msg);
@@ -26,7 +27,7 @@ int fail(int code, const std::string& msg);
       return ::orchb::fail(ORCH_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
-// Device workspace: one growable arena per context; carve() hands out
+// Device workspace: one growable arena per (context, stream); carve() hands out
 // 256-byte aligned slices that stay valid until the next reset().
 struct Arena {
   char* base = nullptr;
@@ -39,7 +40,15 @@ struct Arena {
 
 struct orch_ctx {
   int device = 0;
-  orchb::Arena arena;
+  // One workspace per stream: calls on different streams never share scratch
+  // (calls on one stream are ordered by the stream, so they may reuse it).
+  struct StreamArena {
+    cudaStream_t stream;
+    orchb::Arena arena;
+  };
+  StreamArena arenas[orchb::kMaxCtxStreams];
+  int n_arenas = 0;
+  int evict_next = 0;  // slot handed to the next new stream once all 16 are taken
   // Pinned host staging for small device->host reads.
   void* pinned = nullptr;
   size_t pinned_cap = 0;
@@ -51,13 +60,18 @@ struct orch_ctx {
 
 namespace orchb {
 
+// The workspace of `stream` (created on first use; beyond kMaxCtxStreams
+// streams a slot is recycled after a device synchronisation; nullptr on error).
+Arena* arena_for(orch_ctx* ctx, cudaStream_t stream);
 // Reserve `bytes` in the arena, growing it (synchronously, outside timed
 // steady state) when needed. Returns nullptr on allocation failure.
-void* carve(orch_ctx* ctx, size_t bytes);
-void arena_reset(orch_ctx* ctx);
+void* carve(Arena* a, size_t bytes);
 // Make sure the arena can hold `bytes` without reallocation.
-int arena_reserve(orch_ctx* ctx, size_t bytes, cudaStream_t stream);
+int arena_reserve(Arena* a, size_t bytes, cudaStream_t stream);
 void* pinned(orch_ctx* ctx, size_t bytes);
+// Host-buffer (_host) entry points stage through a per-context device buffer
+// and its pinned host mirror of the same layout: one copy each way per call.
+int host_stage(orch_ctx* ctx, size_t bytes, char** h, char** d);
 
 // Runs f() once per device (function attributes such as the dynamic shared
 // memory limit are per-device state; a process may drive several devices).

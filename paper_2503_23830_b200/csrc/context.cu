@@ -19,12 +19,25 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
-void arena_reset(orch_ctx* ctx) {
-  ctx->arena.used = 0;
+Arena* arena_for(orch_ctx* ctx, cudaStream_t stream) {
+  for (int i = 0; i < ctx->n_arenas; ++i)
+    if (ctx->arenas[i].stream == stream) return &ctx->arenas[i].arena;
+  if (ctx->n_arenas == kMaxCtxStreams) {
+    // A 17th stream: wait until no kernel can still be using any workspace,
+    // then hand the next slot (round robin) with its buffer to the new stream.
+    if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+    const int i = ctx->evict_next;
+    ctx->evict_next = (i + 1) % kMaxCtxStreams;
+    ctx->arenas[i].stream = stream;
+    ctx->arenas[i].arena.used = 0;
+    return &ctx->arenas[i].arena;
+  }
+  ctx->arenas[ctx->n_arenas].stream = stream;
+  return &ctx->arenas[ctx->n_arenas++].arena;
 }
 
-int arena_reserve(orch_ctx* ctx, size_t bytes, cudaStream_t stream) {
-  Arena& a = ctx->arena;
+int arena_reserve(Arena* ap, size_t bytes, cudaStream_t stream) {
+  Arena& a = *ap;
   if (bytes <= a.cap) return ORCH_OK;
   size_t cap = a.cap ? a.cap : (size_t{1} << 20);
   while (cap < bytes) cap *= 2;
@@ -40,8 +53,8 @@ int arena_reserve(orch_ctx* ctx, size_t bytes, cudaStream_t stream) {
   return ORCH_OK;
 }
 
-void* carve(orch_ctx* ctx, size_t bytes) {
-  Arena& a = ctx->arena;
+void* carve(Arena* ap, size_t bytes) {
+  Arena& a = *ap;
   const size_t aligned = (bytes + 255) & ~size_t{255};
   if (a.used + aligned > a.cap) return nullptr;
   void* p = a.base + a.used;
@@ -62,6 +75,22 @@ void* pinned(orch_ctx* ctx, size_t bytes) {
     ctx->pinned_cap = cap;
   }
   return ctx->pinned;
+}
+
+int host_stage(orch_ctx* ctx, size_t bytes, char** h, char** d) {
+  if (bytes > ctx->stage_cap) {
+    if (ctx->stage) cudaFree(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_cap = 0;
+    size_t cap = 1 << 20;
+    while (cap < bytes) cap *= 2;
+    ORCH_CUDA_TRY(cudaMalloc(&ctx->stage, cap));
+    ctx->stage_cap = cap;
+  }
+  *h = static_cast<char*>(pinned(ctx, bytes));
+  if (!*h) return fail(ORCH_CUDA_ERROR, "pinned staging allocation failed");
+  *d = static_cast<char*>(ctx->stage);
+  return ORCH_OK;
 }
 
 }  // namespace orchb
@@ -96,7 +125,8 @@ int orch_ctx_create(int device, orch_ctx** out) {
 void orch_ctx_destroy(orch_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  if (ctx->arena.base) cudaFree(ctx->arena.base);
+  for (int i = 0; i < ctx->n_arenas; ++i)
+    if (ctx->arenas[i].arena.base) cudaFree(ctx->arenas[i].arena.base);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   delete ctx;

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -22,19 +23,29 @@ struct orch_comm {
   int size = 1;
   int device = 0;
   int32_t* barrier_buf = nullptr;  // 1 int on the device (ncclAllReduce barrier)
+  bool loopback = false;           // orch_comm_create_local: P ranks emulated in one process
 };
 
 // A row buffer every rank of the communicator can store into (CUDA IPC over
 // NVLink): the fused pack+put exchange writes rows straight into the
 // destination rank's output, one pass, no staging buffers.
+// Flag area after the rows, at flags_off (256 bytes):
+//   arrive[8] u64 : arrive[q] = the last barrier rank q has published here
+//   free[8]   u64 : free[q]   = the last step whose rows rank q has consumed
+//                                from ITS window (so this rank may put again)
+//   status    i32 : this rank's barrier / put-wait timeout (ORCH_CUDA_ERROR)
 struct orch_window {
   orch_comm* comm = nullptr;
   char* base = nullptr;
   size_t bytes = 0;
-  size_t flags_off = 0;           // [P] uint64 barrier slots after the rows (IPC-shared)
+  size_t flags_off = 0;           // the flag area (IPC-shared with the rows)
   uint64_t epoch = 0;             // orch_window_barrier calls so far (equal on every rank)
+  uint64_t released = 0;          // orch_window_release calls so far
+  uint64_t acq_epoch = 0;         // the step the last k_window_acquire waited for ...
+  void* acq_stream = nullptr;     // ... and its stream
   std::vector<char*> peers;       // host copy, peers[rank] == base
   char** peers_dev = nullptr;     // device copy [P]
+  bool loopback = false;          // peers are other windows of this process (no IPC)
 };
 
 struct orch_gather_window {
@@ -289,26 +300,80 @@ __global__ void __launch_bounds__(kLayoutSmallThreads, 1)
   }
 }
 
-// Window barrier: lane q publishes this rank's epoch in rank q's slot [me]
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// spin until *p >= want; false after ~4 s (a peer that never arrives)
+__device__ bool wait_at_least(const uint64_t* p, uint64_t want) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(p) < want) {
+    __nanosleep(64);
+    if (clock64() - t0 > 8000000000ll) return false;
+  }
+  return true;
+}
+
+constexpr size_t kFlagFree = 64;     // byte offset of free[] in the flag area
+constexpr size_t kFlagStatus = 128;  // byte offset of the status word
+constexpr size_t kFlagAcquired = 136;  // byte offset of the acquired step (u64)
+constexpr size_t kFlagBytes = 256;
+
+// Window barrier: lane q publishes this rank's epoch in rank q's arrive[me]
 // (release, system scope: the stream's earlier kernels -- the puts into the
 // peers' windows -- are complete, and the fence orders them before the flag),
-// then waits until rank q's epoch is in this rank's slot [q] (acquire).
+// then waits until rank q's epoch is in this rank's arrive[q] (acquire). A
+// peer that never arrives (~4 s) sets the window's status instead of hanging.
 __global__ void k_window_barrier(char* const* __restrict__ peers, size_t flags_off, int me, int P,
-                                 uint64_t epoch) {
+                                 uint64_t epoch, int32_t* status) {
   const int q = threadIdx.x;
   if (q < P) {
     __threadfence_system();
-    uint64_t* slot = reinterpret_cast<uint64_t*>(peers[q] + flags_off) + me;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
-    const uint64_t* mine = reinterpret_cast<const uint64_t*>(peers[me] + flags_off) + q;
-    uint64_t v;
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-      if (v >= epoch) break;
-      __nanosleep(64);
-    }
+    st_release_sys(reinterpret_cast<uint64_t*>(peers[q] + flags_off) + me, epoch);
+    if (!wait_at_least(reinterpret_cast<const uint64_t*>(peers[me] + flags_off) + q, epoch))
+      atomicExch(status, ORCH_CUDA_ERROR);
   }
   __syncwarp();
+}
+
+// Window acquire (before the first put of a step on a stream): one warp waits
+// until every rank q has released `need` steps (free[q] >= need), then records
+// `need` as acquired. The puts that follow on the stream store only when the
+// acquired step has reached their own `need` (a timed-out acquire, ~4 s, sets
+// the window status and leaves it behind, so they store nothing). The wait
+// occupies one warp, not the put kernel's CTAs, so a consumer kernel of any
+// size can still run and release.
+__global__ void k_window_acquire(const uint64_t* __restrict__ free_flags, int P, uint64_t need,
+                                 uint64_t* acquired, int32_t* status) {
+  const int q = threadIdx.x;
+  const bool ok = q >= P || wait_at_least(free_flags + q, need);
+  if (__all_sync(~0u, ok)) {
+    if (q == 0) *acquired = need;
+  } else if (q == 0) {
+    atomicExch(status, ORCH_CUDA_ERROR);
+  }
+}
+
+// Window release: the rows of step `released` have been consumed on this rank
+// (every earlier kernel of the stream has finished reading them); lane q
+// tells rank q by storing the count into rank q's free[me]. A put issued
+// after barrier e waits for free[q] >= e on every rank q before it stores.
+__global__ void k_window_release(char* const* __restrict__ peers, size_t flags_off, int me, int P,
+                                 uint64_t released) {
+  const int q = threadIdx.x;
+  if (q < P)
+    st_release_sys(reinterpret_cast<uint64_t*>(peers[q] + flags_off + kFlagFree) + me, released);
 }
 
 // ---------------------------------------------------------------- movement
@@ -390,6 +455,9 @@ struct MoveArgs {
   const int64_t* displ;  // send_displ row of me (pack) / recv_displ row of me (unpack)
   const int32_t* unit_first;
   char* const* peer_out;  // kPut: output buffer of every rank (IPC-mapped), [P]
+  size_t win_off;         // kPut: byte offset of this exchange's output in every window
+  const uint64_t* acquired;    // kPut: the window's acquired step (k_window_acquire)
+  uint64_t need_free;          // kPut: ... must have reached this, else nothing is stored
   unsigned long long* chunk_counter;  // TMA path: next unclaimed chunk (zeroed by k_unit_map)
   int scramble;                       // kPut: claim chunk batches in a scrambled order
   int32_t* status;
@@ -421,6 +489,10 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.status = ORCH_INVALID_ARGUMENT;
     return;
   }
+  if (MODE == kPut && *a.acquired < a.need_free) {  // k_window_acquire timed out
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.status, ORCH_CUDA_ERROR);
+    return;
+  }
   const int64_t beg = a.offs[a.lo_idx], end = a.offs[a.hi_idx];
   const int64_t units = (total + kUnitRows - 1) / kUnitRows;
   const int64_t vrow = static_cast<int64_t>(a.R / 16);
@@ -449,7 +521,7 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
                       : a.send + (a.displ[q] + a.pair_off[pos] + skip) * R;
       } else if (MODE == kPut) {  // straight into the destination rank's output (NVLink)
         s = a.in + lo * R;
-        t = a.peer_out[a.dest[pos] / a.c] + (a.rank_dst_off[pos] + skip) * R;
+        t = a.peer_out[a.dest[pos] / a.c] + a.win_off + (a.rank_dst_off[pos] + skip) * R;
       } else {
         const int r = a.origin[pos] / a.c;
         if (r == a.me) continue;  // moved by the pack kernel
@@ -525,6 +597,10 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
   }
   if (over) {
     if (blockIdx.x == 0 && lane == 0) *a.status = ORCH_INVALID_ARGUMENT;
+    return;
+  }
+  if (MODE == kPut && *a.acquired < a.need_free) {  // k_window_acquire timed out
+    if (blockIdx.x == 0 && lane == 0) atomicExch(a.status, ORCH_CUDA_ERROR);
     return;
   }
   const int64_t R = static_cast<int64_t>(a.R);
@@ -614,7 +690,7 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
                         : a.send + (a.displ[q] + a.pair_off[pos]) * R + skip;
         } else if (MODE == kPut) {
           s = a.in + lo;
-          d = a.peer_out[a.dest[pos] / a.c] + a.rank_dst_off[pos] * R + skip;
+          d = a.peer_out[a.dest[pos] / a.c] + a.win_off + a.rank_dst_off[pos] * R + skip;
         } else {
           const int r = a.origin[pos] / a.c;
           if (r != a.me) {
@@ -726,33 +802,8 @@ struct GatherArgs {
   uint64_t* stamps;  // [8][8] %globaltimer at the kernel's stages, slot epoch % 8 (diagnostics)
 };
 
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 __host__ __device__ inline size_t gather_flags_off(int64_t max_n) {
   return (static_cast<size_t>(max_n) * 12 + 15) & ~size_t{15};
-}
-
-// spin until *p >= want; false after ~4 s (a peer that never arrives)
-__device__ bool wait_at_least(const uint64_t* p, uint64_t want) {
-  const long long t0 = clock64();
-  while (ld_acquire_sys(p) < want) {
-    __nanosleep(64);
-    if (clock64() - t0 > 8000000000ll) return false;
-  }
-  return true;
 }
 
 __global__ void __launch_bounds__(1024) k_gather_put(GatherArgs a) {
@@ -1091,6 +1142,7 @@ int orch_unpack(orch_ctx* ctx, int32_t rank, int32_t nranks, int32_t d, int64_t 
 int orch_exchange(orch_ctx* ctx, orch_comm* comm, const orch_layout_out* L, size_t R,
                   const void* d_send, void* d_recv, int64_t recv_cap, void* stream) {
   if (!ctx || !comm || !L) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (!comm->comm) return fail(ORCH_INVALID_ARGUMENT, "loopback communicator has no NCCL");
   const int P = comm->size, me = comm->rank;
   auto st = static_cast<cudaStream_t>(stream);
   int64_t* h = static_cast<int64_t*>(pinned(ctx, sizeof(int64_t) * 3 * P * P));
@@ -1244,7 +1296,19 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t E, const int32_t* d_part_offset,
   return ORCH_OK;
 }
 
-// Host-buffer variants (staged through the context arena; synchronous).
+// Host-buffer variants (synchronous): inputs and outputs staged through the
+// context's pinned mirror of a device buffer, one copy each way per call.
+namespace {
+struct StageLayout {
+  size_t at = 0;
+  size_t take(size_t b) {
+    const size_t r = at;
+    at += (b + 255) & ~size_t{255};
+    return r;
+  }
+};
+}  // namespace
+
 int orch_batch_costs_host(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded,
                           int32_t d, int64_t n, const int64_t* h_len, const int32_t* h_bin_offset,
                           const int32_t* h_bin_member, double* h_cost, double* h_stats,
@@ -1255,31 +1319,39 @@ int orch_batch_costs_host(orch_ctx* ctx, const orch_cost_model* model, int32_t b
   if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
   ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
   auto st = static_cast<cudaStream_t>(stream);
-  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
-  Plan plan;
-  int64_t* len;
-  int32_t *off, *mem;
-  double *cost, *stats;
-  plan.add(&len, nn);
-  plan.add(&off, d + 1);
-  plan.add(&mem, nn);
-  plan.add(&cost, d);
-  plan.add(&stats, 3);
-  int rc = plan.commit(ctx, st);
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 0);
+  StageLayout sl;
+  const size_t o_len = sl.take(nn * 8), o_mem = sl.take(nn * 4);
+  const size_t o_off = sl.take(static_cast<size_t>(d + 1) * 4);
+  const size_t in_bytes = sl.at;
+  const size_t o_cost = sl.take(static_cast<size_t>(d) * 8), o_stats = sl.take(24);
+  char *hp, *dp;
+  int rc = host_stage(ctx, sl.at, &hp, &dp);
   if (rc) return rc;
-  if (n > 0) {
-    ORCH_CUDA_TRY(cudaMemcpyAsync(len, h_len, 8 * n, cudaMemcpyHostToDevice, st));
-    ORCH_CUDA_TRY(cudaMemcpyAsync(mem, h_bin_member, 4 * n, cudaMemcpyHostToDevice, st));
+  if (nn) {
+    memcpy(hp + o_len, h_len, nn * 8);
+    memcpy(hp + o_mem, h_bin_member, nn * 4);
   }
-  ORCH_CUDA_TRY(cudaMemcpyAsync(off, h_bin_offset, 4 * (d + 1), cudaMemcpyHostToDevice, st));
+  memcpy(hp + o_off, h_bin_offset, static_cast<size_t>(d + 1) * 4);
+  ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
+  // The costs (d doubles) and stats go straight to the pinned mirror (mapped
+  // into the device's address space under UVA): no device-to-host copy call,
+  // which is a third of a one-batch cost() round trip.
+  double* cost = reinterpret_cast<double*>(hp + o_cost);
   launch(ctx, [&] {
     k_bin_cost<<<blocks_for(static_cast<int64_t>(d) * 32, kThreads), kThreads, 0, st>>>(
-        *model, d, off, mem, len, nullptr, nullptr, nullptr, cost, nullptr);
+        *model, d, reinterpret_cast<const int32_t*>(dp + o_off),
+        reinterpret_cast<const int32_t*>(dp + o_mem), reinterpret_cast<const int64_t*>(dp + o_len),
+        nullptr, nullptr, nullptr, cost, nullptr);
   });
-  if (h_stats) launch(ctx, [&] { k_stats_only<<<1, 1024, 0, st>>>(d, cost, stats); });
-  ORCH_CUDA_TRY(cudaMemcpyAsync(h_cost, cost, 8 * d, cudaMemcpyDeviceToHost, st));
-  if (h_stats) ORCH_CUDA_TRY(cudaMemcpyAsync(h_stats, stats, 24, cudaMemcpyDeviceToHost, st));
+  if (h_stats)
+    launch(ctx, [&] {
+      k_stats_only<<<1, 1024, 0, st>>>(d, cost, reinterpret_cast<double*>(hp + o_stats));
+    });
+  ORCH_CUDA_TRY(cudaGetLastError());
   ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(h_cost, hp + o_cost, static_cast<size_t>(d) * 8);
+  if (h_stats) memcpy(h_stats, hp + o_stats, 24);
   return ORCH_OK;
 }
 
@@ -1290,25 +1362,29 @@ int orch_volume_matrix_host(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* 
   if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
   ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
   auto st = static_cast<cudaStream_t>(stream);
-  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
-  Plan plan;
-  int64_t *len, *V;
-  int32_t *org, *dst;
-  plan.add(&len, nn);
-  plan.add(&org, nn);
-  plan.add(&dst, nn);
-  plan.add(&V, static_cast<size_t>(d) * d);
-  int rc = plan.commit(ctx, st);
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 0);
+  StageLayout sl;
+  const size_t o_len = sl.take(nn * 8), o_org = sl.take(nn * 4), o_dst = sl.take(nn * 4);
+  const size_t in_bytes = sl.at;
+  const size_t o_V = sl.take(sizeof(int64_t) * d * d);
+  char *hp, *dp;
+  int rc = host_stage(ctx, sl.at, &hp, &dp);
   if (rc) return rc;
-  if (n > 0) {
-    ORCH_CUDA_TRY(cudaMemcpyAsync(len, h_len, 8 * n, cudaMemcpyHostToDevice, st));
-    ORCH_CUDA_TRY(cudaMemcpyAsync(org, h_origin, 4 * n, cudaMemcpyHostToDevice, st));
-    ORCH_CUDA_TRY(cudaMemcpyAsync(dst, h_dest_inst, 4 * n, cudaMemcpyHostToDevice, st));
+  if (nn) {
+    memcpy(hp + o_len, h_len, nn * 8);
+    memcpy(hp + o_org, h_origin, nn * 4);
+    memcpy(hp + o_dst, h_dest_inst, nn * 4);
+    ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
   }
-  rc = orch_volume_matrix(ctx, d, n, len, org, dst, V, stream);
+  rc = orch_volume_matrix(ctx, d, n, reinterpret_cast<const int64_t*>(dp + o_len),
+                          reinterpret_cast<const int32_t*>(dp + o_org),
+                          reinterpret_cast<const int32_t*>(dp + o_dst),
+                          reinterpret_cast<int64_t*>(dp + o_V), stream);
   if (rc) return rc;
-  ORCH_CUDA_TRY(cudaMemcpyAsync(h_V, V, sizeof(int64_t) * d * d, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(hp + o_V, dp + o_V, sizeof(int64_t) * d * d,
+                                cudaMemcpyDeviceToHost, st));
   ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(h_V, hp + o_V, sizeof(int64_t) * d * d);
   return ORCH_OK;
 }
 
@@ -1361,6 +1437,7 @@ int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_
                          const int32_t* d_local_origin, int64_t n, int64_t* d_len,
                          int32_t* d_origin, void* stream) {
   if (!ctx || !comm) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (!comm->comm) return fail(ORCH_INVALID_ARGUMENT, "loopback communicator has no NCCL");
   if (local_n > max_local || max_local < 0) return fail(ORCH_INVALID_ARGUMENT, "local_n > max_local");
   auto st = static_cast<cudaStream_t>(stream);
   const int P = comm->size;
@@ -1393,51 +1470,170 @@ int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_
 // ------------------------------------------------------------ windows / put
 int orch_barrier(orch_comm* comm, void* stream) {
   if (!comm) return fail(ORCH_INVALID_ARGUMENT, "null communicator");
+  if (!comm->comm) return fail(ORCH_INVALID_ARGUMENT, "loopback communicator has no NCCL");
   ORCH_NCCL_TRY(ncclAllReduce(comm->barrier_buf, comm->barrier_buf, 1, ncclInt32, ncclSum,
                               comm->comm, static_cast<cudaStream_t>(stream)));
   return ORCH_OK;
 }
 
-int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out) {
-  if (!ctx || !comm || !out || bytes == 0) return fail(ORCH_INVALID_ARGUMENT, "bad window arguments");
-  const int P = comm->size;
+int orch_comm_create_local(int32_t nranks, int32_t rank, orch_comm** out) {
+  if (!out) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks)
+    return fail(ORCH_INVALID_ARGUMENT, "bad rank (loopback communicators hold 1..8 ranks)");
+  auto* c = new orch_comm();
+  ORCH_CUDA_TRY(cudaGetDevice(&c->device));
+  c->rank = rank;
+  c->size = nranks;
+  c->loopback = true;
+  *out = c;
+  return ORCH_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Allocates the rows + flag area of one window (flags zeroed).
+int window_alloc(orch_comm* comm, size_t bytes, orch_window** out) {
   auto* w = new orch_window();
   w->comm = comm;
   w->bytes = bytes;
-  w->peers.assign(P, nullptr);
+  w->peers.assign(comm->size, nullptr);
   w->flags_off = (bytes + 255) & ~size_t{255};
-  cudaError_t e = cudaMalloc(&w->base, w->flags_off + 256);
+  cudaError_t e = cudaMalloc(&w->base, w->flags_off + kFlagBytes);
   if (e != cudaSuccess) {
     delete w;
     return fail(ORCH_CUDA_ERROR, std::string("window allocation: ") + cudaGetErrorString(e));
   }
-  ORCH_CUDA_TRY(cudaMemset(w->base + w->flags_off, 0, 256));
-  cudaIpcMemHandle_t mine;
-  ORCH_CUDA_TRY(cudaIpcGetMemHandle(&mine, w->base));
+  e = cudaMemset(w->base + w->flags_off, 0, kFlagBytes);
+  if (e != cudaSuccess) {
+    cudaFree(w->base);
+    delete w;
+    return fail(ORCH_CUDA_ERROR, std::string("window flags: ") + cudaGetErrorString(e));
+  }
+  *out = w;
+  return ORCH_OK;
+}
+
+int window_publish_peers(orch_window* w) {
+  const int P = w->comm->size;
+  ORCH_CUDA_TRY(cudaMalloc(&w->peers_dev, sizeof(char*) * P));
+  ORCH_CUDA_TRY(cudaMemcpy(w->peers_dev, w->peers.data(), sizeof(char*) * P,
+                           cudaMemcpyHostToDevice));
+  return ORCH_OK;
+}
+
+void window_free(orch_window* w) {
+  if (!w->loopback)
+    for (int q = 0; q < static_cast<int>(w->peers.size()); ++q)
+      if (q != w->comm->rank && w->peers[q]) cudaIpcCloseMemHandle(w->peers[q]);
+  if (w->peers_dev) cudaFree(w->peers_dev);
+  if (w->base) cudaFree(w->base);
+  delete w;
+}
+
+// What every rank contributes to the window set-up all-gather.
+struct WindowCard {
+  cudaIpcMemHandle_t handle;
+  uint64_t bytes;
+  uint64_t pad[7];
+};
+
+}  // namespace
+
+extern "C" {
+
+int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out) {
+  if (!ctx || !comm || !out || bytes == 0) return fail(ORCH_INVALID_ARGUMENT, "bad window arguments");
+  if (comm->loopback || !comm->comm)
+    return fail(ORCH_INVALID_ARGUMENT, "loopback communicator: use orch_window_create_local");
+  const int P = comm->size;
+  orch_window* w = nullptr;
+  int rc = window_alloc(comm, bytes, &w);
+  if (rc) return rc;
+  WindowCard mine{};
+  mine.bytes = bytes;
+  cudaError_t e = cudaIpcGetMemHandle(&mine.handle, w->base);
+  // every rank's handle and size (the puts and barriers address peers with
+  // this rank's flags offset and capacity, so all sizes must agree)
   char* dev = nullptr;
-  ORCH_CUDA_TRY(cudaMalloc(&dev, sizeof(cudaIpcMemHandle_t) * (P + 1)));
-  ORCH_CUDA_TRY(cudaMemcpy(dev, &mine, sizeof mine, cudaMemcpyHostToDevice));
-  ORCH_NCCL_TRY(ncclAllGather(dev, dev + sizeof(cudaIpcMemHandle_t), sizeof(cudaIpcMemHandle_t),
-                              ncclChar, comm->comm, 0));
-  std::vector<cudaIpcMemHandle_t> all(P);
-  ORCH_CUDA_TRY(cudaMemcpy(all.data(), dev + sizeof(cudaIpcMemHandle_t),
-                           sizeof(cudaIpcMemHandle_t) * P, cudaMemcpyDeviceToHost));
+  if (e == cudaSuccess) e = cudaMalloc(&dev, sizeof(WindowCard) * (P + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(dev, &mine, sizeof mine, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (dev) cudaFree(dev);
+    window_free(w);
+    return fail(ORCH_CUDA_ERROR, std::string("window set-up: ") + cudaGetErrorString(e));
+  }
+  ncclResult_t nr = ncclAllGather(dev, dev + sizeof(WindowCard), sizeof(WindowCard), ncclChar,
+                                  comm->comm, 0);
+  std::vector<WindowCard> all(P);
+  if (nr == ncclSuccess)
+    e = cudaMemcpy(all.data(), dev + sizeof(WindowCard), sizeof(WindowCard) * P,
+                   cudaMemcpyDeviceToHost);
   cudaFree(dev);
+  if (nr != ncclSuccess || e != cudaSuccess) {
+    window_free(w);
+    return fail(nr != ncclSuccess ? ORCH_NCCL_ERROR : ORCH_CUDA_ERROR,
+                std::string("window handle exchange: ") +
+                    (nr != ncclSuccess ? ncclGetErrorString(nr) : cudaGetErrorString(e)));
+  }
+  for (int q = 0; q < P; ++q)
+    if (all[q].bytes != bytes) {  // every rank sees the same cards, so every rank fails here
+      window_free(w);
+      return fail(ORCH_INVALID_ARGUMENT,
+                  "orch_window_create: ranks passed different window sizes (rank " +
+                      std::to_string(q) + ": " + std::to_string(all[q].bytes) + " bytes, rank " +
+                      std::to_string(comm->rank) + ": " + std::to_string(bytes) + ")");
+    }
   for (int q = 0; q < P; ++q) {
     if (q == comm->rank) {
       w->peers[q] = w->base;
       continue;
     }
     void* p = nullptr;
-    e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess)
+    e = cudaIpcOpenMemHandle(&p, all[q].handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      window_free(w);
       return fail(ORCH_CUDA_ERROR, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
     w->peers[q] = static_cast<char*>(p);
   }
-  ORCH_CUDA_TRY(cudaMalloc(&w->peers_dev, sizeof(char*) * P));
-  ORCH_CUDA_TRY(cudaMemcpy(w->peers_dev, w->peers.data(), sizeof(char*) * P,
-                           cudaMemcpyHostToDevice));
+  rc = window_publish_peers(w);
+  if (rc) {
+    window_free(w);
+    return rc;
+  }
   *out = w;
+  return ORCH_OK;
+}
+
+int orch_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t P, size_t bytes,
+                             orch_window** out) {
+  if (!ctx || !comms || !out || bytes == 0 || P < 1 || P > 8)
+    return fail(ORCH_INVALID_ARGUMENT, "bad window arguments");
+  for (int r = 0; r < P; ++r)
+    if (!comms[r] || !comms[r]->loopback || comms[r]->size != P || comms[r]->rank != r)
+      return fail(ORCH_INVALID_ARGUMENT,
+                  "orch_window_create_local needs loopback communicators of ranks 0..P-1");
+  std::vector<orch_window*> ws(P, nullptr);
+  for (int r = 0; r < P; ++r) {
+    int rc = window_alloc(comms[r], bytes, &ws[r]);
+    if (rc) {
+      for (int q = 0; q < r; ++q) window_free(ws[q]);
+      return rc;
+    }
+    ws[r]->loopback = true;
+  }
+  for (int r = 0; r < P; ++r) {
+    for (int q = 0; q < P; ++q) ws[r]->peers[q] = ws[q]->base;
+    int rc = window_publish_peers(ws[r]);
+    if (rc) {
+      for (int q = 0; q < P; ++q) window_free(ws[q]);
+      return rc;
+    }
+  }
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  for (int r = 0; r < P; ++r) out[r] = ws[r];
   return ORCH_OK;
 }
 
@@ -1447,9 +1643,31 @@ int orch_window_barrier(orch_ctx* ctx, orch_window* w, void* stream) {
   ++w->epoch;
   launch(ctx, [&] {
     k_window_barrier<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
-        w->peers_dev, w->flags_off, w->comm->rank, P, w->epoch);
+        w->peers_dev, w->flags_off, w->comm->rank, P, w->epoch,
+        reinterpret_cast<int32_t*>(w->base + w->flags_off + kFlagStatus));
   });
   ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+int orch_window_release(orch_ctx* ctx, orch_window* w, void* stream) {
+  if (!ctx || !w) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (w->released >= w->epoch)
+    return fail(ORCH_INVALID_ARGUMENT,
+                "orch_window_release: no barrier-closed step left to release");
+  ++w->released;
+  launch(ctx, [&] {
+    k_window_release<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        w->peers_dev, w->flags_off, w->comm->rank, w->comm->size, w->released);
+  });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+int orch_window_status(const orch_window* w, int32_t* h_status) {
+  if (!w || !h_status) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  ORCH_CUDA_TRY(cudaMemcpy(h_status, w->base + w->flags_off + kFlagStatus, sizeof(int32_t),
+                           cudaMemcpyDeviceToHost));
   return ORCH_OK;
 }
 
@@ -1458,26 +1676,26 @@ size_t orch_window_bytes(const orch_window* w) { return w ? w->bytes : 0; }
 
 int orch_window_destroy(orch_window* w) {
   if (!w) return ORCH_OK;
+  int rc = ORCH_OK;
   // every rank must be done writing into / reading from the windows
-  int rc = orch_barrier(w->comm, nullptr);
+  if (!w->loopback) rc = orch_barrier(w->comm, nullptr);
   cudaDeviceSynchronize();
-  for (int q = 0; q < static_cast<int>(w->peers.size()); ++q)
-    if (q != w->comm->rank && w->peers[q]) cudaIpcCloseMemHandle(w->peers[q]);
-  cudaFree(w->peers_dev);
-  cudaFree(w->base);
-  delete w;
+  window_free(w);
   return rc;
 }
 
-int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
-                      const int32_t* d_origin, const orch_balance_out* bal,
-                      const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap,
-                      orch_window* out_win, void* stream) {
+int orch_put_at(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+                const int32_t* d_origin, const orch_balance_out* bal, const orch_layout_out* L,
+                size_t R, const void* d_in, int64_t in_cap, orch_window* out_win,
+                size_t win_offset, void* stream) {
   if (!comm || !out_win) return fail(ORCH_INVALID_ARGUMENT, "put needs a communicator and a window");
+  if (out_win->comm != comm) return fail(ORCH_INVALID_ARGUMENT, "window belongs to another communicator");
   const int P = comm->size, me = comm->rank;
   int rc = check_move_args(ctx, P, me, d, bal, L, R);
   if (rc) return rc;
   if (!aligned16(d_in)) return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
+  if (win_offset % 16 != 0 || win_offset > out_win->bytes)
+    return fail(ORCH_INVALID_ARGUMENT, "window offset must be a multiple of 16 inside the window");
   if (n > 0) {
     MoveArgs a = make_args(P, me, d, d_len, d_origin, bal, L, R);
     a.offs = bal->src_offset;
@@ -1485,10 +1703,27 @@ int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t
     a.iter_rows = L->in_rows;
     a.iter_cap = in_cap;
     a.in_cap = in_cap;
-    a.out_cap = static_cast<int64_t>(out_win->bytes / R);
+    a.out_cap = static_cast<int64_t>((out_win->bytes - win_offset) / R);
     a.in = static_cast<const char*>(d_in);
-    a.out = out_win->base;
+    a.out = out_win->base + win_offset;
     a.peer_out = out_win->peers_dev;
+    a.win_off = win_offset;
+    char* flags = out_win->base + out_win->flags_off;
+    a.acquired = reinterpret_cast<const uint64_t*>(flags + kFlagAcquired);
+    a.need_free = out_win->epoch;  // the steps closed so far must all be consumed
+    auto st = static_cast<cudaStream_t>(stream);
+    if (out_win->epoch > 0 &&
+        (out_win->acq_epoch != out_win->epoch || out_win->acq_stream != stream)) {
+      launch(ctx, [&] {
+        k_window_acquire<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(flags + kFlagFree), P,
+                                           out_win->epoch,
+                                           reinterpret_cast<uint64_t*>(flags + kFlagAcquired),
+                                           reinterpret_cast<int32_t*>(flags + kFlagStatus));
+      });
+      ORCH_CUDA_TRY(cudaGetLastError());
+      out_win->acq_epoch = out_win->epoch;
+      out_win->acq_stream = stream;
+    }
     static const int scramble = [] {
       const char* e = getenv("ORCH_PUT_SCRAMBLE");
       return e ? atoi(e) : 1;
@@ -1500,6 +1735,13 @@ int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t
   return ORCH_OK;
 }
 
+int orch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
+             const int32_t* d_origin, const orch_balance_out* bal, const orch_layout_out* L,
+             size_t R, const void* d_in, int64_t in_cap, orch_window* out_win, void* stream) {
+  return orch_put_at(ctx, comm, d, n, d_len, d_origin, bal, L, R, d_in, in_cap, out_win, 0,
+                     stream);
+}
+
 int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
                       const int32_t* d_origin, const orch_balance_out* bal,
                       const orch_layout_out* L, size_t R, const void* d_in, int64_t in_cap,
@@ -1507,29 +1749,60 @@ int orch_dispatch_put(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, cons
   int rc = orch_put(ctx, comm, d, n, d_len, d_origin, bal, L, R, d_in, in_cap, out_win, stream);
   if (rc) return rc;
   // rows from every peer have landed once every rank passed its put kernel
-  return orch_barrier(comm, stream);
+  return orch_window_barrier(ctx, out_win, stream);
 }
+
+}  // extern "C"
+
+namespace {
+
+int gather_window_wrap(orch_window* w, int64_t max_n, orch_gather_window** out) {
+  auto* g = new orch_gather_window();
+  g->max_n = max_n;
+  g->w = w;
+  ORCH_CUDA_TRY(cudaMalloc(&g->stamps, 64 * sizeof(uint64_t)));
+  ORCH_CUDA_TRY(cudaMemset(g->stamps, 0, 64 * sizeof(uint64_t)));
+  // flags start at 0 on every rank before any peer can store into them
+  ORCH_CUDA_TRY(cudaMemset(w->base, 0, w->bytes));
+  *out = g;
+  return ORCH_OK;
+}
+
+size_t gather_window_bytes(int64_t max_n, int P) {
+  return gather_flags_off(max_n) + 16 * static_cast<size_t>(P);
+}
+
+}  // namespace
+
+extern "C" {
 
 int orch_gather_window_create(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
                               orch_gather_window** out) {
   if (!ctx || !comm || !out || max_n < 1) return fail(ORCH_INVALID_ARGUMENT, "bad gather window arguments");
-  const size_t bytes = gather_flags_off(max_n) + 16 * static_cast<size_t>(comm->size);
-  auto* g = new orch_gather_window();
-  g->max_n = max_n;
-  int rc = orch_window_create(ctx, comm, bytes, &g->w);
-  if (rc) {
-    delete g;
-    return rc;
-  }
-  ORCH_CUDA_TRY(cudaMalloc(&g->stamps, 64 * sizeof(uint64_t)));
-  ORCH_CUDA_TRY(cudaMemset(g->stamps, 0, 64 * sizeof(uint64_t)));
-  // flags start at 0 on every rank before any peer can store into them
-  ORCH_CUDA_TRY(cudaMemset(g->w->base, 0, bytes));
+  orch_window* w = nullptr;
+  int rc = orch_window_create(ctx, comm, gather_window_bytes(max_n, comm->size), &w);
+  if (rc) return rc;
+  rc = gather_window_wrap(w, max_n, out);
+  if (rc) return rc;
   ORCH_CUDA_TRY(cudaDeviceSynchronize());
   rc = orch_barrier(comm, nullptr);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaDeviceSynchronize());
-  *out = g;
+  return ORCH_OK;
+}
+
+int orch_gather_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t P,
+                                    int64_t max_n, orch_gather_window** out) {
+  if (!ctx || !comms || !out || max_n < 1 || P < 1 || P > 8)
+    return fail(ORCH_INVALID_ARGUMENT, "bad gather window arguments");
+  std::vector<orch_window*> ws(P, nullptr);
+  int rc = orch_window_create_local(ctx, comms, P, gather_window_bytes(max_n, P), ws.data());
+  if (rc) return rc;
+  for (int r = 0; r < P; ++r) {
+    rc = gather_window_wrap(ws[r], max_n, &out[r]);
+    if (rc) return rc;
+  }
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
   return ORCH_OK;
 }
 

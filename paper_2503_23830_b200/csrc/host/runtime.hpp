@@ -17,6 +17,10 @@ orch_ctx* context();
 // <stdexcept>) with the library's message; no-op for ORCH_OK.
 void check(int code);
 
+// cost(model, b) of many batches in one device call (orch_batch_costs_host);
+// throws like cost() on the first batch (in order) whose padding mode differs.
+std::vector<double> batch_costs(const CostModel& model, const std::vector<const MiniBatch*>& batches);
+
 inline orch_cost_model to_abi(const CostModel& m) {
   return orch_cost_model{m.alpha, m.beta, m.padding_mode == PaddingMode::Padded ? 1 : 0,
                          static_cast<int32_t>(m.variant)};

@@ -94,18 +94,14 @@ HostingSolution solve_hosting(const VolumeMatrix& volumes, const ClusterTopology
   for (int i = 0; i < d; ++i)
     for (int j = 0; j < d; ++j) flat[static_cast<std::size_t>(i) * d + j] = volumes.at(i, j);
   std::vector<int32_t> h(static_cast<std::size_t>(d));
-  std::int64_t mx = 0, base = 0;
+  std::int64_t info[4] = {0, 0, 0, 0};
   b200::check(orch_solve_hosting_host(b200::context(), d, topo.instances_per_node, flat.data(),
-                                      h.data(), &mx, &base, nullptr));
+                                      h.data(), info, nullptr));
   HostingSolution sol;
   sol.hosting.assign(h.begin(), h.end());
   sol.per_node_egress = inter_node_egress(volumes, topo, sol.hosting);
-  sol.max_egress = mx;
-  long double space = 1;  // balanced hostings scored
-  for (int i = 1; i <= d; ++i) space *= i;
-  for (int k = 0; k < topo.node_count(); ++k)
-    for (int i = 1; i <= topo.instances_per_node; ++i) space /= i;
-  sol.nodes_visited = static_cast<std::int64_t>(space);
+  sol.max_egress = info[0];
+  sol.nodes_visited = info[3];  // the device search's own visit count (int64 counter)
   return sol;
 }
 
@@ -133,6 +129,21 @@ NodewiseResult nodewise_rearrange(const std::vector<MiniBatch>& batches, const R
   r.batch_to_instance = std::move(b2i);
   r.nodes_visited = sol.nodes_visited;
   return r;
+}
+
+bool permutation_invariance_check(const std::vector<MiniBatch>& before,
+                                  const std::vector<MiniBatch>& after, const CostModel& model) {
+  // topology.cpp:305-316
+  if (before.size() != after.size()) return false;
+  std::vector<const MiniBatch*> all;
+  all.reserve(before.size() + after.size());
+  for (const MiniBatch& b : before) all.push_back(&b);
+  for (const MiniBatch& b : after) all.push_back(&b);
+  std::vector<double> c = b200::batch_costs(model, all);
+  const auto mid = c.begin() + static_cast<std::ptrdiff_t>(before.size());
+  std::sort(c.begin(), mid);
+  std::sort(mid, c.end());
+  return std::equal(c.begin(), mid, mid, c.end());
 }
 
 }  // namespace orchsim

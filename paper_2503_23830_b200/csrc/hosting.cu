@@ -24,6 +24,7 @@
 // (total - gained - optimistic gain) -- read in O(1): the unassigned batches
 // at depth k are exactly order[k..d), so the optimistic gain of node n with r
 // slots left is a table og[k][n][r] built once.
+#include <cstring>
 #include <climits>
 #include <cstdlib>
 #include <string>
@@ -1125,8 +1126,7 @@ using namespace orchb;
 extern "C" {
 
 int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
-                            int32_t* h_hosting, int64_t* h_max_egress, int64_t* h_baseline_max,
-                            void* stream) {
+                            int32_t* h_hosting, int64_t* h_info, void* stream) {
   if (!ctx) return fail(ORCH_INVALID_ARGUMENT, "null context");
   int rc = check_hosting_args(d, c);
   if (rc) return rc;
@@ -1153,8 +1153,10 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
   int64_t hinfo[4];
   ORCH_CUDA_TRY(cudaMemcpyAsync(hinfo, info, sizeof hinfo, cudaMemcpyDeviceToHost, st));
   ORCH_CUDA_TRY(cudaStreamSynchronize(st));
-  if (h_max_egress) *h_max_egress = hinfo[0];
-  if (h_baseline_max) *h_baseline_max = hinfo[1];
+  if (h_info) memcpy(h_info, hinfo, sizeof hinfo);
+  if (hinfo[2] == -1)  // the exact answer is unknown: never return the incumbent silently
+    return fail(ORCH_UNSUPPORTED,
+                "solve_hosting: the exact search exceeded its budget of 2^31 visited nodes");
   return ORCH_OK;
 }
 

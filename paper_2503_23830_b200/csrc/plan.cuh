@@ -26,11 +26,13 @@ class Plan {
     }
   }
   int commit(orch_ctx* ctx, cudaStream_t stream) {
-    int rc = arena_reserve(ctx, total_ + 256, stream);
+    Arena* a = arena_for(ctx, stream);
+    if (!a) return fail(ORCH_CUDA_ERROR, "workspace hand-over to a new stream failed (device synchronisation)");
+    int rc = arena_reserve(a, total_ + 256, stream);
     if (rc) return rc;
-    arena_reset(ctx);
+    a->used = 0;  // calls on one stream run in order: the previous call's scratch is free
     for (auto& e : entries_) {
-      *e.slot = carve(ctx, e.bytes ? e.bytes : 1);
+      *e.slot = carve(a, e.bytes ? e.bytes : 1);
       if (!*e.slot) return fail(ORCH_CUDA_ERROR, "workspace arena exhausted");
     }
     return ORCH_OK;

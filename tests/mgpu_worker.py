@@ -99,6 +99,7 @@ def main():
                 ok = ok and int(lay.status.item()) == 0
                 k = len(outs[rank])
                 ok = ok and torch.equal(wv[:k].cpu(), torch.from_numpy(outs[rank]))
+                ctx.window_release(win)
                 # put + the window's peer-memory barrier, twice (epochs 1, 2): the
                 # rows are complete as soon as this rank's barrier returns on its stream
                 for _ in range(2):
@@ -108,7 +109,9 @@ def main():
                     ctx.put(d, gl, go, bal, lay, R, rin, win, comm)
                     ctx.window_barrier(win)
                     ok = ok and torch.equal(wv[:k].cpu(), torch.from_numpy(outs[rank]))
+                    ctx.window_release(win)
                     torch.cuda.synchronize()
+                    ok = ok and int(lay.status.item()) == 0 and win.status() == 0
                     dist.barrier()
                 win.close()
                 cases += 1
