@@ -204,7 +204,8 @@ def run_reference(args):
 def run_b200(args):
     import torch
     import torch.distributed as dist
-    from paper_2503_23830_b200.capi import Balance, Comm, Context, GatherWindow, Layout, Window
+    from paper_2503_23830_b200.capi import (Balance, Comm, Context, GatherWindow, Layout, Window,
+                                            XPlan)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -265,7 +266,9 @@ def run_b200(args):
         s["lorg"] = s["h_org"].to(dev)
         s["buf"] = [dict(glen=torch.from_numpy(L).to(dev), gorg=torch.from_numpy(O).to(dev),
                          bal=Balance.alloc(D_INST, n, dev), lay=Layout.alloc(P, n, dev),
-                         meta_done=torch.cuda.Event(), data_done=torch.cuda.Event())
+                         meta_done=torch.cuda.Event(), data_done=torch.cuda.Event(),
+                         xplan=XPlan(ctx_data, n, P)
+                         if P > 1 and args.exchange in ("nccl", "nccl-direct") else None)
                     for _ in range(2)]
         s["ctx"], s["ms"], s["gwin"] = meta_ctx[i_ph], meta_streams[i_ph], gwins[i_ph]
         st.append(s)
@@ -312,6 +315,9 @@ def run_b200(args):
             ctx_meta.nodewise(D_INST, c, B["glen"], B["gorg"], B["bal"], stream=stream)
         mark(stream)
         ctx_meta.layout(D_INST, P, B["glen"], B["gorg"], B["bal"], out=B["lay"], stream=stream)
+        if B["xplan"] is not None:  # the per-item runs for the host's NCCL calls
+            ctx_meta.xplan_fetch(B["xplan"], D_INST, B["glen"], B["gorg"], B["bal"], B["lay"],
+                                 stream=stream)
         mark(stream)
 
     # sizing pass (not timed): buffers from this batch's layout
@@ -349,7 +355,7 @@ def run_b200(args):
     rin = torch.randint(0, 255, (max(max(s["in_rows"] for s in st), 1) * R,), dtype=torch.uint8,
                         device=dev)
     send = recv = None
-    if P > 1:
+    if P > 1 and args.exchange in ("nccl", "nccl-sync"):
         send = torch.empty(max(max(s["send_rows"] for s in st), 1) * R, dtype=torch.uint8,
                            device=dev)
         recv = torch.empty(max(max(s["recv_rows"] for s in st), 1) * R, dtype=torch.uint8,
@@ -357,6 +363,10 @@ def run_b200(args):
     for s in st:
         s["rin"] = rin[:max(s["in_rows"], 1) * R]
         s["send"], s["recv"] = send, recv
+    reg = []
+    if P > 1 and args.exchange.startswith("nccl") and args.nccl_register:
+        reg = [comm_data.register(rin)] + [comm_data.register(s["rout"]) for s in st]
+        reg += [comm_data.register(t) for t in (send, recv) if t is not None]
 
     disp_events = []
     counter = [0]
@@ -408,6 +418,9 @@ def run_b200(args):
                         ctx_data.window_release(win, stream=data_stream)
                     elif args.barrier == "nccl":
                         ctx_data.barrier(comm_data, stream=data_stream)
+            elif B["xplan"] is not None:  # NCCL with host counts from the metadata stream
+                ctx_data.dispatch_nccl(B["xplan"], R, s["rin"], s["rout"], comm_data,
+                                       send=s["send"], recv=s["recv"], stream=data_stream)
             else:
                 ctx_data.dispatch(D_INST, B["glen"], B["gorg"], B["bal"], B["lay"], R, s["rin"],
                                   s["rout"], s["send"], s["recv"], comm_data, stream=data_stream)
@@ -489,7 +502,7 @@ def run_b200(args):
     disp_ms = sum(e0.elapsed_time(e1) for _, e0, e1 in disp_events)
     moved = sum(s["moved_rows"] for s in st) * R * args.steps  # rows written once, read once
     hbm_bytes = 2 * moved
-    if P > 1 and args.exchange == "nccl":  # staging: pack to send, recv to out
+    if P > 1 and args.exchange in ("nccl", "nccl-sync"):  # staging: pack to send, recv to out
         hbm_bytes += 2 * sum(s["send_rows"] + s["recv_rows"] for s in st) * R * args.steps
     peak, peak_kind = peaks()
     achieved = hbm_bytes / (disp_ms / 1e3) / 1e9 if disp_ms > 0 else None
@@ -600,8 +613,15 @@ def run_b200(args):
         hbm_view = line["roofline"]
         line["roofline"] = {"bound": "nvlink", "achieved": busbw, "peak": 770.0, "unit": "GB/s",
                             "frac": busbw / 770.0, "traffic": None,
-                            "kernel": ("k_move_tma<kPut> (orch_put)" if args.exchange == "put"
-                                       else "ncclSend/ncclRecv (orch_dispatch)"),
+                            "kernel": {"put": "k_move_tma<kPut> (orch_put)",
+                                       "nccl": "pack + ncclSend/ncclRecv per peer + unpack, host "
+                                               "counts from the metadata stream "
+                                               "(orch_dispatch_nccl)",
+                                       "nccl-direct": "ncclSend/ncclRecv per item run "
+                                                      "(orch_dispatch_nccl)",
+                                       "nccl-sync": "pack + ncclSend/ncclRecv + unpack, counts "
+                                                    "read on the data stream (orch_dispatch)"
+                                       }[args.exchange],
                             "peak_kind": "measured peer copy (B200_PROFILING.md)",
                             "share_of_step": hbm_view["share_of_step"],
                             "hbm_view": {k: hbm_view[k] for k in ("achieved", "peak", "frac")}}
@@ -626,6 +646,8 @@ def run_b200(args):
     for gwin in gwins:
         if gwin is not None:
             gwin.close()
+    for h in reg:
+        comm_data.deregister(h)
     if comm_meta is not None:
         comm_meta.close()
         comm_data.close()
@@ -649,8 +671,13 @@ def main():
     ap.add_argument("--barrier", default="window", choices=["window", "nccl", "none"],
                     help="N>1 put: the per-step barrier through the window's peer memory "
                          "(default), a 1-int ncclAllReduce, or none (diagnostics only)")
-    ap.add_argument("--exchange", default="put", choices=["put", "nccl"],
-                    help="N>1: fused pack+put over NVLink (default) or NCCL send/recv")
+    ap.add_argument("--exchange", default="put",
+                    choices=["put", "nccl", "nccl-direct", "nccl-sync"],
+                    help="N>1: fused pack+put over NVLink (default); NCCL: pack, one send/recv "
+                         "per peer, unpack (nccl), one send/recv per item run (nccl-direct), or "
+                         "the round-1 path that reads the counts on the data stream (nccl-sync)")
+    ap.add_argument("--nccl-register", action="store_true",
+                    help="--exchange nccl*: ncclCommRegister the row buffers")
     args = ap.parse_args()
     CFG.clear()
     CFG.update(CONFIGS[args.config], name=args.config)

@@ -351,6 +351,36 @@ int orch_dispatch(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const in
                   int64_t in_cap, void* d_out, int64_t out_cap, void* d_send, int64_t send_cap,
                   void* d_recv, int64_t recv_cap, void* stream);
 
+/* The NCCL exchange with its counts read from a pinned host mirror of the
+ * layout (orch_xplan), filled on the METADATA stream right after orch_layout:
+ * orch_dispatch_nccl waits for that copy only (an event), never for the data
+ * stream, so the host issues step k+1's exchange while step k's rows still
+ * move. Two forms:
+ *  - staged (d_send, d_recv given): one pass packs the rows that stay into
+ *    d_out and the off-rank rows into per-peer segments of d_send; one grouped
+ *    ncclSend/ncclRecv per peer; one pass unpacks d_recv into d_out;
+ *  - direct (d_send == NULL): every off-rank item is one ncclSend from its run
+ *    in d_in to its run in the peer's d_out (no staging passes; NCCL pairs a
+ *    peer's sends and receives in issue order, item order on both sides), the
+ *    rows that stay move with one copy kernel. Fast only for few, large items
+ *    (every NCCL operation has a fixed cost). */
+typedef struct orch_xplan orch_xplan;
+int orch_xplan_create(orch_ctx* ctx, int64_t max_n, int32_t nranks, orch_xplan** out);
+void orch_xplan_destroy(orch_xplan* x);
+/* Enqueue on `stream` the copy of the layout into the plan's pinned mirror
+ * (the arrays must stay valid until orch_dispatch_nccl has run). */
+int orch_xplan_fetch(orch_ctx* ctx, orch_xplan* x, int32_t d, int64_t n, const int64_t* d_len,
+                     const int32_t* d_origin, const orch_balance_out* bal,
+                     const orch_layout_out* layout, void* stream);
+int orch_dispatch_nccl(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t row_bytes,
+                       const void* d_in, int64_t in_cap, void* d_out, int64_t out_cap,
+                       void* d_send, int64_t send_cap, void* d_recv, int64_t recv_cap,
+                       void* stream);
+/* ncclCommRegister / ncclCommDeregister of a row buffer (zero-copy transfers
+ * where NCCL supports them for send/recv). */
+int orch_comm_register(orch_comm* comm, void* ptr, size_t bytes, void** handle);
+int orch_comm_deregister(orch_comm* comm, void* handle);
+
 /* ----------------------------------------------------------- NCCL comm */
 /* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller. */
 int orch_comm_unique_id(unsigned char* h_id128);

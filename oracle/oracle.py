@@ -322,3 +322,21 @@ class RefLib:
                                           _p(ppe, C.c_int32), _p(mod, C.c_int32),
                                           _p(ml, C.c_int64)))
         return ppe, mod.reshape(n, 3), ml.reshape(n, 3)
+
+    def run_iteration(self, mix, d, per_instance, seed, c=None, nodewise=False):
+        """The reference orchestrator's run_iteration (composed delivery on):
+        LLM destinations per example and, per part (example-major), the
+        instance and position of the backbone's assembled input."""
+        E = d * per_instance
+        ppe, _, _ = self.generate(mix, E, seed)
+        parts = int(ppe.sum())
+        li, ls = np.zeros(E, np.int32), np.zeros(E, np.int32)
+        ai, ap = np.zeros(parts, np.int32), np.zeros(parts, np.int32)
+        flags = np.zeros(3, np.int32)
+        self._check(self.lib.ref_run_iteration(
+            C.c_int(mix), C.c_int(d), C.c_int(c or d), C.c_int(per_instance), C.c_uint64(seed),
+            C.c_int(1 if nodewise else 0), _p(li, C.c_int32), _p(ls, C.c_int32),
+            _p(ai, C.c_int32), _p(ap, C.c_int32), _p(flags, C.c_int32)))
+        return dict(llm_dest_inst=li, llm_dest_slot=ls, asm_inst=ai, asm_pos=ap,
+                    assembly_ok=int(flags[0]), composed_exchanges=int(flags[1]),
+                    vision_delivery_exchanges=int(flags[2]), parts_per_example=ppe)

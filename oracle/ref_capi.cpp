@@ -10,6 +10,7 @@
 //   cost                                proj/include/orchsim/core.hpp:115
 //   volume_matrix                       proj/include/orchsim/topology.hpp:49
 //   generate (synthetic MCI workload)   proj/include/orchsim/workload.hpp:48-51
+//   run_iteration (composed delivery)   proj/include/orchsim/orchestrator.hpp:131-135
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include "orchsim/balancers.hpp"
 #include "orchsim/core.hpp"
 #include "orchsim/errors.hpp"
+#include "orchsim/orchestrator.hpp"
 #include "orchsim/topology.hpp"
 #include "orchsim/workload.hpp"
 
@@ -81,6 +83,49 @@ BalancePolicy make_policy(int kind, double lambda, int64_t v) {
   p.lambda = lambda;
   p.tolerance_v = v;
   return p;
+}
+
+
+// The survey's profile sets through the reference
+// generator (workload.cpp:107-161). mix 2 = C2 (vision-instruct 0.6, text-only
+// 0.4); mix 3 = C3 MCI (vision 0.4, ASR 0.2, speech-QA 0.2, text 0.2).
+bool mix_examples(int mix, int n, uint64_t seed, std::vector<Example>* out) {
+  auto lognormal = [](double mu, double sigma, int64_t lo, int64_t hi) {
+    LengthDist d;
+    d.kind = DistKind::LogNormal;
+    d.mu = mu;
+    d.sigma = sigma;
+    d.clip_min = lo;
+    d.clip_max = hi;
+    return d;
+  };
+  TaskProfile vision{"vision-instruct",
+                     {{"vision", lognormal(6.5, 0.8, 64, 4096)},
+                      {"text", lognormal(5.0, 1.0, 8, 2048)}},
+                     0.0, "", ""};
+  TaskProfile text{"text-only", {{"text", lognormal(6.0, 1.0, 16, 8192)}}, 0.0, "", ""};
+  TaskProfile asr{"asr",
+                  {{"audio", lognormal(6.8, 0.6, 50, 3000)},
+                   {"text", lognormal(4.0, 0.6, 4, 512)}},
+                  0.9, "audio", "text"};
+  TaskProfile sqa{"speech-qa",
+                  {{"audio", lognormal(6.5, 0.7, 50, 3000)},
+                   {"text", lognormal(3.0, 1.2, 2, 1024)}},
+                  0.0, "", ""};
+  std::vector<TaskProfile> profiles;
+  std::vector<double> weights;
+  if (mix == 2) {
+    profiles = {vision, text};
+    weights = {0.6, 0.4};
+  } else if (mix == 3) {
+    profiles = {vision, asr, sqa, text};
+    weights = {0.4, 0.2, 0.2, 0.2};
+  } else {
+    g_err = "unknown mix";
+    return false;
+  }
+  *out = generate(profiles, weights, n, seed);
+  return true;
 }
 
 }  // namespace
@@ -199,41 +244,8 @@ int ref_time_balance(int kind, double lambda, int64_t v, int d, int64_t n, const
 int ref_generate(int mix, int n, uint64_t seed, int32_t* parts_per_example, int32_t* modality,
                  int64_t* meta_len) {
   try {
-    auto lognormal = [](double mu, double sigma, int64_t lo, int64_t hi) {
-      LengthDist d;
-      d.kind = DistKind::LogNormal;
-      d.mu = mu;
-      d.sigma = sigma;
-      d.clip_min = lo;
-      d.clip_max = hi;
-      return d;
-    };
-    TaskProfile vision{"vision-instruct",
-                       {{"vision", lognormal(6.5, 0.8, 64, 4096)},
-                        {"text", lognormal(5.0, 1.0, 8, 2048)}},
-                       0.0, "", ""};
-    TaskProfile text{"text-only", {{"text", lognormal(6.0, 1.0, 16, 8192)}}, 0.0, "", ""};
-    TaskProfile asr{"asr",
-                    {{"audio", lognormal(6.8, 0.6, 50, 3000)},
-                     {"text", lognormal(4.0, 0.6, 4, 512)}},
-                    0.9, "audio", "text"};
-    TaskProfile sqa{"speech-qa",
-                    {{"audio", lognormal(6.5, 0.7, 50, 3000)},
-                     {"text", lognormal(3.0, 1.2, 2, 1024)}},
-                    0.0, "", ""};
-    std::vector<TaskProfile> profiles;
-    std::vector<double> weights;
-    if (mix == 2) {
-      profiles = {vision, text};
-      weights = {0.6, 0.4};
-    } else if (mix == 3) {
-      profiles = {vision, asr, sqa, text};
-      weights = {0.4, 0.2, 0.2, 0.2};
-    } else {
-      g_err = "unknown mix";
-      return 1;
-    }
-    const auto examples = generate(profiles, weights, n, seed);
+    std::vector<Example> examples;
+    if (!mix_examples(mix, n, seed, &examples)) return 1;
     for (int j = 0; j < n; ++j) {
       const auto& ex = examples[static_cast<std::size_t>(j)];
       parts_per_example[j] = static_cast<int32_t>(ex.parts.size());
@@ -243,6 +255,69 @@ int ref_generate(int mix, int n, uint64_t seed, int32_t* parts_per_example, int3
         meta_len[3 * j + p] = ex.parts[p].metadata_length;
       }
     }
+    return 0;
+  } catch (...) {
+    return classify(std::current_exception());
+  }
+}
+
+// One training iteration of the reference orchestrator (run_iteration,
+// orchestrator.cpp:563-569) on the mix's examples (ids 0..E-1, origins j % d):
+// encoder phases vision (GreedyUnpadded) and, for mix 3, audio (BinaryPadded),
+// both rate 4, then the LLM phase (GreedyUnpadded) and the composed delivery
+// of the encoder outputs (compose_exchanges on; node-wise hosting as given,
+// on d/c nodes). Out, with parts numbered example-major (global part g):
+//   llm_dest_inst / llm_dest_slot [E]   the LLM rearrangement of each example
+//   asm_inst / asm_pos [parts]          where the backbone's assembled input
+//                                       holds the part (outcome.assembled)
+//   flags[0] assembly_ok, [1] composed exchanges, [2] delivery exchanges of
+//   the vision universe
+int ref_run_iteration(int mix, int d, int c, int per_instance, uint64_t seed, int nodewise,
+                      int32_t* llm_dest_inst, int32_t* llm_dest_slot, int32_t* asm_inst,
+                      int32_t* asm_pos, int32_t* flags) {
+  try {
+    const int E = d * per_instance;
+    std::vector<Example> examples;
+    if (!mix_examples(mix, E, seed, &examples)) return 1;
+    std::vector<int> origins(static_cast<std::size_t>(E));
+    for (int j = 0; j < E; ++j) origins[j] = j % d;
+    auto phase = [](const char* name, const char* modality, PolicyKind kind, int64_t rate) {
+      PhaseSpec p;
+      p.name = name;
+      if (modality) p.modality = ModalityId(modality);
+      p.policy.kind = kind;
+      p.cost_model = policy_cost_model(p.policy);
+      p.downsample_rate = rate;
+      return p;
+    };
+    std::vector<PhaseSpec> phases{phase("vision", "vision", PolicyKind::GreedyUnpadded, 4)};
+    if (mix == 3) phases.push_back(phase("audio", "audio", PolicyKind::BinaryPadded, 4));
+    phases.push_back(phase("llm", nullptr, PolicyKind::GreedyUnpadded, 1));
+    ClusterTopology topo{d, c, 2.0, 1.0};
+    OrchestratorOptions opt;
+    opt.nodewise = nodewise != 0;
+    opt.compose_exchanges = true;
+    const IterationOutcome out = run_iteration(examples, origins, phases, topo, opt);
+    std::vector<int> next(static_cast<std::size_t>(d), 0);
+    std::vector<int64_t> part_base(static_cast<std::size_t>(E) + 1, 0);
+    for (int j = 0; j < E; ++j) {
+      const SlotRef dst = out.llm_rearrangement.dest_of(SlotRef{origins[j], next[origins[j]]++});
+      llm_dest_inst[j] = dst.instance;
+      llm_dest_slot[j] = dst.slot;
+      part_base[j + 1] = part_base[j] + static_cast<int64_t>(examples[j].parts.size());
+    }
+    for (int64_t g = 0; g < part_base[E]; ++g) asm_inst[g] = asm_pos[g] = -1;
+    for (int i = 0; i < d; ++i)
+      for (std::size_t k = 0; k < out.assembled[i].size(); ++k) {
+        const PlacedPart& pp = out.assembled[i][k];
+        const int64_t g = part_base[pp.example_id] + pp.part_index;
+        asm_inst[g] = i;
+        asm_pos[g] = static_cast<int32_t>(k);
+      }
+    flags[0] = out.report.assembly_ok ? 1 : 0;
+    flags[1] = out.report.composed_exchange_count;
+    const auto it = out.report.delivery_exchanges_per_encoder.find("vision");
+    flags[2] = it == out.report.delivery_exchanges_per_encoder.end() ? -1 : it->second;
     return 0;
   } catch (...) {
     return classify(std::current_exception());

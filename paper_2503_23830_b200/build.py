@@ -59,17 +59,19 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_cuda(force=False):
-    os.makedirs(LIB, exist_ok=True)
+def build_cuda(force=False, lib_dir=LIB):
+    """lib_dir: a diagnostics variant (e.g. ORCH_NVCC_EXTRA=-DORCH_SMALL_PROFILE) can be
+    built beside the product library and selected with ORCH_LIB_PATH."""
+    os.makedirs(lib_dir, exist_ok=True)
     nccl_inc, nccl_lib = _nccl_dirs()
-    out = os.path.join(LIB, "liborchsim_b200.so")
+    out = os.path.join(lib_dir, "liborchsim_b200.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
     deps.append(os.path.join(INCLUDE, "orchsim_capi.h"))
     if not force and not _stale(out, deps):
         return out
     objs = []
     for src in CU_SOURCES:
-        obj = os.path.join(LIB, src.replace(".cu", ".o"))
+        obj = os.path.join(lib_dir, src.replace(".cu", ".o"))
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if os.environ.get("ORCH_PTXAS_V") else "-O3",
               *os.environ.get("ORCH_NVCC_EXTRA", "").split(),
@@ -128,11 +130,21 @@ def build_cpp_api_bench(force=False):
     return outs
 
 
+def build_p2pbench(force=False):
+    """scripts/p2pbench.cu: the NVLink push / pull / copy-engine ceilings (measurement tool)."""
+    out = os.path.join(LIB, "p2pbench")
+    src = os.path.join(ROOT, "scripts", "p2pbench.cu")
+    if force or _stale(out, [src]):
+        _run([NVCC, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-o", out, src])
+    return out
+
+
 def build_all(force=False):
     build_cuda(force)
     build_host(force)
     build_ref_tests(force)
     build_cpp_api_bench(force)
+    build_p2pbench(force)
 
 
 if __name__ == "__main__":

@@ -36,7 +36,8 @@ EXPORTED = [
     "orch_gather_window_stamps", "orch_window_release", "orch_window_status", "orch_put_at",
     "orch_comm_create_local", "orch_window_create_local", "orch_gather_window_create_local",
     "orch_exchange_report", "orch_exchange_report_host", "orch_allgather_volumes",
-    "orch_allgather_volumes_host",
+    "orch_allgather_volumes_host", "orch_xplan_create", "orch_xplan_destroy", "orch_xplan_fetch",
+    "orch_dispatch_nccl", "orch_comm_register", "orch_comm_deregister",
 ]
 
 
@@ -96,6 +97,7 @@ def lib():
         L.orch_ctx_destroy.restype = None
         L.orch_comm_destroy.restype = None
         L.orch_window_ptr.restype = C.c_void_p
+        L.orch_xplan_destroy.restype = None
         L.orch_window_bytes.restype = C.c_size_t
         _lib = L
     return _lib
@@ -225,10 +227,39 @@ class Comm:
         _check(lib().orch_comm_unique_id(buf))
         return bytes(buf)
 
+    def register(self, t) -> C.c_void_p:
+        """ncclCommRegister of a device buffer (a torch tensor); returns the handle."""
+        h = C.c_void_p()
+        _check(lib().orch_comm_register(self.h, _ptr(t), C.c_size_t(t.numel() * t.element_size()),
+                                        C.byref(h)))
+        return h
+
+    def deregister(self, h):
+        _check(lib().orch_comm_deregister(self.h, h))
+
     def close(self):
         if self.h:
             lib().orch_comm_destroy(self.h)
             self.h = C.c_void_p()
+
+
+class XPlan:
+    """orch_xplan: pinned host mirror of a layout for orch_dispatch_nccl."""
+
+    def __init__(self, ctx: "Context", max_n: int, P: int):
+        self.h = C.c_void_p()
+        _check(lib().orch_xplan_create(ctx.h, C.c_int64(max_n), C.c_int32(P), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().orch_xplan_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Window:
@@ -525,6 +556,24 @@ class Context:
                                    C.c_int64(self._rows(rows_out, R)), _ptr(send),
                                    C.c_int64(self._rows(send, R)), _ptr(recv),
                                    C.c_int64(self._rows(recv, R)), _stream(stream)))
+
+    def xplan_fetch(self, xplan: "XPlan", d, length, origin, bal: Balance, lay: Layout,
+                    stream=None):
+        """Copy the layout's per-item runs into the plan's pinned mirror (metadata stream)."""
+        _check(lib().orch_xplan_fetch(self.h, xplan.h, C.c_int32(d), C.c_int64(length.numel()),
+                                      _ptr(length), _ptr(origin), C.byref(bal.struct()),
+                                      C.byref(lay.struct()), _stream(stream)))
+
+    def dispatch_nccl(self, xplan: "XPlan", row_bytes, rows_in, rows_out, comm: Comm,
+                      send=None, recv=None, stream=None):
+        """NCCL exchange with host counts from the plan: staged (send/recv given: pack,
+        one send/recv per peer, unpack) or direct (one ncclSend/ncclRecv per item run)."""
+        R = row_bytes
+        _check(lib().orch_dispatch_nccl(self.h, comm.h, xplan.h, C.c_size_t(R), _ptr(rows_in),
+                                        C.c_int64(self._rows(rows_in, R)), _ptr(rows_out),
+                                        C.c_int64(self._rows(rows_out, R)), _ptr(send),
+                                        C.c_int64(self._rows(send, R)), _ptr(recv),
+                                        C.c_int64(self._rows(recv, R)), _stream(stream)))
 
     def pack(self, rank, P, d, length, origin, bal: Balance, lay: Layout, row_bytes, rows_in,
              rows_out, send, stream=None):

@@ -627,3 +627,13 @@ int orch_padded_bound_feasible_host(orch_ctx* ctx, int32_t d, int64_t n, const i
 }
 
 }  // extern "C"
+
+#ifdef ORCH_SMALL_PROFILE
+// Diagnostics build only (ORCH_NVCC_EXTRA=-DORCH_SMALL_PROFILE): clock64 stamps
+// of the last k_balance_small launch at its stage boundaries (SMALL_MARK/SUB).
+extern "C" int orch_debug_small_profile(long long* h_out16) {
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  ORCH_CUDA_TRY(cudaMemcpyFromSymbol(h_out16, orchb::g_small_prof, 16 * sizeof(long long)));
+  return ORCH_OK;
+}
+#endif

@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
   if (MODE != kUnpack) over = over || a.in_rows[a.me] > a.in_cap;
   if (MODE == kPut)  // every rank's window has the same capacity
     for (int q = 0; q < a.P; ++q) over = over || a.out_rows[q] > a.out_cap;
-  if (MODE == kPack) {
+  if (MODE == kPack && a.send) {
     int64_t st = 0;
     for (int q = 0; q < a.P; ++q)
       if (q != a.me) st += a.send_rows[a.me * a.P + q];
@@ -517,6 +517,7 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
       } else if (MODE == kPack) {
         s = a.in + lo * R;
         const int q = a.dest[pos] / a.c;
+        if (q != a.me && !a.send) continue;  // local rows only (orch_dispatch_nccl)
         t = q == a.me ? a.out + (a.rank_dst_off[pos] + skip) * R
                       : a.send + (a.displ[q] + a.pair_off[pos] + skip) * R;
       } else if (MODE == kPut) {  // straight into the destination rank's output (NVLink)
@@ -589,7 +590,7 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
   if (MODE != kUnpack) over = over || a.in_rows[a.me] > a.in_cap;
   if (MODE == kPut)  // every rank's window has the same capacity
     for (int q = 0; q < a.P; ++q) over = over || a.out_rows[q] > a.out_cap;
-  if (MODE == kPack) {
+  if (MODE == kPack && a.send) {
     int64_t st = 0;
     for (int q = 0; q < a.P; ++q)
       if (q != a.me) st += a.send_rows[a.me * a.P + q];
@@ -684,10 +685,12 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
           s = a.in + a.rank_src_off[pos] * R + skip;
           d = a.out + lo;
         } else if (MODE == kPack) {
-          s = a.in + lo;
           const int q = a.dest[pos] / a.c;
-          d = q == a.me ? a.out + a.rank_dst_off[pos] * R + skip
-                        : a.send + (a.displ[q] + a.pair_off[pos]) * R + skip;
+          if (q == a.me || a.send) {  // no send buffer: local rows only (orch_dispatch_nccl)
+            s = a.in + lo;
+            d = q == a.me ? a.out + a.rank_dst_off[pos] * R + skip
+                          : a.send + (a.displ[q] + a.pair_off[pos]) * R + skip;
+          }
         } else if (MODE == kPut) {
           s = a.in + lo;
           d = a.peer_out[a.dest[pos] / a.c] + a.win_off + a.rank_dst_off[pos] * R + skip;
@@ -1210,6 +1213,207 @@ int orch_dispatch(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const in
   if (rc) return rc;
   return orch_unpack(ctx, me, P, d, n, d_len, d_origin, bal, L, R, d_recv, d_out, out_cap,
                      stream);
+}
+
+// -------------------------------------------- NCCL exchange, per item run
+}  // extern "C"
+
+struct orch_xplan {
+  int64_t max_n = 0;
+  int P = 1;
+  char* pinned = nullptr;  // h_len | h_rso | h_rdo | in/out rows | send rows, displs | h_org | h_dst
+  int64_t *h_len = nullptr, *h_rso = nullptr, *h_rdo = nullptr, *h_in = nullptr, *h_out = nullptr;
+  int64_t *h_send = nullptr, *h_sdis = nullptr, *h_rdis = nullptr;  // [P*P] each
+  int32_t *h_org = nullptr, *h_dst = nullptr;
+  cudaEvent_t ready = nullptr;
+  // the device-side view of the same layout (for the local-rows kernel)
+  int d = 0;
+  int64_t n = 0;
+  const int64_t* d_len = nullptr;
+  const int32_t* d_origin = nullptr;
+  orch_balance_out bal{};
+  orch_layout_out lay{};
+  bool fetched = false;
+  std::vector<int64_t> order;  // host scratch: per-peer item lists
+};
+
+extern "C" {
+
+int orch_xplan_create(orch_ctx* ctx, int64_t max_n, int32_t P, orch_xplan** out) {
+  if (!ctx || !out || max_n < 0 || P < 1 || P > 8) return fail(ORCH_INVALID_ARGUMENT, "bad plan arguments");
+  auto* x = new orch_xplan();
+  x->max_n = max_n;
+  x->P = P;
+  const size_t nn = static_cast<size_t>(max_n > 0 ? max_n : 1);
+  const size_t bytes = nn * (8 * 3 + 4 * 2) + 16 * static_cast<size_t>(P) + 24 * P * P;
+  if (cudaMallocHost(&x->pinned, bytes) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->ready, cudaEventDisableTiming) != cudaSuccess) {
+    if (x->pinned) cudaFreeHost(x->pinned);
+    delete x;
+    return fail(ORCH_CUDA_ERROR, "exchange plan allocation failed");
+  }
+  char* p = x->pinned;
+  x->h_len = reinterpret_cast<int64_t*>(p);
+  x->h_rso = x->h_len + nn;
+  x->h_rdo = x->h_rso + nn;
+  x->h_in = x->h_rdo + nn;
+  x->h_out = x->h_in + P;
+  x->h_send = x->h_out + P;
+  x->h_sdis = x->h_send + P * P;
+  x->h_rdis = x->h_sdis + P * P;
+  x->h_org = reinterpret_cast<int32_t*>(x->h_rdis + P * P);
+  x->h_dst = x->h_org + nn;
+  x->order.reserve(nn);
+  *out = x;
+  return ORCH_OK;
+}
+
+void orch_xplan_destroy(orch_xplan* x) {
+  if (!x) return;
+  if (x->ready) cudaEventDestroy(x->ready);
+  if (x->pinned) cudaFreeHost(x->pinned);
+  delete x;
+}
+
+int orch_xplan_fetch(orch_ctx* ctx, orch_xplan* x, int32_t d, int64_t n, const int64_t* d_len,
+                     const int32_t* d_origin, const orch_balance_out* bal,
+                     const orch_layout_out* L, void* stream) {
+  if (!ctx || !x || !bal || !L) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (n < 0 || n > x->max_n) return fail(ORCH_INVALID_ARGUMENT, "plan holds fewer items than n");
+  if (d % x->P != 0) return fail(ORCH_INVALID_ARGUMENT, "rank count must divide the instance count");
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t nn = static_cast<size_t>(n);
+  if (nn) {
+    ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_len, d_len, nn * 8, cudaMemcpyDeviceToHost, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_org, d_origin, nn * 4, cudaMemcpyDeviceToHost, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_dst, bal->dest_inst, nn * 4, cudaMemcpyDeviceToHost, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_rso, L->rank_src_off, nn * 8, cudaMemcpyDeviceToHost, st));
+    ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_rdo, L->rank_dst_off, nn * 8, cudaMemcpyDeviceToHost, st));
+  }
+  ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_in, L->in_rows, 8 * x->P, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_out, L->out_rows, 8 * x->P, cudaMemcpyDeviceToHost, st));
+  const size_t pp = 8 * static_cast<size_t>(x->P) * x->P;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_send, L->send_rows, pp, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_sdis, L->send_displ, pp, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(x->h_rdis, L->recv_displ, pp, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaEventRecord(x->ready, st));
+  x->d = d;
+  x->n = n;
+  x->d_len = d_len;
+  x->d_origin = d_origin;
+  x->bal = *bal;
+  x->lay = *L;
+  x->fetched = true;
+  return ORCH_OK;
+}
+
+int orch_dispatch_nccl(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const void* d_in,
+                       int64_t in_cap, void* d_out, int64_t out_cap, void* d_send,
+                       int64_t send_cap, void* d_recv, int64_t recv_cap, void* stream) {
+  if (!ctx || !comm || !x) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (!comm->comm) return fail(ORCH_INVALID_ARGUMENT, "loopback communicator has no NCCL");
+  if (!x->fetched) return fail(ORCH_INVALID_ARGUMENT, "orch_xplan_fetch has not been called");
+  const int P = comm->size, me = comm->rank;
+  if (P != x->P) return fail(ORCH_INVALID_ARGUMENT, "plan and communicator rank counts differ");
+  int rc = check_move_args(ctx, P, me, x->d, &x->bal, &x->lay, R);
+  if (rc) return rc;
+  const bool staged = d_send != nullptr;
+  if (!aligned16(d_in) || !aligned16(d_out) || !aligned16(d_send) || !aligned16(d_recv))
+    return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
+  if (staged && !d_recv) return fail(ORCH_INVALID_ARGUMENT, "staged exchange needs a receive buffer");
+  auto st = static_cast<cudaStream_t>(stream);
+  // 1. local rows to the output, and (staged) the off-rank rows to the send
+  //    buffer, segment by segment: one pass over the input
+  if (x->n > 0) {
+    MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
+    a.offs = x->bal.src_offset;
+    a.members = x->bal.src_member;
+    a.iter_rows = x->lay.in_rows;
+    a.iter_cap = in_cap;
+    a.in_cap = in_cap;
+    a.out_cap = out_cap;
+    a.send_cap = send_cap;
+    a.displ = x->lay.send_displ + me * P;
+    a.in = static_cast<const char*>(d_in);
+    a.out = static_cast<char*>(d_out);
+    a.send = static_cast<char*>(d_send);  // NULL: off-rank rows go item by item below
+    rc = run_move(ctx, kPack, a, x->n, x->lay.rank_src_off, st);
+    if (rc) return rc;
+  }
+  // 2. the layout's host mirror: waits for the metadata stream's copy only,
+  //    never for this stream
+  ORCH_CUDA_TRY(cudaEventSynchronize(x->ready));
+  if (x->h_in[me] > in_cap || x->h_out[me] > out_cap)
+    return fail(ORCH_INVALID_ARGUMENT, "row buffer smaller than the layout");
+  const char* in = static_cast<const char*>(d_in);
+  char* out = static_cast<char*>(d_out);
+  if (staged) {  // one send and one receive per peer
+    int64_t stot = 0, rtot = 0;
+    for (int q = 0; q < P; ++q)
+      if (q != me) {
+        stot += x->h_send[me * P + q];
+        rtot += x->h_send[q * P + me];
+      }
+    if (stot > send_cap || rtot > recv_cap)
+      return fail(ORCH_INVALID_ARGUMENT, "send / receive buffer smaller than the off-rank rows");
+    const char* send = static_cast<const char*>(d_send);
+    char* recv = static_cast<char*>(d_recv);
+    ORCH_NCCL_TRY(ncclGroupStart());
+    for (int k = 1; k < P; ++k) {
+      const int q = (me + k) % P, r = (me + P - k) % P;
+      const int64_t s_rows = x->h_send[me * P + q], r_rows = x->h_send[r * P + me];
+      if (s_rows > 0)
+        ORCH_NCCL_TRY(ncclSend(send + x->h_sdis[me * P + q] * R, static_cast<size_t>(s_rows) * R,
+                               ncclInt8, q, comm->comm, st));
+      if (r_rows > 0)
+        ORCH_NCCL_TRY(ncclRecv(recv + x->h_rdis[me * P + r] * R, static_cast<size_t>(r_rows) * R,
+                               ncclInt8, r, comm->comm, st));
+    }
+    ORCH_NCCL_TRY(ncclGroupEnd());
+    // 3. received rows to their destination slots
+    if (x->n > 0) {
+      MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
+      a.offs = x->bal.bin_offset;
+      a.members = x->bal.bin_member;
+      a.iter_rows = x->lay.out_rows;
+      a.iter_cap = out_cap;
+      a.out_cap = out_cap;
+      a.displ = x->lay.recv_displ + me * P;
+      a.recv = static_cast<const char*>(d_recv);
+      a.out = out;
+      rc = run_move(ctx, kUnpack, a, x->n, x->lay.rank_dst_off, st);
+      if (rc) return rc;
+    }
+    return ORCH_OK;
+  }
+  const int c = x->d / P;
+  ORCH_NCCL_TRY(ncclGroupStart());
+  for (int k = 1; k < P; ++k) {  // peers in ring order from this rank
+    const int q = (me + k) % P;
+    for (int64_t i = 0; i < x->n; ++i) {
+      const int r = x->h_org[i] / c, t = x->h_dst[i] / c;
+      const size_t bytes = static_cast<size_t>(x->h_len[i]) * R;
+      if (r == me && t == q)
+        ORCH_NCCL_TRY(ncclSend(in + x->h_rso[i] * R, bytes, ncclInt8, q, comm->comm, st));
+      else if (r == q && t == me)
+        ORCH_NCCL_TRY(ncclRecv(out + x->h_rdo[i] * R, bytes, ncclInt8, q, comm->comm, st));
+    }
+  }
+  ORCH_NCCL_TRY(ncclGroupEnd());
+  return ORCH_OK;
+}
+
+int orch_comm_register(orch_comm* comm, void* ptr, size_t bytes, void** handle) {
+  if (!comm || !ptr || !handle) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (!comm->comm) return fail(ORCH_INVALID_ARGUMENT, "loopback communicator has no NCCL");
+  ORCH_NCCL_TRY(ncclCommRegister(comm->comm, ptr, bytes, handle));
+  return ORCH_OK;
+}
+
+int orch_comm_deregister(orch_comm* comm, void* handle) {
+  if (!comm || !comm->comm) return fail(ORCH_INVALID_ARGUMENT, "null communicator");
+  ORCH_NCCL_TRY(ncclCommDeregister(comm->comm, handle));
+  return ORCH_OK;
 }
 
 // ------------------------------------------------------------- cost model

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 from oracle import Oracle  # noqa: E402
-from paper_2503_23830_b200.capi import Comm, Context, GatherWindow, Window  # noqa: E402
+from paper_2503_23830_b200.capi import Comm, Context, GatherWindow, OrchError, Window, XPlan  # noqa: E402
 
 
 def main():
@@ -87,6 +87,23 @@ def main():
                 torch.cuda.synchronize()
                 ok = ok and int(lay.status.item()) == 0
                 ok = ok and torch.equal(rout.cpu(), torch.from_numpy(outs[rank]))
+                # per-item ncclSend/ncclRecv between the row buffers (no staging)
+                xp = XPlan(ctx, n, P)
+                ms = torch.cuda.Stream()
+                ms.wait_stream(torch.cuda.current_stream())
+                ctx.xplan_fetch(xp, d, gl, go, bal, lay, stream=ms)
+                rout.zero_()
+                ctx.dispatch_nccl(xp, R, rin, rout, comm)
+                torch.cuda.synchronize()
+                ok = ok and int(lay.status.item()) == 0
+                ok = ok and torch.equal(rout.cpu(), torch.from_numpy(outs[rank]))
+                # the same plan, staged: pack, one send/recv per peer, unpack
+                rout.zero_()
+                ctx.dispatch_nccl(xp, R, rin, rout, comm, send=send, recv=recv)
+                torch.cuda.synchronize()
+                ok = ok and int(lay.status.item()) == 0
+                ok = ok and torch.equal(rout.cpu(), torch.from_numpy(outs[rank]))
+                xp.close()
                 # fused pack + put into IPC windows (one pass over NVLink)
                 wbytes = max(int(e["out_tokens"].max()), 1) * R
                 win = Window(ctx, comm, wbytes)
@@ -119,6 +136,12 @@ def main():
                     failures += 1
                     print(f"rank {rank}: MISMATCH seed={seed} kind={kind} R={R} d={d} n={n}",
                           flush=True)
+    # windows of different sizes are refused on every rank, before any mapping
+    try:
+        Window(ctx, comm, 4096 * (1 + rank)).close()
+        failures += 1
+    except OrchError as e:
+        failures += 0 if e.code == 1 else 1
     t = torch.tensor([failures])
     dist.all_reduce(t)
     gwin.close()
