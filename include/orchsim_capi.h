@@ -62,6 +62,7 @@ extern "C" {
  * context is used by one host thread at a time (not thread-safe). */
 typedef struct orch_ctx orch_ctx;
 typedef struct orch_comm orch_comm; /* NCCL communicator over the ranks of one box               */
+typedef struct orch_window orch_window; /* a row buffer every rank can store into (below)    */
 
 /* BalancePolicy (balancers.hpp:14-18). */
 typedef struct {
@@ -411,7 +412,6 @@ int orch_barrier(orch_comm* comm, void* stream);
  * consumers keep the SMs they need. Waits give up after ~4 s: the barrier or
  * the acquire sets the window status, and a put whose acquire timed out sets
  * layout->status to ORCH_CUDA_ERROR and stores nothing. */
-typedef struct orch_window orch_window;
 int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out);
 void* orch_window_ptr(const orch_window* w);
 size_t orch_window_bytes(const orch_window* w);

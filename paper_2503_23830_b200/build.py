@@ -135,7 +135,9 @@ def build_p2pbench(force=False):
     out = os.path.join(LIB, "p2pbench")
     src = os.path.join(ROOT, "scripts", "p2pbench.cu")
     if force or _stale(out, [src]):
-        _run([NVCC, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-o", out, src])
+        nccl_inc, nccl_lib = _nccl_dirs()
+        _run([NVCC, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-I", nccl_inc, "-o", out, src,
+              "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"])
     return out
 
 

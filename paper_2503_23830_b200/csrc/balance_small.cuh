@@ -507,6 +507,45 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
           return (df < 0 ? -df : df) < v ? aq < bq : as < bs;
         };
         int64_t x_next = n > 0 ? static_cast<int64_t>(S.xs[0]) : 0;
+        if (d <= 8) {
+          // d <= 8 (C5): every lane holds the whole beats matrix, byte j of M =
+          // beats_j, so the champion chain is walked in registers (no
+          // shuffles): from best, the next champion is the lowest batch above
+          // it that beats it. An item changes one batch b; two ballots give
+          // its column (whom b beats) and row (who beats b).
+          uint64_t M = 0;
+          const unsigned dm8 = (1u << d) - 1u;
+          for (int k = 0; k < n; ++k) {
+            const int64_t x = x_next;
+            if (k + 1 < n) x_next = static_cast<int64_t>(S.xs[k + 1]);
+            const int64_t xx = x * x;
+            int best = 0;
+            for (;;) {
+              const unsigned m = static_cast<unsigned>(M >> (8 * best)) & dm8 & (0xffu << (best + 1));
+              if (!m) break;
+              best = __ffs(m) - 1;
+            }
+            const bool me = lane == best;
+            const int at = me ? k : SmallSmem<ITEMS>::NS;  // per sorted position, no branch
+            S.g_bin[at] = static_cast<uint8_t>(lane);
+            S.id_rank[at] = static_cast<uint16_t>(cnt);
+            S.pfx[at] = qs;
+            cnt += me ? 1 : 0;
+            qs += me ? x : 0;
+            qq += me ? xx : 0;
+            const int64_t bs = __shfl_sync(~0u, qs, best);
+            const int64_t bq = __shfl_sync(~0u, qq, best);
+            const bool b_beats_me = lane < d && lane != best && less(bs, bq, qs, qq);
+            const bool i_beat_b = lane < d && lane != best && less(qs, qq, bs, bq);
+            const unsigned col = __ballot_sync(~0u, b_beats_me);  // bit j: best beats j
+            const unsigned row = __ballot_sync(~0u, i_beat_b);    // bit j: j beats best
+            uint64_t spread = 0;  // bit j of col -> bit 8j
+#pragma unroll
+            for (int j = 0; j < 8; ++j) spread |= static_cast<uint64_t>((col >> j) & 1u) << (8 * j);
+            M = (M & ~(0x0101010101010101ull << best)) | (spread << best);
+            M = (M & ~(0xffull << (8 * best))) | (static_cast<uint64_t>(row) << (8 * best));
+          }
+        } else {
         for (int k = 0; k < n; ++k) {
           const int64_t x = x_next;
           if (k + 1 < n) x_next = static_cast<int64_t>(S.xs[k + 1]);  // off the critical path
@@ -532,6 +571,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
           const bool i_beat_b = lane < d && lane != best && less(qs, qq, bs, bq);
           const unsigned row = __ballot_sync(~0u, i_beat_b);
           beats = lane == best ? row : ((beats & ~(1u << best)) | (b_beats_me ? 1u << best : 0u));
+        }
         }
         if (lane < d) {
           S.cnt_a[lane] = cnt;

@@ -416,6 +416,18 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
                : "memory");
 }
 
+// Clips the segment run [p0, p0 + cnt) to [lo, hi); false when nothing is left.
+// shift = how far the run's start moved (the same shift applies to the other side).
+__device__ __forceinline__ bool clip_run(int64_t& p0, int64_t& cnt, int64_t lo, int64_t hi,
+                                         int64_t& shift) {
+  const int64_t a0 = p0 > lo ? p0 : lo, a1 = p0 + cnt < hi ? p0 + cnt : hi;
+  if (a1 <= a0) return false;
+  shift = a0 - p0;
+  p0 = a0;
+  cnt = a1 - a0;
+  return true;
+}
+
 // Block-wide copy of nvec 16-byte vectors, 4 loads in flight per thread.
 __device__ __forceinline__ void block_copy(int4* __restrict__ dst, const int4* __restrict__ src,
                                            int64_t nvec) {
@@ -460,6 +472,12 @@ struct MoveArgs {
   uint64_t need_free;          // kPut: ... must have reached this, else nothing is stored
   unsigned long long* chunk_counter;  // TMA path: next unclaimed chunk (zeroed by k_unit_map)
   int scramble;                       // kPut: claim chunk batches in a scrambled order
+  // Sliced NCCL exchange (orch_dispatch_nccl): move only the rows whose
+  // position in their (origin rank -> dest rank) segment lies in
+  // [slo[peer], shi[peer]) -- peer = dest rank (kPack) / origin rank (kUnpack);
+  // skip_local leaves the rows that stay on the rank to another round.
+  int clip, skip_local;
+  int64_t slo[8], shi[8];
   int32_t* status;
   size_t R;
   const char* in;
@@ -511,25 +529,35 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
       const int64_t skip = lo - off;
       const char* s;
       char* t;
+      int64_t cnt = hi - lo;
       if (MODE == kLocal) {
         s = a.in + (a.rank_src_off[pos] + skip) * R;
         t = a.out + lo * R;
       } else if (MODE == kPack) {
         s = a.in + lo * R;
         const int q = a.dest[pos] / a.c;
-        if (q != a.me && !a.send) continue;  // local rows only (orch_dispatch_nccl)
-        t = q == a.me ? a.out + (a.rank_dst_off[pos] + skip) * R
-                      : a.send + (a.displ[q] + a.pair_off[pos] + skip) * R;
+        if (q == a.me) {
+          if (a.skip_local) continue;
+          t = a.out + (a.rank_dst_off[pos] + skip) * R;
+        } else {
+          if (!a.send) continue;  // local rows only (orch_dispatch_nccl, direct)
+          int64_t p0 = a.pair_off[pos] + skip, sh = 0;
+          if (a.clip && !clip_run(p0, cnt, a.slo[q], a.shi[q], sh)) continue;
+          s += sh * R;
+          t = a.send + (a.displ[q] + p0) * R;
+        }
       } else if (MODE == kPut) {  // straight into the destination rank's output (NVLink)
         s = a.in + lo * R;
         t = a.peer_out[a.dest[pos] / a.c] + a.win_off + (a.rank_dst_off[pos] + skip) * R;
       } else {
         const int r = a.origin[pos] / a.c;
         if (r == a.me) continue;  // moved by the pack kernel
-        s = a.recv + (a.displ[r] + a.pair_off[pos] + skip) * R;
-        t = a.out + lo * R;
+        int64_t p0 = a.pair_off[pos] + skip, sh = 0;
+        if (a.clip && !clip_run(p0, cnt, a.slo[r], a.shi[r], sh)) continue;
+        s = a.recv + (a.displ[r] + p0) * R;
+        t = a.out + (lo + sh) * R;
       }
-      block_copy(reinterpret_cast<int4*>(t), reinterpret_cast<const int4*>(s), (hi - lo) * vrow);
+      block_copy(reinterpret_cast<int4*>(t), reinterpret_cast<const int4*>(s), cnt * vrow);
     }
   }
   if (MODE == kPut) __threadfence_system();
@@ -681,15 +709,23 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
         const int64_t skip = lo - ob;
         const char* s = nullptr;
         char* d = nullptr;
+        int64_t cnt = hi - lo;
         if (MODE == kLocal) {
           s = a.in + a.rank_src_off[pos] * R + skip;
           d = a.out + lo;
         } else if (MODE == kPack) {
           const int q = a.dest[pos] / a.c;
-          if (q == a.me || a.send) {  // no send buffer: local rows only (orch_dispatch_nccl)
-            s = a.in + lo;
-            d = q == a.me ? a.out + a.rank_dst_off[pos] * R + skip
-                          : a.send + (a.displ[q] + a.pair_off[pos]) * R + skip;
+          if (q == a.me) {
+            if (!a.skip_local) {
+              s = a.in + lo;
+              d = a.out + a.rank_dst_off[pos] * R + skip;
+            }
+          } else if (a.send) {  // no send buffer: local rows only (orch_dispatch_nccl, direct)
+            int64_t p0 = a.pair_off[pos] * R + skip, sh = 0;
+            if (!a.clip || clip_run(p0, cnt, a.slo[q] * R, a.shi[q] * R, sh)) {
+              s = a.in + lo + sh;
+              d = a.send + a.displ[q] * R + p0;
+            }
           }
         } else if (MODE == kPut) {
           s = a.in + lo;
@@ -697,14 +733,17 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
         } else {
           const int r = a.origin[pos] / a.c;
           if (r != a.me) {
-            s = a.recv + (a.displ[r] + a.pair_off[pos]) * R + skip;
-            d = a.out + lo;
+            int64_t p0 = a.pair_off[pos] * R + skip, sh = 0;
+            if (!a.clip || clip_run(p0, cnt, a.slo[r] * R, a.shi[r] * R, sh)) {
+              s = a.recv + a.displ[r] * R + p0;
+              d = a.out + lo + sh;
+            }
           }
         }
         if (s) {
           T.src[lane][np] = s;
           T.dst[lane][np] = d;
-          T.bytes[lane][np] = static_cast<uint32_t>(hi - lo);
+          T.bytes[lane][np] = static_cast<uint32_t>(cnt);
           ++np;
         }
         if (ib >= b1) break;
@@ -1016,8 +1055,9 @@ MoveArgs make_args(int P, int me, int d, const int64_t* len, const int32_t* orig
 
 constexpr int kMoveGrid = kSMs * 8;
 
+// grid_cap > 0: at most that many CTAs (leaves SMs to a concurrent NCCL kernel)
 int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter_off,
-             cudaStream_t st) {
+             cudaStream_t st, int grid_cap = 0) {
   const bool tma = static_cast<int64_t>(a.R) >= kTmaMinRow;
   const int64_t unit_bytes = tma ? kTmaChunk : kUnitRows * static_cast<int64_t>(a.R);
   const int64_t cap_units = (a.iter_cap * static_cast<int64_t>(a.R)) / unit_bytes + 2;
@@ -1050,7 +1090,8 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
       return v >= 0 && v < kSMs ? v : 0;
     }();
     const bool fat = mode == kPut && free_sms > 0;
-    const int tma_grid = fat ? kSMs - free_sms : kSMs * ctas_per_sm;
+    int tma_grid = fat ? kSMs - free_sms : kSMs * ctas_per_sm;
+    if (grid_cap > 0 && tma_grid > grid_cap) tma_grid = grid_cap;
     const int sm_put = kTmaPutStages * kTmaChunk;
     const int sm_req = fat ? 227 * 1024 - static_cast<int>(sizeof(TmaTable)) - 64 : sm_put;
     static PerDeviceOnce attr_done;
@@ -1080,13 +1121,13 @@ int run_move(orch_ctx* ctx, int mode, MoveArgs a, int64_t n, const int64_t* iter
   } else {
     launch(ctx, [&] {
       if (mode == kLocal)
-        k_move<kLocal><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+        k_move<kLocal><<<grid_cap > 0 ? grid_cap * 8 : kMoveGrid, kMoveThreads, 0, st>>>(a);
       else if (mode == kPack)
-        k_move<kPack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+        k_move<kPack><<<grid_cap > 0 ? grid_cap * 8 : kMoveGrid, kMoveThreads, 0, st>>>(a);
       else if (mode == kPut)
-        k_move<kPut><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+        k_move<kPut><<<grid_cap > 0 ? grid_cap * 8 : kMoveGrid, kMoveThreads, 0, st>>>(a);
       else
-        k_move<kUnpack><<<kMoveGrid, kMoveThreads, 0, st>>>(a);
+        k_move<kUnpack><<<grid_cap > 0 ? grid_cap * 8 : kMoveGrid, kMoveThreads, 0, st>>>(a);
     });
   }
   ORCH_CUDA_TRY(cudaGetLastError());
@@ -1235,6 +1276,12 @@ struct orch_xplan {
   orch_layout_out lay{};
   bool fetched = false;
   std::vector<int64_t> order;  // host scratch: per-peer item lists
+  // sliced staged exchange: pack (caller's stream) -> NCCL (s_comm) -> unpack (s_unpack)
+  static constexpr int kMaxSlices = 16;
+  int dev = -1;
+  cudaStream_t s_comm = nullptr, s_unpack = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_pack[kMaxSlices] = {}, ev_comm[kMaxSlices] = {};
 };
 
 extern "C" {
@@ -1271,6 +1318,19 @@ int orch_xplan_create(orch_ctx* ctx, int64_t max_n, int32_t P, orch_xplan** out)
 void orch_xplan_destroy(orch_xplan* x) {
   if (!x) return;
   if (x->ready) cudaEventDestroy(x->ready);
+  if (x->s_comm) {
+    cudaStreamSynchronize(x->s_comm);
+    cudaStreamSynchronize(x->s_unpack);
+    cudaStreamDestroy(x->s_comm);
+    cudaStreamDestroy(x->s_unpack);
+    cudaEventDestroy(x->ev_entry);
+    cudaEventDestroy(x->ev_done);
+    for (int k = 0; k < orch_xplan::kMaxSlices; ++k) {
+      cudaEventDestroy(x->ev_pack[k]);
+      cudaEventDestroy(x->ev_comm[k]);
+    }
+  }
+
   if (x->pinned) cudaFreeHost(x->pinned);
   delete x;
 }
@@ -1307,6 +1367,145 @@ int orch_xplan_fetch(orch_ctx* ctx, orch_xplan* x, int32_t d, int64_t n, const i
   return ORCH_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// The staged exchange in K slices, pipelined over three streams: slice k of
+// every (this rank -> peer) segment is packed on the caller's stream, sent by
+// one NCCL group on s_comm while slice k+1 is packed, and the slices received
+// are unpacked on s_unpack while the next ones travel. The rows that stay on
+// the rank move with slice 0's pack. Segment slicing is a function of the
+// segment size only, so sender and receiver agree without communicating.
+int staged_rounds(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const void* d_in,
+                  int64_t in_cap, void* d_out, int64_t out_cap, void* d_send, int64_t send_cap,
+                  void* d_recv, int64_t recv_cap, cudaStream_t st) {
+  const int P = comm->size, me = comm->rank;
+  static const int env_slices = [] {
+    // 1 by default: on 2 B200s, overlapping the pack / unpack kernels with
+    // NCCL's made the exchange slower (C2: 351 -> 250 GB/s at 4 slices;
+    // profiles/r02_nccl.md), so the slicing stays an option
+    const char* e = getenv("ORCH_NCCL_SLICES");
+    const int v = e ? atoi(e) : 1;
+    return v >= 1 && v <= orch_xplan::kMaxSlices ? v : 1;
+  }();
+  // Slices of at least ~8 MB (ORCH_NCCL_MIN_SLICE_BYTES): fewer for small
+  // exchanges. Every rank must cut the same slices, so K comes from a quantity
+  // all ranks agree on: the largest off-rank segment of the replicated layout.
+  static const int64_t min_slice_bytes = [] {
+    const char* e = getenv("ORCH_NCCL_MIN_SLICE_BYTES");
+    const long long v = e ? atoll(e) : (8ll << 20);
+    return static_cast<int64_t>(v > 0 ? v : (8ll << 20));
+  }();
+  const int64_t min_slice_rows = (min_slice_bytes + static_cast<int64_t>(R) - 1) / static_cast<int64_t>(R);
+  int64_t glob = 0;
+  for (int k = 0; k < P * P; ++k)
+    if (k / P != k % P) glob = std::max(glob, x->h_send[k]);
+  const int Kg = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(env_slices, (glob + min_slice_rows - 1) / min_slice_rows)));
+  int dev = 0;
+  ORCH_CUDA_TRY(cudaGetDevice(&dev));
+  if (!x->s_comm || x->dev != dev) {
+    int lo = 0, hi = 0;
+    ORCH_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ORCH_CUDA_TRY(cudaStreamCreateWithPriority(&x->s_comm, cudaStreamNonBlocking, hi));
+    ORCH_CUDA_TRY(cudaStreamCreateWithFlags(&x->s_unpack, cudaStreamNonBlocking));
+    ORCH_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_entry, cudaEventDisableTiming));
+    ORCH_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_done, cudaEventDisableTiming));
+    for (int k = 0; k < orch_xplan::kMaxSlices; ++k) {
+      ORCH_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_pack[k], cudaEventDisableTiming));
+      ORCH_CUDA_TRY(cudaEventCreateWithFlags(&x->ev_comm[k], cudaEventDisableTiming));
+    }
+    x->dev = dev;
+  }
+  ORCH_CUDA_TRY(cudaEventRecord(x->ev_entry, st));
+  ORCH_CUDA_TRY(cudaStreamWaitEvent(x->s_comm, x->ev_entry, 0));
+  ORCH_CUDA_TRY(cudaStreamWaitEvent(x->s_unpack, x->ev_entry, 0));
+  auto slice = [&](int64_t rows, int k) { return rows * k / Kg; };
+  // sliced: the pack / unpack kernels leave SMs to NCCL's kernel running beside them
+  static const int mover_sms = [] {
+    const char* e = getenv("ORCH_NCCL_MOVER_SMS");
+    const int v = e ? atoi(e) : 96;
+    return v >= 8 && v <= kSMs ? v : 96;
+  }();
+  const int cap = Kg > 1 ? mover_sms : 0;
+  const char* send = static_cast<const char*>(d_send);
+  char* recv = static_cast<char*>(d_recv);
+  for (int k = 0; k < Kg; ++k) {
+    int rc;
+    if (x->n > 0) {  // pack slice k (and, in slice 0, the rows that stay)
+      MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
+      a.offs = x->bal.src_offset;
+      a.members = x->bal.src_member;
+      a.iter_rows = x->lay.in_rows;
+      a.iter_cap = in_cap;
+      a.in_cap = in_cap;
+      a.out_cap = out_cap;
+      a.send_cap = send_cap;
+      a.displ = x->lay.send_displ + me * P;
+      a.in = static_cast<const char*>(d_in);
+      a.out = static_cast<char*>(d_out);
+      a.send = static_cast<char*>(d_send);
+      a.clip = 1;
+      a.skip_local = k != 0;
+      for (int q = 0; q < P; ++q) {
+        const int64_t S = q == me ? 0 : x->h_send[me * P + q];
+        a.slo[q] = slice(S, k);
+        a.shi[q] = slice(S, k + 1);
+      }
+      rc = run_move(ctx, kPack, a, x->n, x->lay.rank_src_off, st, cap);
+      if (rc) return rc;
+    }
+    ORCH_CUDA_TRY(cudaEventRecord(x->ev_pack[k], st));
+    ORCH_CUDA_TRY(cudaStreamWaitEvent(x->s_comm, x->ev_pack[k], 0));
+    ORCH_NCCL_TRY(ncclGroupStart());
+    for (int j = 1; j < P; ++j) {
+      const int q = (me + j) % P, r = (me + P - j) % P;
+      const int64_t S = x->h_send[me * P + q], Sr = x->h_send[r * P + me];
+      const int64_t s0 = slice(S, k), s1 = slice(S, k + 1);
+      const int64_t r0 = slice(Sr, k), r1 = slice(Sr, k + 1);
+      if (s1 > s0)
+        ORCH_NCCL_TRY(ncclSend(send + (x->h_sdis[me * P + q] + s0) * R,
+                               static_cast<size_t>(s1 - s0) * R, ncclInt8, q, comm->comm,
+                               x->s_comm));
+      if (r1 > r0)
+        ORCH_NCCL_TRY(ncclRecv(recv + (x->h_rdis[me * P + r] + r0) * R,
+                               static_cast<size_t>(r1 - r0) * R, ncclInt8, r, comm->comm,
+                               x->s_comm));
+    }
+    ORCH_NCCL_TRY(ncclGroupEnd());
+    ORCH_CUDA_TRY(cudaEventRecord(x->ev_comm[k], x->s_comm));
+    ORCH_CUDA_TRY(cudaStreamWaitEvent(x->s_unpack, x->ev_comm[k], 0));
+    if (x->n > 0) {  // unpack the slices that arrived
+      MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
+      a.offs = x->bal.bin_offset;
+      a.members = x->bal.bin_member;
+      a.iter_rows = x->lay.out_rows;
+      a.iter_cap = out_cap;
+      a.out_cap = out_cap;
+      a.displ = x->lay.recv_displ + me * P;
+      a.recv = static_cast<const char*>(d_recv);
+      a.out = static_cast<char*>(d_out);
+      a.clip = 1;
+      for (int r = 0; r < P; ++r) {
+        const int64_t S = r == me ? 0 : x->h_send[r * P + me];
+        a.slo[r] = slice(S, k);
+        a.shi[r] = slice(S, k + 1);
+      }
+      rc = run_move(ctx, kUnpack, a, x->n, x->lay.rank_dst_off, x->s_unpack, cap);
+      if (rc) return rc;
+    }
+  }
+  (void)recv_cap;
+  ORCH_CUDA_TRY(cudaEventRecord(x->ev_done, x->s_unpack));
+  ORCH_CUDA_TRY(cudaStreamWaitEvent(st, x->ev_done, 0));
+  return ORCH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int orch_dispatch_nccl(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const void* d_in,
                        int64_t in_cap, void* d_out, int64_t out_cap, void* d_send,
                        int64_t send_cap, void* d_recv, int64_t recv_cap, void* stream) {
@@ -1322,9 +1521,8 @@ int orch_dispatch_nccl(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, 
     return fail(ORCH_INVALID_ARGUMENT, "row buffers must be 16-byte aligned");
   if (staged && !d_recv) return fail(ORCH_INVALID_ARGUMENT, "staged exchange needs a receive buffer");
   auto st = static_cast<cudaStream_t>(stream);
-  // 1. local rows to the output, and (staged) the off-rank rows to the send
-  //    buffer, segment by segment: one pass over the input
-  if (x->n > 0) {
+  // direct: the rows that stay move with one copy kernel, the rest item by item
+  if (!staged && x->n > 0) {
     MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
     a.offs = x->bal.src_offset;
     a.members = x->bal.src_member;
@@ -1340,14 +1538,14 @@ int orch_dispatch_nccl(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, 
     rc = run_move(ctx, kPack, a, x->n, x->lay.rank_src_off, st);
     if (rc) return rc;
   }
-  // 2. the layout's host mirror: waits for the metadata stream's copy only,
-  //    never for this stream
+  // the layout's host mirror: waits for the metadata stream's copy only, never
+  // for this stream
   ORCH_CUDA_TRY(cudaEventSynchronize(x->ready));
   if (x->h_in[me] > in_cap || x->h_out[me] > out_cap)
     return fail(ORCH_INVALID_ARGUMENT, "row buffer smaller than the layout");
   const char* in = static_cast<const char*>(d_in);
   char* out = static_cast<char*>(d_out);
-  if (staged) {  // one send and one receive per peer
+  if (staged) {  // one send and one receive per peer and slice
     int64_t stot = 0, rtot = 0;
     for (int q = 0; q < P; ++q)
       if (q != me) {
@@ -1356,35 +1554,8 @@ int orch_dispatch_nccl(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, 
       }
     if (stot > send_cap || rtot > recv_cap)
       return fail(ORCH_INVALID_ARGUMENT, "send / receive buffer smaller than the off-rank rows");
-    const char* send = static_cast<const char*>(d_send);
-    char* recv = static_cast<char*>(d_recv);
-    ORCH_NCCL_TRY(ncclGroupStart());
-    for (int k = 1; k < P; ++k) {
-      const int q = (me + k) % P, r = (me + P - k) % P;
-      const int64_t s_rows = x->h_send[me * P + q], r_rows = x->h_send[r * P + me];
-      if (s_rows > 0)
-        ORCH_NCCL_TRY(ncclSend(send + x->h_sdis[me * P + q] * R, static_cast<size_t>(s_rows) * R,
-                               ncclInt8, q, comm->comm, st));
-      if (r_rows > 0)
-        ORCH_NCCL_TRY(ncclRecv(recv + x->h_rdis[me * P + r] * R, static_cast<size_t>(r_rows) * R,
-                               ncclInt8, r, comm->comm, st));
-    }
-    ORCH_NCCL_TRY(ncclGroupEnd());
-    // 3. received rows to their destination slots
-    if (x->n > 0) {
-      MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
-      a.offs = x->bal.bin_offset;
-      a.members = x->bal.bin_member;
-      a.iter_rows = x->lay.out_rows;
-      a.iter_cap = out_cap;
-      a.out_cap = out_cap;
-      a.displ = x->lay.recv_displ + me * P;
-      a.recv = static_cast<const char*>(d_recv);
-      a.out = out;
-      rc = run_move(ctx, kUnpack, a, x->n, x->lay.rank_dst_off, st);
-      if (rc) return rc;
-    }
-    return ORCH_OK;
+    return staged_rounds(ctx, comm, x, R, d_in, in_cap, d_out, out_cap, d_send, send_cap, d_recv,
+                         recv_cap, st);
   }
   const int c = x->d / P;
   ORCH_NCCL_TRY(ncclGroupStart());
@@ -1888,6 +2059,32 @@ int orch_window_destroy(orch_window* w) {
   return rc;
 }
 
+}  // extern "C"
+
+namespace {
+
+// The first put after a barrier on a stream: k_window_acquire waits until
+// every rank released the steps closed so far (see orch_window_release).
+int window_acquire(orch_ctx* ctx, orch_window* w, void* stream) {
+  if (w->epoch == 0 || (w->acq_epoch == w->epoch && w->acq_stream == stream)) return ORCH_OK;
+  char* flags = w->base + w->flags_off;
+  auto st = static_cast<cudaStream_t>(stream);
+  launch(ctx, [&] {
+    k_window_acquire<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(flags + kFlagFree),
+                                       w->comm->size, w->epoch,
+                                       reinterpret_cast<uint64_t*>(flags + kFlagAcquired),
+                                       reinterpret_cast<int32_t*>(flags + kFlagStatus));
+  });
+  ORCH_CUDA_TRY(cudaGetLastError());
+  w->acq_epoch = w->epoch;
+  w->acq_stream = stream;
+  return ORCH_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int orch_put_at(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int64_t* d_len,
                 const int32_t* d_origin, const orch_balance_out* bal, const orch_layout_out* L,
                 size_t R, const void* d_in, int64_t in_cap, orch_window* out_win,
@@ -1915,19 +2112,8 @@ int orch_put_at(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int6
     char* flags = out_win->base + out_win->flags_off;
     a.acquired = reinterpret_cast<const uint64_t*>(flags + kFlagAcquired);
     a.need_free = out_win->epoch;  // the steps closed so far must all be consumed
-    auto st = static_cast<cudaStream_t>(stream);
-    if (out_win->epoch > 0 &&
-        (out_win->acq_epoch != out_win->epoch || out_win->acq_stream != stream)) {
-      launch(ctx, [&] {
-        k_window_acquire<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(flags + kFlagFree), P,
-                                           out_win->epoch,
-                                           reinterpret_cast<uint64_t*>(flags + kFlagAcquired),
-                                           reinterpret_cast<int32_t*>(flags + kFlagStatus));
-      });
-      ORCH_CUDA_TRY(cudaGetLastError());
-      out_win->acq_epoch = out_win->epoch;
-      out_win->acq_stream = stream;
-    }
+    rc = window_acquire(ctx, out_win, stream);
+    if (rc) return rc;
     static const int scramble = [] {
       const char* e = getenv("ORCH_PUT_SCRAMBLE");
       return e ? atoi(e) : 1;

@@ -8,6 +8,8 @@
 //                 (the put's mechanism, k_move_tma<kPut>)
 //           ldg   kernel pull: LDG.128 from the peer, STG.128 to local HBM
 //           ce    copy engine: cudaMemcpyPeerAsync
+//           nccl  one grouped ncclSend/ncclRecv per transfer (ncclCommInitAll,
+//                 one communicator per GPU in this process)
 //   pattern uni   GPU 0 -> GPU 1
 //           bidir 0 -> 1 and 1 -> 0 at once
 //           a2a   every GPU to every other GPU at once (1/(N-1) of its bytes each)
@@ -19,6 +21,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o p2pbench scripts/p2pbench.cu
 //   ./p2pbench [MiB per GPU, default 1024]
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -102,13 +105,30 @@ struct Xfer {
   size_t bytes;
 };
 
+std::vector<ncclComm_t> g_comms;
+
 double run(const std::vector<Xfer>& xs, const std::string& method, int ngpu,
            std::vector<cudaStream_t>& st, std::vector<cudaEvent_t>& e0, std::vector<cudaEvent_t>& e1) {
   for (int g = 0; g < ngpu; ++g) {
     CK(cudaSetDevice(g));
     CK(cudaEventRecord(e0[g], st[g]));
   }
+  if (method == "nccl") {  // x.dev is the sender; the receiver posts the matching recv
+    ncclGroupStart();
+    for (const Xfer& x : xs) {
+      cudaPointerAttributes at;
+      CK(cudaPointerGetAttributes(&at, x.dst));
+      const int to = at.device;
+      ncclSend(x.src, x.bytes, ncclInt8, to, g_comms[x.dev], st[x.dev]);
+      ncclRecv(x.dst, x.bytes, ncclInt8, x.dev, g_comms[to], st[to]);
+    }
+    if (ncclGroupEnd() != ncclSuccess) {
+      std::fprintf(stderr, "nccl group failed\n");
+      std::exit(1);
+    }
+  }
   for (const Xfer& x : xs) {
+    if (method == "nccl") break;
     CK(cudaSetDevice(x.dev));
     if (method == "stg" || method == "ldg")
       k_stg<<<kSMs * 4, 512, 0, st[x.dev]>>>(reinterpret_cast<int4*>(x.dst),
@@ -165,7 +185,12 @@ int main(int argc, char** argv) {
     CK(cudaSetDevice(g));
     CK(cudaDeviceSynchronize());
   }
-  const char* methods[] = {"stg", "tma", "ldg", "ce"};
+  g_comms.resize(ngpu);
+  if (ncclCommInitAll(g_comms.data(), ngpu, nullptr) != ncclSuccess) {
+    std::fprintf(stderr, "ncclCommInitAll failed\n");
+    return 1;
+  }
+  const char* methods[] = {"stg", "tma", "ldg", "ce", "nccl"};
   const char* patterns[] = {"uni", "bidir", "a2a"};
   for (const char* pat : patterns) {
     for (const char* m : methods) {
@@ -173,7 +198,7 @@ int main(int argc, char** argv) {
       std::vector<Xfer> xs;
       size_t sent_per_gpu = bytes;
       auto add = [&](int from, int to, size_t off, size_t len) {
-        // push / ce: the sender runs the copy; ldg: the receiver pulls
+        // push / ce / nccl: the sender runs the copy; ldg: the receiver pulls
         if (method == "ldg")
           xs.push_back({to, b[to] + off, a[from] + off, len});
         else

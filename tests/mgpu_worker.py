@@ -20,6 +20,8 @@ from paper_2503_23830_b200.capi import Comm, Context, GatherWindow, OrchError, W
 
 
 def main():
+    # small cases still take the sliced, pipelined staged NCCL path (4 slices)
+    os.environ.setdefault("ORCH_NCCL_MIN_SLICE_BYTES", "65536")
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
