@@ -61,6 +61,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def nvlink_peaks(n_gpus):
+    """NVLink ceilings measured by scripts/p2pbench.cu (profiles/nvlink_peaks.json):
+    the all-to-all pattern at this GPU count when measured, else at 2 GPUs."""
+    with open(os.path.join(ROOT, "profiles", "nvlink_peaks.json")) as f:
+        p = json.load(f)["by_gpus"]
+    key = str(n_gpus) if str(n_gpus) in p else "2"
+    a2a = p[key]["a2a"]
+    return dict(copy_engine=a2a["ce"], kernel_push=max(a2a["tma"], a2a["stg"]), nccl=a2a["nccl"],
+                measured_at_gpus=int(key))
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -602,17 +613,20 @@ def run_b200(args):
         line["exchange"] = args.exchange
         line["gather"] = args.gather
         line["nodewise_hosting"] = bool(args.nodewise)
+        nv = nvlink_peaks(world)
         line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes, "max_egress_bytes": egress,
                        "max_ingress_bytes": ingress, "busbw_gbs_rank": busbw,
-                       "nvlink_peak_gbs": 900.0, "nvlink_measured_gbs": 770.0,
+                       "nvlink_spec_gbs": 900.0, "nvlink_measured": nv,
+                       "frac_of_kernel_push": busbw / nv["kernel_push"],
+                       "frac_of_nccl_ceiling": busbw / nv["nccl"],
                        "note": "max over ranks of max(off-rank bytes sent, received) / max over "
-                               "ranks of the device time of the dispatch calls; NVLink push "
-                               "ceiling measured with scratch/p2pbench.cu: ~710 GB/s per direction"}
-        # at N > 1 the row movement is NVLink-bound: roofline against the
-        # measured peer copy (B200_PROFILING.md: 770 GB/s per direction per GPU)
+                               "ranks of the device time of the dispatch calls; ceilings measured "
+                               "by scripts/p2pbench.cu (profiles/nvlink_peaks.json)"}
+        # at N > 1 the row movement is NVLink-bound: roofline against the best
+        # measured per-direction copy (the copy engines, all-to-all pattern)
         hbm_view = line["roofline"]
-        line["roofline"] = {"bound": "nvlink", "achieved": busbw, "peak": 770.0, "unit": "GB/s",
-                            "frac": busbw / 770.0, "traffic": None,
+        line["roofline"] = {"bound": "nvlink", "achieved": busbw, "peak": nv["copy_engine"],
+                            "unit": "GB/s", "frac": busbw / nv["copy_engine"], "traffic": None,
                             "kernel": {"put": "k_move_tma<kPut> (orch_put)",
                                        "nccl": "pack + ncclSend/ncclRecv per peer + unpack, host "
                                                "counts from the metadata stream "
@@ -622,7 +636,8 @@ def run_b200(args):
                                        "nccl-sync": "pack + ncclSend/ncclRecv + unpack, counts "
                                                     "read on the data stream (orch_dispatch)"
                                        }[args.exchange],
-                            "peak_kind": "measured peer copy (B200_PROFILING.md)",
+                            "peak_kind": "measured copy-engine peer copy, all-to-all at "
+                                         f"{nv['measured_at_gpus']} GPUs (profiles/nvlink_peaks.json)",
                             "share_of_step": hbm_view["share_of_step"],
                             "hbm_view": {k: hbm_view[k] for k in ("achieved", "peak", "frac")}}
     host_bytes = 2 * tokens * R

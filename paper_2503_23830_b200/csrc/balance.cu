@@ -68,10 +68,12 @@ orch_cost_model policy_model(const orch_policy& p) {  // balancers.cpp:162-176
 }
 
 // distribute_min_sum on [first, n) of the descending order.
+// lpt_*: n-sized scratch for the one-CTA LPT's sorted-position results (d > 32).
 int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const uint32_t* xs,
                   const int32_t* order, const int64_t* init_load, const int32_t* init_count,
                   int32_t* di, int32_t* ds, int64_t* doff, int32_t* bc, int64_t* bt,
-                  orch_summary* s, cudaStream_t st) {
+                  orch_summary* s, cudaStream_t st, int32_t* lpt_bin, int32_t* lpt_slot,
+                  int64_t* lpt_off) {
   if (d <= 32) {
     launch(ctx, [&] {
       k_greedy_warp<<<1, 32, 0, st>>>(d, n, first, xs, order, init_load, init_count, di, ds, doff,
@@ -83,8 +85,13 @@ int launch_greedy(orch_ctx* ctx, int d, int64_t n, const int64_t* first, const u
                                          static_cast<int>(sm)));
       launch(ctx, [&] {
         kern<<<1, threads, sm, st>>>(d, n, first, xs, order, init_load, init_count, di, ds, doff,
-                                     bc, bt, s);
+                                     bc, bt, s, lpt_bin, lpt_slot, lpt_off);
       });
+      if (lpt_bin && n > 0)
+        launch(ctx, [&] {
+          k_lpt_scatter<<<blocks_for(n, kThreads), kThreads, 0, st>>>(
+              n, first, order, lpt_bin, lpt_slot, lpt_off, di, ds, doff, s);
+        });
       return ORCH_OK;
     };
     int rc;
@@ -275,6 +282,14 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   plan.add(&pad_cand, kSMs);
   uint16_t* pad_nx1;
   plan.add(&pad_nx1, n <= kNxMax ? n : 1);
+  // sorted-position results of the one-CTA LPT (greedy / conv, d > 32)
+  int32_t *lpt_bin, *lpt_slot;
+  int64_t* lpt_off;
+  const bool lpt = !identity_only && !padded_only && d > 32 &&
+                   (kind == ORCH_GREEDY_UNPADDED || kind == ORCH_CONVTRANSFORMER);
+  plan.add(&lpt_bin, lpt ? nn : 1);
+  plan.add(&lpt_slot, lpt ? nn : 1);
+  plan.add(&lpt_off, lpt ? nn : 1);
   // CUB temporary storage (max over the calls below)
   size_t cub_bytes = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, b, key_org, sorted_org, iota, ident_order, (int)nn, 0,
@@ -406,7 +421,8 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   if (!identity_only && kind != ORCH_BINARY_PADDED) {
     if (kind == ORCH_GREEDY_UNPADDED) {
       rc = launch_greedy(ctx, d, n, nullptr, xs, order, nullptr, nullptr, dest_inst, dest_slot,
-                         dst_off, a_count, a_tokens, S, st);
+                         dst_off, a_count, a_tokens, S, st, lpt ? lpt_bin : nullptr, lpt_slot,
+                         lpt_off);
       if (rc) return rc;
     } else if (kind == ORCH_QUADRATIC_TOLERANCE) {
       const size_t sm = (2 * sizeof(int64_t) + sizeof(int32_t)) * d;
@@ -418,14 +434,15 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
       });
     } else {  // ConvTransformer
       rc = launch_greedy(ctx, d, n, nullptr, xs, order, nullptr, nullptr, g_di, g_ds, g_doff,
-                         a_count, a_tokens, S, st);
+                         a_count, a_tokens, S, st, lpt ? lpt_bin : nullptr, lpt_slot, lpt_off);
       if (rc) return rc;
       launch(ctx, [&] {
         k_conv_seed<<<1, 32, 0, st>>>(d, n, xs, order, a_tokens, dest_inst, dest_slot, dst_off,
                                       seed_load, seed_count, consumed, S);
       });
       rc = launch_greedy(ctx, d, n, consumed, xs, order, seed_load, seed_count, dest_inst,
-                         dest_slot, dst_off, a_count, a_tokens, S, st);
+                         dest_slot, dst_off, a_count, a_tokens, S, st, lpt ? lpt_bin : nullptr,
+                         lpt_slot, lpt_off);
       if (rc) return rc;
     }
     size_t tb = cub_bytes;

@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
   for (int i = tid; i < n; i += kSmallThreads) {
     const int o = S.org[i];
     const int slot = S.chunk_base[o][i >> 5] + S.id_rank[i];
+    ORCH_DCHECK(o >= 0 && o < d && S.off_id[o] + slot < S.off_id[o + 1]);
     a.src_slot[i] = slot;
     S.ord_id[S.off_id[o] + slot] = i;
     S.a_slot[i] = static_cast<uint16_t>(S.off_id[o] + slot);  // identity position (a_slot is free here)
@@ -461,7 +462,22 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
     // key bits of the longest item; ascending padding sorts after equal keys (stable sort)
     const int lbits = 32 - __clz(static_cast<unsigned>(S.maxlen));
     const uint32_t pad_asc = lbits == 32 ? 0xffffffffu : ((1u << lbits) - 1u);
-    {
+    if (n <= kSmallThreads) {
+      // few items (C5: 64): each thread ranks its item against all n keys
+      // (broadcast shared-memory reads) -- the stable order of the reference's
+      // std::stable_sort by length, without the block radix sort's passes
+      if (tid < n) {
+        const uint32_t ki = static_cast<uint32_t>(S.len[tid]);
+        int r = 0;
+        for (int j = 0; j < n; ++j) {
+          const uint32_t kj = static_cast<uint32_t>(S.len[j]);
+          r += (asc ? kj < ki : kj > ki) || (kj == ki && j < tid);
+        }
+        ORCH_DCHECK(r >= 0 && r < n);
+        S.ord[r] = tid;
+        S.xs[r] = ki;
+      }
+    } else {
       uint32_t keys[ITEMS];
       int32_t vals[ITEMS];
 #pragma unroll
@@ -741,6 +757,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       const int sl = S.a_slot[i];
       a.dest_inst[i] = b;
       a.dest_slot[i] = sl;
+      ORCH_DCHECK(b >= 0 && b < d && S.off_a[b] + sl < S.off_a[b + 1]);
       S.ord[S.off_a[b] + sl] = i;  // reuse: algorithm members in (batch, slot) order
     }
     __syncthreads();

@@ -11,6 +11,24 @@
 
 #include "orchsim_capi.h"
 
+// Bounds-checked diagnostics build (ORCH_NVCC_EXTRA=-DORCH_BOUNDS_CHECK): device
+// asserts that print the failing condition and trap, so a bad index or an
+// out-of-buffer copy kills the run loudly (compute-sanitizer is not available
+// on the GPU pool; profiles/r02_bounds_check.md).
+#ifdef ORCH_BOUNDS_CHECK
+#define ORCH_DCHECK(cond)                                                       \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      printf("ORCH_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);     \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define ORCH_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace orchb {
 
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs

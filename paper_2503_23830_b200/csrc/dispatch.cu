@@ -84,8 +84,11 @@ __global__ void k_volume(int d, int64_t n, const int64_t* __restrict__ len,
                          unsigned long long* __restrict__ V) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
+  {
+    ORCH_DCHECK(origin[i] >= 0 && origin[i] < d && dest[i] >= 0 && dest[i] < d);
     atomicAdd(&V[static_cast<size_t>(origin[i]) * d + dest[i]],
               static_cast<unsigned long long>(len[i]));
+  }
 }
 
 // ------------------------------------------------------------------ layout
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(kLayoutSmallThreads, 1)
   for (int i = t; i < d; i += blockDim.x) inst_in[i] = inst_out[i] = 0;
   __syncthreads();
   for (int i = t; i < n; i += blockDim.x) {  // k_inst_rows
+    ORCH_DCHECK(origin[i] >= 0 && origin[i] < d && bal.dest_inst[i] >= 0 && bal.dest_inst[i] < d);
     const unsigned long long l = static_cast<unsigned long long>(len[i]);
     atomicAdd(&inst_in[origin[i]], l);
     atomicAdd(&inst_out[bal.dest_inst[i]], l);
@@ -416,6 +420,24 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
                : "memory");
 }
 
+#ifdef ORCH_BOUNDS_CHECK
+// [p, p + bytes) inside [base, base + cap_bytes) (bounds-checked builds)
+__device__ __forceinline__ bool within(const void* p, int64_t bytes, const void* base,
+                                       int64_t cap_bytes) {
+  const char* c = static_cast<const char*>(p);
+  const char* b = static_cast<const char*>(base);
+  return bytes >= 0 && c >= b && c + bytes <= b + cap_bytes;
+}
+
+// Rows this rank receives from its peers (the recv buffer's extent).
+__device__ __forceinline__ int64_t recv_rows_of(const int64_t* send_rows, int P, int me) {
+  int64_t t = 0;
+  for (int r = 0; r < P; ++r)
+    if (r != me) t += send_rows[r * P + me];
+  return t;
+}
+#endif
+
 // Clips the segment run [p0, p0 + cnt) to [lo, hi); false when nothing is left.
 // shift = how far the run's start moved (the same shift applies to the other side).
 __device__ __forceinline__ bool clip_run(int64_t& p0, int64_t& cnt, int64_t lo, int64_t hi,
@@ -557,6 +579,24 @@ __global__ void __launch_bounds__(kMoveThreads) k_move(MoveArgs a) {
         s = a.recv + (a.displ[r] + p0) * R;
         t = a.out + (lo + sh) * R;
       }
+#ifdef ORCH_BOUNDS_CHECK
+      {
+        const int64_t nb = cnt * static_cast<int64_t>(R);
+        const int64_t Rr = static_cast<int64_t>(R);
+        if (MODE == kUnpack)
+          ORCH_DCHECK(within(s, nb, a.recv, recv_rows_of(a.send_rows, a.P, a.me) * Rr));
+        else
+          ORCH_DCHECK(within(s, nb, a.in, a.in_cap * Rr));
+        if (MODE == kPut) {
+          const char* pb = a.peer_out[a.dest[pos] / a.c] + a.win_off;
+          ORCH_DCHECK(within(t, nb, pb, a.out_cap * Rr));
+        } else if (MODE == kPack && a.dest[pos] / a.c != a.me) {
+          ORCH_DCHECK(within(t, nb, a.send, a.send_cap * Rr));
+        } else {
+          ORCH_DCHECK(within(t, nb, a.out, a.out_cap * Rr));
+        }
+      }
+#endif
       block_copy(reinterpret_cast<int4*>(t), reinterpret_cast<const int4*>(s), cnt * vrow);
     }
   }
@@ -741,6 +781,19 @@ __global__ void __launch_bounds__(32) k_move_tma(MoveArgs a) {
           }
         }
         if (s) {
+#ifdef ORCH_BOUNDS_CHECK
+          if (MODE == kUnpack)
+            ORCH_DCHECK(within(s, cnt, a.recv, recv_rows_of(a.send_rows, a.P, a.me) * R));
+          else
+            ORCH_DCHECK(within(s, cnt, a.in, a.in_cap * R));
+          if (MODE == kPut)
+            ORCH_DCHECK(within(d, cnt, a.peer_out[a.dest[pos] / a.c] + a.win_off, a.out_cap * R));
+          else if (MODE == kPack && a.dest[pos] / a.c != a.me)
+            ORCH_DCHECK(within(d, cnt, a.send, a.send_cap * R));
+          else
+            ORCH_DCHECK(within(d, cnt, a.out, a.out_cap * R));
+          ORCH_DCHECK(cnt > 0 && cnt % 16 == 0);
+#endif
           T.src[lane][np] = s;
           T.dst[lane][np] = d;
           T.bytes[lane][np] = static_cast<uint32_t>(cnt);
@@ -874,6 +927,7 @@ __global__ void __launch_bounds__(1024) k_gather_put(GatherArgs a) {
     }
     const int64_t l = a.len[i];
     const int32_t o = a.org[i];
+    ORCH_DCHECK(p < a.max_n);
     for (int q = 0; q < a.P; ++q) {
       len_of(q)[p] = l;
       org_of(q)[p] = o;

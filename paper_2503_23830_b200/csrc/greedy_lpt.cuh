@@ -131,7 +131,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const int64_t* __restrict__ init_load, const int32_t* __restrict__ init_count,
                  int32_t* __restrict__ dest_inst, int32_t* __restrict__ dest_slot,
                  int64_t* __restrict__ dst_off, int32_t* __restrict__ bin_count,
-                 int64_t* __restrict__ bin_tokens, orch_summary* s) {
+                 int64_t* __restrict__ bin_tokens, orch_summary* s,
+                 int32_t* __restrict__ s_bin, int32_t* __restrict__ s_slot,
+                 int64_t* __restrict__ s_off) {
+  // s_bin given: results go out by SORTED position (coalesced stores from the
+  // one SM; k_lpt_scatter moves them to input positions on every SM) -- the
+  // scattered per-item stores were half of a round's time at d = 2560
   using Sh = LptShape<kThreads>;
   if (pipeline_failed(s)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -165,6 +170,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   int64_t base = static_cast<int64_t>(s_min);
   int64_t next = d_first ? *d_first : 0;
   int64_t rounds = 0;
+#ifdef ORCH_SMALL_PROFILE
+  // diagnostics build: cycles per round stage, summed over the rounds
+  long long prof[4] = {0, 0, 0, 0}, t_prev = clock64();
+#define LPT_STAGE(i)                       \
+  do {                                     \
+    const long long t_ = clock64();        \
+    prof[i] += t_ - t_prev;                \
+    t_prev = t_;                           \
+  } while (0)
+#else
+#define LPT_STAGE(i) \
+  do {               \
+  } while (0)
+#endif
   constexpr int kPer = Sh::kSlots / kThreads;  // round slots r = tid + i * kThreads
   while (next < n) {
     const int m = static_cast<int>(n - next < d ? n - next : d);
@@ -175,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kPer; ++i) {
       const int r = tid + i * kThreads;
       xr[i] = r < m ? static_cast<int64_t>(xs[next + r]) : 0;
-      pr[i] = r < m ? order[next + r] : 0;
+      pr[i] = r < m && !s_bin ? order[next + r] : 0;
     }
     // ---- rank the bins by (load, index)
     if (tid == 0) {
@@ -201,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (__any_sync(~0u, wd) && lane == 0) s_wide = 1;
     if (lane == 0) atomicMax(&s_max, mx);
     __syncthreads();
+    LPT_STAGE(0);
     const uint16_t* rank_bin;
     if (!s_wide) {
       const int bits = s_max ? 32 - __clz(s_max) : 1;
@@ -230,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncthreads();
       rank_bin = out;
     }
+    LPT_STAGE(1);
     // ---- k = first rank r with load_(r) - load_(0) >= x_r
     const int64_t L0 = load[rank_bin[0]];
 #pragma unroll
@@ -244,29 +265,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
+    LPT_STAGE(2);
     const int k = s_k;  // >= 1: x_0 >= 1 > 0 = load_(0) - load_(0)
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int r = tid + i * kThreads;
       if (r < k) {
         const int b = rank_bin[r];  // distinct bins within a round
-        const int32_t pos = pr[i];
-        dest_inst[pos] = b;
-        dest_slot[pos] = cnt[b]++;
-        dst_off[pos] = load[b];
+        if (s_bin) {
+          const int64_t q = next + r;
+          s_bin[q] = b;
+          s_slot[q] = cnt[b];
+          s_off[q] = load[b];
+        } else {
+          const int32_t pos = pr[i];
+          dest_inst[pos] = b;
+          dest_slot[pos] = cnt[b];
+          dst_off[pos] = load[b];
+        }
+        ++cnt[b];
         load[b] += xr[i];
       }
     }
     __syncthreads();
+    LPT_STAGE(3);
     base = L0;
     next += k;
     ++rounds;
   }
+#ifdef ORCH_SMALL_PROFILE
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) g_small_prof[8 + i] = prof[i];
+    g_small_prof[12] = rounds;
+  }
+#endif
+#undef LPT_STAGE
   for (int b = tid; b < d; b += kThreads) {
     bin_tokens[b] = load[b];
     bin_count[b] = cnt[b];
   }
   if (tid == 0) s->rounds = rounds;
+}
+
+// Sorted-position results of k_greedy_lpt -> input positions.
+__global__ void k_lpt_scatter(int64_t n, const int64_t* __restrict__ d_first,
+                              const int32_t* __restrict__ order, const int32_t* __restrict__ s_bin,
+                              const int32_t* __restrict__ s_slot, const int64_t* __restrict__ s_off,
+                              int32_t* __restrict__ dest_inst, int32_t* __restrict__ dest_slot,
+                              int64_t* __restrict__ dst_off, orch_summary* s) {
+  if (pipeline_failed(s)) return;
+  const int64_t f = d_first ? *d_first : 0;
+  for (int64_t k = f + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t pos = order[k];
+    dest_inst[pos] = s_bin[k];
+    dest_slot[pos] = s_slot[k];
+    dst_off[pos] = s_off[k];
+  }
 }
 
 }  // namespace
