@@ -278,6 +278,9 @@ def run_b200(args):
         s["buf"] = [dict(glen=torch.from_numpy(L).to(dev), gorg=torch.from_numpy(O).to(dev),
                          bal=Balance.alloc(D_INST, n, dev), lay=Layout.alloc(P, n, dev),
                          meta_done=torch.cuda.Event(), data_done=torch.cuda.Event(),
+                         hosting=(torch.empty(D_INST, dtype=torch.int32, device=dev),
+                                  torch.empty(D_INST, dtype=torch.int32, device=dev),
+                                  torch.empty(4, dtype=torch.int64, device=dev)),
                          xplan=XPlan(ctx_data, n, P)
                          if P > 1 and args.exchange in ("nccl", "nccl-direct") else None)
                     for _ in range(2)]
@@ -323,7 +326,8 @@ def run_b200(args):
                          out=B["bal"], stream=stream)
         mark(stream)
         if args.nodewise:  # GPU-wise hosting (orchestrator.cpp:283 with node = GPU)
-            ctx_meta.nodewise(D_INST, c, B["glen"], B["gorg"], B["bal"], stream=stream)
+            ctx_meta.nodewise(D_INST, c, B["glen"], B["gorg"], B["bal"], out=B["hosting"],
+                              stream=stream)
         mark(stream)
         ctx_meta.layout(D_INST, P, B["glen"], B["gorg"], B["bal"], out=B["lay"], stream=stream)
         if B["xplan"] is not None:  # the per-item runs for the host's NCCL calls
@@ -592,7 +596,7 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "traffic_algorithmic_per_launch": traffic_alg,
-                     "kernel": "k_move (orch_dispatch)", "peak_kind": peak_kind,
+                     "kernel": "k_move_tma<kLocal> (orch_dispatch)", "peak_kind": peak_kind,
                      "share_of_step": disp_ms / (t0.elapsed_time(t1) or 1.0)},
         "e2e": {"value": tokens * args.steps / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

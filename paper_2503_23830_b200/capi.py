@@ -373,8 +373,9 @@ class Context:
                 stream=None) -> Balance:
         """length int64 / origin int32 CUDA tensors, input order."""
         n = int(length.numel())
-        with _on(stream):
-            out = out or Balance.alloc(d, n, length.device)
+        if out is None:
+            with _on(stream):
+                out = Balance.alloc(d, n, length.device)
         pol = Policy(kind, 0, v, lam)
         s = out.struct()
         _check(lib().orch_balance(self.h, C.byref(pol), C.c_int32(d), C.c_int64(n), _ptr(length),
@@ -386,9 +387,10 @@ class Context:
                         out=None, layout=None, stream=None):
         """orch_balance_layout1: balance + the single-rank layout (fused when small)."""
         n = int(length.numel())
-        with _on(stream):
-            out = out or Balance.alloc(d, n, length.device)
-            layout = layout or Layout.alloc(1, n, length.device)
+        if out is None or layout is None:
+            with _on(stream):
+                out = out or Balance.alloc(d, n, length.device)
+                layout = layout or Layout.alloc(1, n, length.device)
         pol = Policy(kind, 0, v, lam)
         _check(lib().orch_balance_layout1(self.h, C.byref(pol), C.c_int32(d), C.c_int64(n),
                                           _ptr(length), _ptr(origin),
@@ -474,14 +476,16 @@ class Context:
         return dict(hosting=hosting, max_egress=int(info[0]), baseline_max=int(info[1]),
                     leaf_used=int(info[2]), visited=int(info[3]))
 
-    def nodewise(self, d, c, length, origin, bal: "Balance", stream=None):
+    def nodewise(self, d, c, length, origin, bal: "Balance", out=None, stream=None):
         """Relabels bal's destination batches in place; returns device tensors
-        (hosting[d], batch_to_instance[d], info[4])."""
+        (hosting[d], batch_to_instance[d], info[4]) -- `out` when given."""
         dev = length.device
-        with _on(stream):
-            hosting = torch.empty(d, dtype=torch.int32, device=dev)
-            b2i = torch.empty(d, dtype=torch.int32, device=dev)
-            info = torch.empty(4, dtype=torch.int64, device=dev)
+        if out is None:
+            with _on(stream):
+                out = (torch.empty(d, dtype=torch.int32, device=dev),
+                       torch.empty(d, dtype=torch.int32, device=dev),
+                       torch.empty(4, dtype=torch.int64, device=dev))
+        hosting, b2i, info = out
         b = bal.struct()
         _check(lib().orch_nodewise(self.h, C.c_int32(d), C.c_int32(c), C.c_int64(length.numel()),
                                    _ptr(length), _ptr(origin), C.byref(b), _ptr(hosting),
@@ -534,8 +538,9 @@ class Context:
     def layout(self, d, P, length, origin, bal: Balance, out: Layout | None = None,
                stream=None) -> Layout:
         n = length.numel()
-        with _on(stream):
-            out = out or Layout.alloc(P, n, length.device)
+        if out is None:
+            with _on(stream):
+                out = Layout.alloc(P, n, length.device)
         b, lo = bal.struct(), out.struct()
         _check(lib().orch_layout(self.h, C.c_int32(d), C.c_int32(P), C.c_int64(n), _ptr(length),
                                  _ptr(origin), C.byref(b), C.byref(lo), _stream(stream)))

@@ -9,8 +9,6 @@
 //   K5 padded search       Alg.2 GetLeastBatches + search      (balancers.cpp:111-143)
 //   K6 quadratic tolerance champion scan                       (balancers.cpp:210-233)
 //   K7 k_bin_cost/k_decide cost(), objective, never_worse      (balancers.cpp:43-76)
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstring>
@@ -20,6 +18,7 @@
 #include "balance_small.cuh"
 #include "greedy_lpt.cuh"
 #include "plan.cuh"
+#include "radix.cuh"
 
 namespace orchb {
 
@@ -152,7 +151,6 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   const bool padded_only = mode >= 2;
   const bool needs_desc = !identity_only && !padded_only && kind != ORCH_BINARY_PADDED;
   const bool needs_asc = padded_only || (!identity_only && kind == ORCH_BINARY_PADDED);
-  const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
 
   // quadratic tolerance and ConvTransformer keep one batch per lane (d <= 32)
@@ -229,7 +227,6 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   int32_t *dest_inst, *dest_slot, *src_slot, *bin_count, *bin_offset, *bin_member, *a_count;
   int64_t *src_off, *dst_off, *bin_len, *bin_tokens, *a_tokens;
   double* bin_cost;
-  void* cub_tmp;
   plan.add(&flags, 1);
   plan.add(&key_len, nn);
   plan.add(&key_org, nn);
@@ -290,21 +287,17 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   plan.add(&lpt_bin, lpt ? nn : 1);
   plan.add(&lpt_slot, lpt ? nn : 1);
   plan.add(&lpt_off, lpt ? nn : 1);
-  // CUB temporary storage (max over the calls below)
-  size_t cub_bytes = 0, b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b, key_org, sorted_org, iota, ident_order, (int)nn, 0,
-                                  obits, st);
-  cub_bytes = std::max(cub_bytes, b);
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, b, key_len, xs, iota, order, (int)nn, 0, 32,
-                                            st);
-  cub_bytes = std::max(cub_bytes, b);
-  cub::DeviceRadixSort::SortPairs(nullptr, b, key_len, xs, iota, order, (int)nn, 0, 32, st);
-  cub_bytes = std::max(cub_bytes, b);
-  cub::DeviceScan::ExclusiveSum(nullptr, b, ident_len, ident_prefix, (int)nn + 1, st);
-  cub_bytes = std::max(cub_bytes, b);
-  cub::DeviceScan::ExclusiveSum(nullptr, b, ident_count, ident_offset, d + 1, st);
-  cub_bytes = std::max(cub_bytes, b);
-  plan.add(reinterpret_cast<char**>(&cub_tmp), cub_bytes);
+  // radix sort / scan scratch (radix.cuh)
+  uint32_t *rs_kt, *rs_hist;
+  int32_t *rs_vt, *scan32_part;
+  int64_t* scan64_part;
+  RsState* rs_state;
+  plan.add(&rs_kt, nn);
+  plan.add(&rs_vt, nn);
+  plan.add(&rs_hist, rs_hist_words(static_cast<int64_t>(nn)));
+  plan.add(&rs_state, 1);
+  plan.add(&scan64_part, static_cast<size_t>(rs_tiles(static_cast<int64_t>(nn) + 1)));
+  plan.add(&scan32_part, static_cast<size_t>(rs_tiles(static_cast<int64_t>(d) + 1)));
   int rc = plan.commit(ctx, st);
   if (rc) return rc;
 
@@ -321,20 +314,20 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
 
   // ---- identity (origin) batches: always needed (never_worse)
   if (n > 0) {
-    size_t tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key_org, sorted_org, iota,
-                                                  ident_order, (int)n, 0, obits, st));
+    rc = rs_sort_pairs(ctx, key_org, iota, sorted_org, ident_order, rs_kt, rs_vt, n, false,
+                       rs_hist, rs_state, st);
+    if (rc) return rc;
     launch(ctx, [&] {
       k_ident_count<<<gb, kThreads, 0, st>>>(n, ident_order, origin, len, ident_count, ident_len, S);
     });
   }
   {
-    size_t tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ident_count, ident_offset, d + 1, st));
+    rc = rs_exclusive_scan<int32_t>(ctx, ident_count, ident_offset, d + 1, scan32_part, st);
+    if (rc) return rc;
   }
   if (n > 0) {
-    size_t tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ident_len, ident_prefix, (int)n + 1, st));
+    rc = rs_exclusive_scan<int64_t>(ctx, ident_len, ident_prefix, n + 1, scan64_part, st);
+    if (rc) return rc;
     launch(ctx, [&] {
       k_ident_slots<<<gb, kThreads, 0, st>>>(n, ident_order, origin, ident_offset, ident_prefix,
                                              src_slot, src_off, S);
@@ -348,18 +341,17 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
 
   // ---- the balancer's own packing
   if (needs_desc && n > 0) {
-    size_t tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(cub_tmp, tb, key_len, xs, iota, order,
-                                                            (int)n, 0, 32, st));
+    rc = rs_sort_pairs(ctx, key_len, iota, xs, order, rs_kt, rs_vt, n, true, rs_hist, rs_state, st);
+    if (rc) return rc;
   }
   if (needs_asc) {
-    size_t tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, key_len, xs, iota, order, (int)n, 0,
-                                                  32, st));
+    rc = rs_sort_pairs(ctx, key_len, iota, xs, order, rs_kt, rs_vt, n, false, rs_hist, rs_state,
+                       st);
+    if (rc) return rc;
     launch(ctx, [&] { k_u32_to_i64<<<gb, kThreads, 0, st>>>(n, xs, asc_len); });
     ORCH_CUDA_TRY(cudaMemsetAsync(asc_len + n, 0, sizeof(int64_t), st));
-    tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, asc_len, asc_prefix, (int)n + 1, st));
+    rc = rs_exclusive_scan<int64_t>(ctx, asc_len, asc_prefix, n + 1, scan64_part, st);
+    if (rc) return rc;
     const bool use_nx = n <= kNxMax;
     const int nx_smem = static_cast<int>(n) * 2;
     static PerDeviceOnce pad_configured;
@@ -445,8 +437,8 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
                          lpt_slot, lpt_off);
       if (rc) return rc;
     }
-    size_t tb = cub_bytes;
-    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, a_count, bin_offset, d + 1, st));
+    rc = rs_exclusive_scan<int32_t>(ctx, a_count, bin_offset, d + 1, scan32_part, st);
+    if (rc) return rc;
     if (n > 0)
       launch(ctx, [&] {
         k_scatter_members<<<gb, kThreads, 0, st>>>(n, dest_inst, dest_slot, bin_offset,

@@ -16,8 +16,6 @@
 //  * the quadratic-tolerance champion scan keeps (sum, square sum) in lanes.
 #pragma once
 
-#include <cub/block/block_radix_sort.cuh>
-#include <cub/block/block_scan.cuh>
 
 #include "balance_kernels.cuh"
 
@@ -71,8 +69,6 @@ template <int ITEMS>
 struct SmallSmem {
   static constexpr int NS = kSmallThreads * ITEMS;
   static constexpr int NCH = NS / 32;  // 32-item chunks of the identity ranking
-  using Sort = cub::BlockRadixSort<uint32_t, kSmallThreads, ITEMS, int32_t>;
-  using Scan = cub::BlockScan<int64_t, kSmallThreads>;
   int64_t len[NS];
   int64_t pfx[NS + 1];  // exclusive prefix of lengths in identity order, then in policy order
   int32_t org[NS];
@@ -86,9 +82,14 @@ struct SmallSmem {
   uint8_t chunk_cnt[kSmallMaxD][NCH + 4];    // lanes of one chunk hit different banks)
   uint8_t a_dest[NS];
   uint8_t g_bin[NS + 1];  // greedy: bin per sorted position (g_slot = id_rank, g_off = pfx)
+  struct SortTmp {  // block_sort_pairs: the other half of the key / value ping-pong
+    uint32_t k[NS];
+    int32_t v[NS];
+    uint16_t hist[256 * kSmallWarps];  // [digit][warp]
+  };
   union {
-    typename Sort::TempStorage sort;
-    typename Scan::TempStorage scan;
+    SortTmp sort;
+    int64_t wsum[kSmallWarps];  // block_exclusive_sum
   } tmp;
   int32_t cnt_id[kSmallMaxD + 1], off_id[kSmallMaxD + 1];
   int32_t cnt_a[kSmallMaxD + 1], off_a[kSmallMaxD + 1];
@@ -315,6 +316,126 @@ __device__ __forceinline__ void block_max_total(SmallSmem<ITEMS>& S, int64_t mx,
   }
 }
 
+// Exclusive sum over the block of ITEMS values per thread (blocked order:
+// thread t holds elements t * ITEMS + j); agg = the total. Caller syncs before
+// reusing wsum.
+template <int ITEMS>
+__device__ __forceinline__ void block_exclusive_sum(int64_t (&v)[ITEMS], int64_t* wsum,
+                                                    int64_t& agg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) s += v[j];
+  int64_t incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t u = __shfl_up_sync(~0u, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int64_t before = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kSmallWarps; ++w) {
+    const int64_t x = wsum[w];
+    before += w < warp ? x : 0;
+    total += x;
+  }
+  int64_t ex = before + incl - s;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int64_t x = v[j];
+    v[j] = ex;
+    ex += x;
+  }
+  agg = total;
+}
+
+// Stable block LSD radix sort of the first `ns` slots of (kin, vin), 8-bit
+// digits over bits [0, bits): each warp owns 32 * ITEMS consecutive slots,
+// ranks its digits with __match_any_sync against per-warp counters, and a
+// scan over (digit, warp) gives every slot its position. desc: digit' = 255 -
+// digit (descending, equal keys keep their order). The result ends in
+// (kout, vout); (kt, vt) is the other half of the ping-pong.
+template <int ITEMS>
+__device__ void block_sort_pairs(uint32_t* kin, int32_t* vin, uint32_t* kout, int32_t* vout,
+                                 uint32_t* kt, int32_t* vt, uint16_t* hist, int bits, bool desc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int passes = bits > 0 ? (bits + 7) / 8 : 1;
+  // odd pass count: start in (kin -> kout), even: (kin -> kt -> kout)
+  uint32_t* ks = kin;
+  int32_t* vs = vin;
+  for (int p = 0; p < passes; ++p) {
+    const bool last = p == passes - 1;
+    uint32_t* kd = last ? kout : ((passes - p) % 2 == 0 ? kt : kout);
+    int32_t* vd = last ? vout : ((passes - p) % 2 == 0 ? vt : vout);
+    for (int i = threadIdx.x; i < 256 * kSmallWarps; i += kSmallThreads) hist[i] = 0;
+    __syncthreads();
+    uint32_t key[ITEMS];
+    int32_t val[ITEMS];
+    int dig[ITEMS], rank[ITEMS];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int i = warp * 32 * ITEMS + j * 32 + lane;
+      key[j] = ks[i];
+      val[j] = vs[i];
+      const int dg = static_cast<int>((key[j] >> (8 * p)) & 255u);
+      dig[j] = desc ? 255 - dg : dg;
+    }
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const unsigned peers = __match_any_sync(~0u, dig[j]);
+      const int before = __popc(peers & lt);
+      uint16_t* h = hist + dig[j] * kSmallWarps + warp;
+      const int run = *h;
+      rank[j] = run + before;
+      __syncwarp();
+      if (before == 0) *h = static_cast<uint16_t>(run + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive scan over hist[digit][warp], 8 entries per thread
+      static_assert(256 * kSmallWarps == 8 * kSmallThreads, "8 counters per thread");
+      __shared__ uint32_t ws[kSmallWarps];
+      uint32_t v[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[q] = hist[8 * threadIdx.x + q];
+        sum += v[q];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(~0u, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) ws[warp] = incl;
+      __syncthreads();
+      uint32_t before = 0;
+#pragma unroll
+      for (int w = 0; w < kSmallWarps; ++w) before += w < warp ? ws[w] : 0u;
+      uint32_t ex = before + incl - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        hist[8 * threadIdx.x + q] = static_cast<uint16_t>(ex);
+        ex += v[q];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int pos = hist[dig[j] * kSmallWarps + warp] + rank[j];
+      ORCH_DCHECK(pos < kSmallThreads * ITEMS);
+      kd[pos] = key[j];
+      vd[pos] = val[j];
+    }
+    __syncthreads();
+    ks = kd;
+    vs = vd;
+  }
+}
+
 template <int ITEMS>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -443,7 +564,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       v[j] = k < n ? S.len[S.ord_id[k]] : 0;
     }
     int64_t agg;
-    typename SS::Scan(S.tmp.scan).ExclusiveSum(v, v, agg);
+    block_exclusive_sum<ITEMS>(v, S.tmp.wsum, agg);
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) S.pfx[tid * ITEMS + j] = v[j];
     if (tid == 0) S.pfx[SS::NS] = agg;
@@ -469,6 +590,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
       if (tid < n) {
         const uint32_t ki = static_cast<uint32_t>(S.len[tid]);
         int r = 0;
+#pragma unroll 8
         for (int j = 0; j < n; ++j) {
           const uint32_t kj = static_cast<uint32_t>(S.len[j]);
           r += (asc ? kj < ki : kj > ki) || (kj == ki && j < tid);
@@ -478,24 +600,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         S.xs[r] = ki;
       }
     } else {
-      uint32_t keys[ITEMS];
-      int32_t vals[ITEMS];
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
-        const int i = tid * ITEMS + j;
-        keys[j] = i < n ? static_cast<uint32_t>(S.len[i]) : (asc ? pad_asc : 0u);
-        vals[j] = i;
-      }
+      // stage the keys (padding slots sort last) and sort into (S.xs, S.ord)
       __syncthreads();  // tmp storage reuse
-      if (asc)
-        typename SS::Sort(S.tmp.sort).Sort(keys, vals, 0, lbits);
-      else
-        typename SS::Sort(S.tmp.sort).SortDescending(keys, vals, 0, lbits);
-#pragma unroll
-      for (int j = 0; j < ITEMS; ++j) {
-        S.ord[tid * ITEMS + j] = vals[j];
-        S.xs[tid * ITEMS + j] = keys[j];
+      uint32_t* kst = S.tmp.sort.k;
+      int32_t* vst = S.tmp.sort.v;
+      for (int i = tid; i < SS::NS; i += kSmallThreads) {
+        kst[i] = i < n ? static_cast<uint32_t>(S.len[i]) : (asc ? pad_asc : 0u);
+        vst[i] = i;
       }
+      __syncthreads();
+      block_sort_pairs<ITEMS>(kst, vst, S.xs, S.ord, kst, vst, S.tmp.sort.hist, lbits, !asc);
     }
     __syncthreads();
     SMALL_MARK(3);
@@ -668,7 +782,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         }
         int64_t agg;
         __syncthreads();
-        typename SS::Scan(S.tmp.scan).ExclusiveSum(v, v, agg);
+        block_exclusive_sum<ITEMS>(v, S.tmp.wsum, agg);
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) S.pfx[tid * ITEMS + j] = v[j];

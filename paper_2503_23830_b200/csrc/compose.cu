@@ -15,12 +15,12 @@
 //                          orch_layout / orch_dispatch / orch_put move its rows.
 // Composition and inversion of flat rearrangements are argument swaps: the
 // encoder result's (dest_inst, dest_slot) is the composed move's source.
-#include <cub/device/device_scan.cuh>
 
 #include <string>
 
 #include "common.cuh"
 #include "plan.cuh"
+#include "radix.cuh"
 
 namespace orchb {
 namespace {
@@ -188,19 +188,16 @@ int orch_rearrange(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
   Plan plan;
   RrFlags* f;
   int32_t *scnt, *dcnt;
-  int64_t *glen, *spfx, *dpfx;
-  void* tmp;
+  int64_t *glen, *spfx, *dpfx, *part64;
+  int32_t* part32;
   plan.add(&f, 1);
   plan.add(&scnt, d + 1);
   plan.add(&dcnt, d + 1);
   plan.add(&glen, nn + 1);
   plan.add(&spfx, nn + 1);
   plan.add(&dpfx, nn + 1);
-  size_t tb = 0, t2 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, scnt, out->src_offset, d + 1, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, t2, glen, spfx, static_cast<int>(nn) + 1, st);
-  tb = tb > t2 ? tb : t2;
-  plan.add(reinterpret_cast<char**>(&tmp), tb);
+  plan.add(&part64, static_cast<size_t>(rs_tiles(static_cast<int64_t>(nn) + 1)));
+  plan.add(&part32, static_cast<size_t>(rs_tiles(static_cast<int64_t>(d) + 1)));
   int rc = plan.commit(ctx, st);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaMemsetAsync(f, 0, sizeof(RrFlags), st));
@@ -211,10 +208,10 @@ int orch_rearrange(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
   ORCH_CUDA_TRY(cudaMemsetAsync(glen + n, 0, 8, st));
   const int gb = blocks_for(n, kT);
   if (n > 0) k_rr_count<<<gb, kT, 0, st>>>(d, n, d_src_inst, d_dst_inst, scnt, dcnt, f);
-  size_t t = tb;
-  ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t, scnt, out->src_offset, d + 1, st));
-  t = tb;
-  ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t, dcnt, out->bin_offset, d + 1, st));
+  rc = rs_exclusive_scan<int32_t>(ctx, scnt, out->src_offset, d + 1, part32, st);
+  if (rc) return rc;
+  rc = rs_exclusive_scan<int32_t>(ctx, dcnt, out->bin_offset, d + 1, part32, st);
+  if (rc) return rc;
   if (n > 0) {
     k_rr_scatter<<<gb, kT, 0, st>>>(d, n, d_dst_inst, d_dst_slot, out->bin_offset,
                                     out->bin_member, &f->dup_dst);
@@ -230,8 +227,8 @@ int orch_rearrange(orch_ctx* ctx, int32_t d, int64_t n, const int64_t* d_len,
   for (int side = 0; side < 2; ++side) {
     if (n > 0)
       k_rr_gather_len<<<gb, kT, 0, st>>>(n, mem[side], d_len, glen);
-    t = tb;
-    ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t, glen, pfx[side], static_cast<int>(n) + 1, st));
+    rc = rs_exclusive_scan<int64_t>(ctx, glen, pfx[side], n + 1, part64, st);
+    if (rc) return rc;
     if (n > 0) k_rr_offsets<<<gb, kT, 0, st>>>(n, mem[side], ins[side], offs[side], pfx[side], tok[side]);
   }
   k_rr_finish<<<blocks_for(n > d ? n : d, kT), kT, 0, st>>>(
@@ -254,16 +251,13 @@ int orch_backbone_targets(orch_ctx* ctx, int32_t d, int64_t E, const int32_t* d_
   Plan plan;
   int32_t* part_example;
   uint8_t* in_u;
-  int64_t *cnt, *pfx, *base;
-  void* tmp;
+  int64_t *cnt, *pfx, *base, *part;
   plan.add(&part_example, pp);
   plan.add(&in_u, pp);
   plan.add(&cnt, ee + 1);
   plan.add(&pfx, ee + 1);
   plan.add(&base, ee);
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, pfx, static_cast<int>(ee) + 1, st);
-  plan.add(reinterpret_cast<char**>(&tmp), tb);
+  plan.add(&part, static_cast<size_t>(rs_tiles(static_cast<int64_t>(ee) + 1)));
   int rc = plan.commit(ctx, st);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaMemsetAsync(in_u, 0, pp, st));
@@ -272,7 +266,8 @@ int orch_backbone_targets(orch_ctx* ctx, int32_t d, int64_t E, const int32_t* d_
   if (n > 0) k_bt_mark<<<blocks_for(n, kT), kT, 0, st>>>(n, d_item_part, in_u);
   if (E > 0)
     k_bt_count<<<blocks_for(E, kT), kT, 0, st>>>(E, d_llm_bin_member, d_part_offset, in_u, cnt);
-  ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, pfx, static_cast<int>(E) + 1, st));
+  rc = rs_exclusive_scan<int64_t>(ctx, cnt, pfx, E + 1, part, st);
+  if (rc) return rc;
   if (E > 0)
     k_bt_base<<<blocks_for(E, kT), kT, 0, st>>>(E, d_llm_bin_member, d_llm_bin_offset,
                                                 d_llm_dest_inst, pfx, base);

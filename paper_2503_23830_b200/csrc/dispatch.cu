@@ -4,8 +4,6 @@
 // on bf16 token rows: every item is a contiguous run of len rows in its origin
 // rank's input buffer and lands as a contiguous run in its destination rank's
 // output buffer; off-rank runs travel through one grouped NCCL send/recv.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <nccl.h>
 
 #include <algorithm>
@@ -16,6 +14,7 @@
 
 #include "balance_kernels.cuh"
 #include "plan.cuh"
+#include "radix.cuh"
 
 struct orch_comm {
   ncclComm_t comm = nullptr;
@@ -1668,20 +1667,19 @@ int orch_group_by_origin(orch_ctx* ctx, int32_t d, int64_t n, const int32_t* d_o
   if (d < 1) return fail(ORCH_INVALID_ARGUMENT, "instance count must be >= 1");
   auto st = static_cast<cudaStream_t>(stream);
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
-  const int obits = std::max(1u, ceil_log2(static_cast<unsigned long long>(d)));
   Plan plan;
-  uint32_t *k_in, *k_out;
-  int32_t *iota, *cnt;
-  void* tmp;
+  uint32_t *k_in, *k_out, *rs_kt, *rs_hist;
+  int32_t *iota, *cnt, *rs_vt, *part;
+  RsState* rs_state;
   plan.add(&k_in, nn);
   plan.add(&k_out, nn);
   plan.add(&iota, nn);
   plan.add(&cnt, d + 1);
-  size_t tb = 0, b2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, iota, d_bin_member, (int)nn, 0, obits, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, b2, cnt, d_bin_offset, d + 1, st);
-  tb = std::max(tb, b2);
-  plan.add(reinterpret_cast<char**>(&tmp), tb);
+  plan.add(&rs_kt, nn);
+  plan.add(&rs_vt, nn);
+  plan.add(&rs_hist, rs_hist_words(static_cast<int64_t>(nn)));
+  plan.add(&rs_state, 1);
+  plan.add(&part, static_cast<size_t>(rs_tiles(static_cast<int64_t>(d) + 1)));
   int rc = plan.commit(ctx, st);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (d + 1), st));
@@ -1689,12 +1687,12 @@ int orch_group_by_origin(orch_ctx* ctx, int32_t d, int64_t n, const int32_t* d_o
     launch(ctx, [&] {
       k_origin_keys<<<blocks_for(n, kThreads), kThreads, 0, st>>>(d, n, d_origin, k_in, iota, cnt);
     });
-    size_t t = tb;
-    ORCH_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, t, k_in, k_out, iota, d_bin_member, (int)n,
-                                                  0, obits, st));
+    rc = rs_sort_pairs(ctx, k_in, iota, k_out, d_bin_member, rs_kt, rs_vt, n, false, rs_hist,
+                       rs_state, st);
+    if (rc) return rc;
   }
-  size_t t = tb;
-  ORCH_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, t, cnt, d_bin_offset, d + 1, st));
+  rc = rs_exclusive_scan<int32_t>(ctx, cnt, d_bin_offset, d + 1, part, st);
+  if (rc) return rc;
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
 }

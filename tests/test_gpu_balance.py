@@ -308,3 +308,29 @@ def test_reference_library_agrees(ctx, reflib):
             np.testing.assert_array_equal(b.dest_inst[:n].cpu().numpy(), di)
             np.testing.assert_array_equal(b.dest_slot[:n].cpu().numpy(), ds)
             assert np.float64(b.summary().objective).tobytes() == np.float64(obj).tobytes()
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_radix_passes_and_tiles(ctx, oracle, kind):
+    """The hand-written device radix sort (radix.cuh) on the multi-kernel path:
+    several 4096-item tiles, lengths needing 2 and 4 passes (below and above
+    2^16), heavy ties (stability), origins spanning d up to 4096 (two passes)."""
+    rng = np.random.default_rng(4000 + kind)
+    for d, n, hi in [(100, 9000, 200), (1500, 20000, 1 << 20), (4096, 12000, 70000),
+                     (80, 5000, 3)]:
+        length, origin = random_instance(rng, d, n, 1, hi)
+        b = gpu_balance(ctx, kind, d, length, origin, lam=1e-6, v=100)
+        o = oracle.balance(kind, d, length, origin, lam=1e-6, v=100)
+        check_same(b, o, n, d)
+
+
+def test_group_by_origin_tiles(ctx):
+    """orch_group_by_origin: the stable order by origin over many tiles."""
+    rng = np.random.default_rng(77)
+    for d, n in [(4096, 100000), (7, 50000), (300, 4097)]:
+        origin = rng.integers(0, d, n).astype(np.int32)
+        off, mem = ctx.group_by_origin(d, torch.from_numpy(origin).cuda())
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(mem.cpu().numpy(), np.argsort(origin, kind="stable"))
+        np.testing.assert_array_equal(off.cpu().numpy(),
+                                      np.concatenate([[0], np.cumsum(np.bincount(origin, minlength=d))]))
