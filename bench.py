@@ -7,9 +7,11 @@ per instance from the reference's synthetic MCI generator, per-phase
 rebalancing (vision encoder phase on metadata lengths, LLM phase on
 interleaved lengths, GreedyUnpadded), bf16 d_model=4096 token rows (8 KiB).
 Per phase: [all-gather of lengths] -> cost model + ordering + greedy
-assignment + never-worse (one balance call) -> send/recv layout -> pack ->
-[NCCL grouped send/recv] -> unpack. At N GPUs the 8 instances are spread
-8/N per GPU (strong scaling: the job is fixed).
+assignment + never-worse (one balance call) -> [node-wise hosting] -> send/recv
+layout -> row movement. At N GPUs the 8 instances are spread 8/N per GPU
+(strong scaling: the job is fixed); the rows move by the fused pack+put into
+the peers' windows (window barrier + release per step) or, with
+--exchange nccl, by pack -> grouped ncclSend/ncclRecv -> unpack.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
@@ -30,6 +32,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the data, metadata and per-phase streams each get a hardware queue: a kernel that
+# waits for a peer (window barrier, gather) must never sit in front of another
+# stream's work in a shared queue (set before CUDA initialises)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 METRIC = "balance+dispatch tokens/s at 1–8 B200; a2a GB/s vs NVLink; max/mean load"

@@ -169,6 +169,108 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_scatter(
   }
 }
 
+// The whole sort of n <= kRsTile items in one CTA (shared memory ping-pong):
+// one launch instead of a hist / scatter pair per pass.
+struct RsTileSmem {
+  uint32_t k[2][kRsTile];
+  int32_t v[2][kRsTile];
+  uint16_t hist[256 * kRsWarps];  // [digit][warp]
+  uint32_t ws[kRsWarps];
+  unsigned mx;
+};
+
+__global__ void __launch_bounds__(kRsThreads, 1)
+    k_rs_sort_tile(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
+                   uint32_t* __restrict__ kout, int32_t* __restrict__ vout, int n, bool desc) {
+  extern __shared__ __align__(16) unsigned char rs_raw[];
+  RsTileSmem& S = *reinterpret_cast<RsTileSmem*>(rs_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) S.mx = 0;
+  __syncthreads();
+  unsigned mx = 0;
+  for (int i = t; i < kRsTile; i += kRsThreads) {
+    const uint32_t k = i < n ? kin[i] : 0u;
+    S.k[0][i] = k;
+    S.v[0][i] = i < n ? vin[i] : 0;
+    mx = k > mx ? k : mx;
+  }
+  mx = __reduce_max_sync(~0u, mx);
+  if (lane == 0) atomicMax(&S.mx, mx);
+  __syncthreads();
+  const unsigned kmax = S.mx;
+  const int passes = kmax < 256u ? 1 : kmax < 65536u ? 2 : kmax < (1u << 24) ? 3 : 4;
+  const unsigned lt = (1u << lane) - 1u;
+  int cur = 0;
+  for (int p = 0; p < passes; ++p) {
+    for (int i = t; i < 256 * kRsWarps; i += kRsThreads) S.hist[i] = 0;
+    __syncthreads();
+    uint32_t key[kRsPer];
+    int32_t val[kRsPer];
+    int dig[kRsPer], rank[kRsPer];
+#pragma unroll
+    for (int j = 0; j < kRsPer; ++j) {
+      const int i = warp * 32 * kRsPer + j * 32 + lane;
+      key[j] = S.k[cur][i];
+      val[j] = S.v[cur][i];
+      dig[j] = i < n ? rs_digit(key[j], 8 * p, desc) : 256;  // padding sorts last
+    }
+#pragma unroll
+    for (int j = 0; j < kRsPer; ++j) {
+      const unsigned peers = __match_any_sync(~0u, dig[j]);
+      const int before = __popc(peers & lt);
+      int run = 0;
+      if (dig[j] < 256) run = S.hist[dig[j] * kRsWarps + warp];
+      rank[j] = run + before;
+      __syncwarp();
+      if (dig[j] < 256 && before == 0)
+        S.hist[dig[j] * kRsWarps + warp] = static_cast<uint16_t>(run + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive scan over hist[digit][warp], 8 counters per thread
+      static_assert(256 * kRsWarps == 8 * kRsThreads, "8 counters per thread");
+      uint32_t v[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[q] = S.hist[8 * t + q];
+        sum += v[q];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(~0u, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) S.ws[warp] = incl;
+      __syncthreads();
+      uint32_t before = 0;
+#pragma unroll
+      for (int w = 0; w < kRsWarps; ++w) before += w < warp ? S.ws[w] : 0u;
+      uint32_t ex = before + incl - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        S.hist[8 * t + q] = static_cast<uint16_t>(ex);
+        ex += v[q];
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < kRsPer; ++j) {
+      if (dig[j] == 256) continue;
+      const int pos = S.hist[dig[j] * kRsWarps + warp] + rank[j];
+      ORCH_DCHECK(pos < n);
+      S.k[cur ^ 1][pos] = key[j];
+      S.v[cur ^ 1][pos] = val[j];
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  for (int i = t; i < n; i += kRsThreads) {
+    kout[i] = S.k[cur][i];
+    vout[i] = S.v[cur][i];
+  }
+}
+
 // Exclusive scan of int32 / int64 counts: out[i] = sum of in[0, i). Tiles of
 // 4096 elements: k_scan_partial sums every tile, k_scan_tiles scans each tile
 // on top of the sum of the tiles before it (read from the partial sums).
@@ -251,6 +353,20 @@ inline int rs_sort_pairs(orch_ctx* ctx, const uint32_t* kin, const int32_t* vin,
                          int32_t* vout, uint32_t* kt, int32_t* vt, int64_t n, bool desc,
                          uint32_t* hist, RsState* st, cudaStream_t s) {
   if (n <= 0) return ORCH_OK;
+  if (n <= kRsTile) {  // one CTA sorts everything in shared memory
+    static PerDeviceOnce configured;
+    const int rc = configured([&]() -> int {
+      ORCH_CUDA_TRY(cudaFuncSetAttribute(k_rs_sort_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(RsTileSmem))));
+      return ORCH_OK;
+    });
+    if (rc) return rc;
+    k_rs_sort_tile<<<1, kRsThreads, sizeof(RsTileSmem), s>>>(kin, vin, kout, vout,
+                                                              static_cast<int>(n), desc);
+    ctx->launches += 1;
+    ORCH_CUDA_TRY(cudaGetLastError());
+    return ORCH_OK;
+  }
   const int tiles = rs_tiles(n);
   ORCH_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(RsState), s));
   const uint32_t* ki[4] = {kin, kt, kout, kt};
@@ -273,9 +389,12 @@ inline int rs_exclusive_scan(orch_ctx* ctx, const T* in, T* out, int64_t count, 
                              cudaStream_t s) {
   if (count <= 0) return ORCH_OK;
   const int tiles = rs_tiles(count);
-  k_scan_partial<T><<<tiles, kRsThreads, 0, s>>>(in, count, part);
+  if (tiles > 1) {  // one tile needs no partial sums (nothing before it)
+    k_scan_partial<T><<<tiles, kRsThreads, 0, s>>>(in, count, part);
+    ctx->launches += 1;
+  }
   k_scan_tiles<T><<<tiles, kRsThreads, 0, s>>>(in, out, count, part);
-  ctx->launches += 2;
+  ctx->launches += 1;
   ORCH_CUDA_TRY(cudaGetLastError());
   return ORCH_OK;
 }

@@ -3,6 +3,12 @@
 import os
 import sys
 
+# The emulated-rank tests run several ranks' spinning kernels (window barriers,
+# gathers) on one GPU, one stream per rank: give every stream its own hardware
+# queue so no kernel waits behind another stream's blocked one (set before CUDA
+# initialises).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 import pytest
 
