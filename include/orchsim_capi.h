@@ -461,7 +461,9 @@ int orch_put_at(orch_ctx* ctx, orch_comm* comm, int32_t d, int64_t n, const int6
  * windows of such communicators at once, each rank's peers being the other
  * windows' device buffers. Puts, window barriers, releases and the gather
  * window then run the same kernels as across GPUs; each emulated rank needs
- * its own stream (a barrier waits for the other ranks' kernels). */
+ * its own stream (a barrier waits for the other ranks' kernels). A rank's
+ * window lives on the device current when its loopback communicator was
+ * created, so one process can also drive P GPUs (peer access over NVLink). */
 int orch_comm_create_local(int32_t nranks, int32_t rank, orch_comm** out);
 int orch_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t nranks, size_t bytes,
                              orch_window** out /* [nranks] */);

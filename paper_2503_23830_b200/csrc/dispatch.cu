@@ -1951,12 +1951,16 @@ int window_publish_peers(orch_window* w) {
 }
 
 void window_free(orch_window* w) {
+  int dev0 = 0;
+  cudaGetDevice(&dev0);
+  cudaSetDevice(w->comm->device);
   if (!w->loopback)
     for (int q = 0; q < static_cast<int>(w->peers.size()); ++q)
       if (q != w->comm->rank && w->peers[q]) cudaIpcCloseMemHandle(w->peers[q]);
   if (w->peers_dev) cudaFree(w->peers_dev);
   if (w->base) cudaFree(w->base);
   delete w;
+  cudaSetDevice(dev0);
 }
 
 // What every rank contributes to the window set-up all-gather.
@@ -2042,24 +2046,41 @@ int orch_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t P, 
     if (!comms[r] || !comms[r]->loopback || comms[r]->size != P || comms[r]->rank != r)
       return fail(ORCH_INVALID_ARGUMENT,
                   "orch_window_create_local needs loopback communicators of ranks 0..P-1");
+  // Each rank's window lives on the device its loopback communicator was made
+  // on: one device (all ranks on one GPU) or one per rank (several GPUs driven
+  // by one process, peers reached over NVLink through peer access).
+  int dev0 = 0;
+  ORCH_CUDA_TRY(cudaGetDevice(&dev0));
   std::vector<orch_window*> ws(P, nullptr);
-  for (int r = 0; r < P; ++r) {
-    int rc = window_alloc(comms[r], bytes, &ws[r]);
-    if (rc) {
-      for (int q = 0; q < r; ++q) window_free(ws[q]);
-      return rc;
-    }
-    ws[r]->loopback = true;
+  int rc = ORCH_OK;
+  for (int r = 0; r < P && !rc; ++r) {
+    ORCH_CUDA_TRY(cudaSetDevice(comms[r]->device));
+    rc = window_alloc(comms[r], bytes, &ws[r]);
+    if (!rc) ws[r]->loopback = true;
   }
-  for (int r = 0; r < P; ++r) {
-    for (int q = 0; q < P; ++q) ws[r]->peers[q] = ws[q]->base;
-    int rc = window_publish_peers(ws[r]);
-    if (rc) {
-      for (int q = 0; q < P; ++q) window_free(ws[q]);
-      return rc;
+  for (int r = 0; r < P && !rc; ++r) {
+    ORCH_CUDA_TRY(cudaSetDevice(comms[r]->device));
+    for (int q = 0; q < P; ++q) {
+      ws[r]->peers[q] = ws[q]->base;
+      if (comms[q]->device != comms[r]->device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(comms[q]->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          rc = fail(ORCH_CUDA_ERROR, std::string("peer access: ") + cudaGetErrorString(e));
+        cudaGetLastError();  // clear "already enabled"
+      }
     }
+    if (!rc) rc = window_publish_peers(ws[r]);
   }
-  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  for (int r = 0; r < P && !rc; ++r) {
+    ORCH_CUDA_TRY(cudaSetDevice(comms[r]->device));
+    ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  }
+  cudaSetDevice(dev0);
+  if (rc) {
+    for (int q = 0; q < P; ++q)
+      if (ws[q]) window_free(ws[q]);
+    return rc;
+  }
   for (int r = 0; r < P; ++r) out[r] = ws[r];
   return ORCH_OK;
 }
@@ -2106,7 +2127,11 @@ int orch_window_destroy(orch_window* w) {
   int rc = ORCH_OK;
   // every rank must be done writing into / reading from the windows
   if (!w->loopback) rc = orch_barrier(w->comm, nullptr);
+  int dev0 = 0;
+  cudaGetDevice(&dev0);
+  cudaSetDevice(w->comm->device);
   cudaDeviceSynchronize();
+  cudaSetDevice(dev0);
   window_free(w);
   return rc;
 }
@@ -2240,11 +2265,15 @@ int orch_gather_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int3
   std::vector<orch_window*> ws(P, nullptr);
   int rc = orch_window_create_local(ctx, comms, P, gather_window_bytes(max_n, P), ws.data());
   if (rc) return rc;
+  int dev0 = 0;
+  ORCH_CUDA_TRY(cudaGetDevice(&dev0));
   for (int r = 0; r < P; ++r) {
+    ORCH_CUDA_TRY(cudaSetDevice(comms[r]->device));
     rc = gather_window_wrap(ws[r], max_n, &out[r]);
     if (rc) return rc;
+    ORCH_CUDA_TRY(cudaDeviceSynchronize());
   }
-  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  ORCH_CUDA_TRY(cudaSetDevice(dev0));
   return ORCH_OK;
 }
 

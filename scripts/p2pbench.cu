@@ -19,7 +19,7 @@
 // median of 5 repetitions after 2 warm-ups.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o p2pbench scripts/p2pbench.cu
-//   ./p2pbench [MiB per GPU, default 1024]
+//   ./p2pbench [MiB per GPU, default 1024] [method] [pattern]   (one combination only)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -186,15 +186,18 @@ int main(int argc, char** argv) {
     CK(cudaDeviceSynchronize());
   }
   g_comms.resize(ngpu);
-  if (ncclCommInitAll(g_comms.data(), ngpu, nullptr) != ncclSuccess) {
+  if ((argc <= 2 || std::string(argv[2]) == "nccl") &&
+      ncclCommInitAll(g_comms.data(), ngpu, nullptr) != ncclSuccess) {
     std::fprintf(stderr, "ncclCommInitAll failed\n");
     return 1;
   }
   const char* methods[] = {"stg", "tma", "ldg", "ce", "nccl"};
   const char* patterns[] = {"uni", "bidir", "a2a"};
+  const std::string only_m = argc > 2 ? argv[2] : "", only_p = argc > 3 ? argv[3] : "";
   for (const char* pat : patterns) {
     for (const char* m : methods) {
       const std::string method = m, pattern = pat;
+      if ((!only_m.empty() && only_m != method) || (!only_p.empty() && only_p != pattern)) continue;
       std::vector<Xfer> xs;
       size_t sent_per_gpu = bytes;
       auto add = [&](int from, int to, size_t off, size_t len) {
