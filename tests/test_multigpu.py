@@ -23,3 +23,17 @@ def test_exchange_multi_gpu():
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert f"MGPU world={n}" in r.stdout and "failures=0" in r.stdout
+
+
+@pytest.mark.gpu
+def test_put_one_process_two_gpus():
+    """The fused put over real NVLink with loopback windows on two devices of one
+    process (scripts/put_nvlink.py): the C2 LLM phase, byte-exact on both ranks."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (gpurun --gpus N)")
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "scripts",
+                                                     "put_nvlink.py"), "2"],
+                       capture_output=True, text=True, timeout=600)
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0 and "bytes OK" in r.stdout
