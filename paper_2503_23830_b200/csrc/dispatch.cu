@@ -1424,12 +1424,13 @@ int orch_xplan_fetch(orch_ctx* ctx, orch_xplan* x, int32_t d, int64_t n, const i
 
 namespace {
 
-// The staged exchange in K slices, pipelined over three streams: slice k of
-// every (this rank -> peer) segment is packed on the caller's stream, sent by
-// one NCCL group on s_comm while slice k+1 is packed, and the slices received
-// are unpacked on s_unpack while the next ones travel. The rows that stay on
-// the rank move with slice 0's pack. Segment slicing is a function of the
-// segment size only, so sender and receiver agree without communicating.
+// The staged exchange in K slices (K = 1 by default), over three streams: slice
+// k of every (this rank -> peer) segment is packed on the caller's stream, sent
+// by one NCCL group on s_comm while slice k+1 is packed, and the slices
+// received are unpacked on s_unpack while the next ones travel. The rows that
+// stay on the rank move last on the caller's stream, beside the transfer (HBM
+// only, no NVLink). Segment slicing is a function of the segment size only, so
+// sender and receiver agree without communicating.
 int staged_rounds(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const void* d_in,
                   int64_t in_cap, void* d_out, int64_t out_cap, void* d_send, int64_t send_cap,
                   void* d_recv, int64_t recv_cap, cudaStream_t st) {
@@ -1486,7 +1487,7 @@ int staged_rounds(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const
   char* recv = static_cast<char*>(d_recv);
   for (int k = 0; k < Kg; ++k) {
     int rc;
-    if (x->n > 0) {  // pack slice k (and, in slice 0, the rows that stay)
+    if (x->n > 0) {  // pack slice k of every off-rank segment
       MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
       a.offs = x->bal.src_offset;
       a.members = x->bal.src_member;
@@ -1500,7 +1501,7 @@ int staged_rounds(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const
       a.out = static_cast<char*>(d_out);
       a.send = static_cast<char*>(d_send);
       a.clip = 1;
-      a.skip_local = k != 0;
+      a.skip_local = 1;  // the rows that stay move below, beside the transfer
       for (int q = 0; q < P; ++q) {
         const int64_t S = q == me ? 0 : x->h_send[me * P + q];
         a.slo[q] = slice(S, k);
@@ -1548,6 +1549,21 @@ int staged_rounds(orch_ctx* ctx, orch_comm* comm, orch_xplan* x, size_t R, const
       rc = run_move(ctx, kUnpack, a, x->n, x->lay.rank_dst_off, x->s_unpack, cap);
       if (rc) return rc;
     }
+  }
+  // the rows that stay on this rank: HBM only, while NCCL moves the rest
+  if (x->n > 0) {
+    MoveArgs a = make_args(P, me, x->d, x->d_len, x->d_origin, &x->bal, &x->lay, R);
+    a.offs = x->bal.src_offset;
+    a.members = x->bal.src_member;
+    a.iter_rows = x->lay.in_rows;
+    a.iter_cap = in_cap;
+    a.in_cap = in_cap;
+    a.out_cap = out_cap;
+    a.in = static_cast<const char*>(d_in);
+    a.out = static_cast<char*>(d_out);
+    a.send = nullptr;
+    const int rc = run_move(ctx, kPack, a, x->n, x->lay.rank_src_off, st, cap);
+    if (rc) return rc;
   }
   (void)recv_cap;
   ORCH_CUDA_TRY(cudaEventRecord(x->ev_done, x->s_unpack));
