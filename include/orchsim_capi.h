@@ -213,8 +213,11 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_pa
  * matrix h_V[d*d] with c instances per node: exact (the reference's answer,
  * including its tie-breaking) by a parallel two-pass branch and bound on the
  * device; ORCH_UNSUPPORTED when d > 64 or d/c > 32 nodes. h_info (optional,
- * [4]) as orch_nodewise's d_info below. A search that exceeds 2^31 visited
- * nodes returns ORCH_UNSUPPORTED (h_hosting then holds the incumbent). */
+ * [4]) as orch_nodewise's d_info below, except h_info[3]: the reference's own
+ * nodes_visited (topology.cpp:150,263), replayed on the device from its chain of
+ * improving leaves (-1 if that replay exceeds 2^31 nodes; h_info == NULL skips
+ * it). A search that exceeds 2^31 visited nodes returns ORCH_UNSUPPORTED
+ * (h_hosting then holds the incumbent). */
 int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
                             int32_t* h_hosting, int64_t* h_info, void* stream);
 

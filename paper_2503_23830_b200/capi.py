@@ -464,17 +464,22 @@ class Context:
         return di[:n], ds[:n]
 
     # ---- node-wise hosting
-    def solve_hosting(self, d, c, V):
+    def solve_hosting(self, d, c, V, info=True):
+        """info=False: the hosting alone (no egress figures, no replay of the
+        reference's nodes_visited)."""
         import numpy as np
         V = np.ascontiguousarray(V, dtype=np.int64).reshape(-1)
         hosting = np.zeros(d, np.int32)
-        info = np.zeros(4, np.int64)
+        inf = np.zeros(4, np.int64)
         _check(lib().orch_solve_hosting_host(self.h, C.c_int32(d), C.c_int32(c),
                                              V.ctypes.data_as(C.c_void_p),
                                              hosting.ctypes.data_as(C.c_void_p),
-                                             info.ctypes.data_as(C.c_void_p), _stream()))
-        return dict(hosting=hosting, max_egress=int(info[0]), baseline_max=int(info[1]),
-                    leaf_used=int(info[2]), visited=int(info[3]))
+                                             inf.ctypes.data_as(C.c_void_p) if info else None,
+                                             _stream()))
+        if not info:
+            return dict(hosting=hosting)
+        return dict(hosting=hosting, max_egress=int(inf[0]), baseline_max=int(inf[1]),
+                    leaf_used=int(inf[2]), visited=int(inf[3]))
 
     def nodewise(self, d, c, length, origin, bal: "Balance", out=None, stream=None):
         """Relabels bal's destination batches in place; returns device tensors

@@ -101,7 +101,7 @@ HostingSolution solve_hosting(const VolumeMatrix& volumes, const ClusterTopology
   sol.hosting.assign(h.begin(), h.end());
   sol.per_node_egress = inter_node_egress(volumes, topo, sol.hosting);
   sol.max_egress = info[0];
-  sol.nodes_visited = info[3];  // the device search's own visit count (int64 counter)
+  sol.nodes_visited = info[3];  // the reference's count, replayed on the device
   return sol;
 }
 

@@ -15,6 +15,14 @@
 //   pass 2  (only if V* beats the incumbents) the first leaf of value V* in DFS
 //           order, pruning on lb > V* and on paths that already sort after the
 //           best V*-leaf found so far.
+// The reference also reports how many nodes its sequential DFS entered
+// (nodes_visited); orch_solve_hosting_host replays that count exactly:
+//   pass 3  (one launch per link) the reference's chain of improving leaves:
+//           the first leaf after the previous link, in DFS order, of value
+//           below it -- pass 2 with a threshold and a lower end;
+//   pass 4  a DFS that cuts each node on lb >= the incumbent the reference held
+//           when it reached it (set by the chain leaves that sort before it),
+//           and counts.
 // Work: the DFS tree cut at depth k0 into <= 8192 prefixes, then work stealing:
 // one warp runs a subtree depth-first (lane = node); when warps are idle, a busy
 // warp donates the shallowest untried sibling of its current path to a global
@@ -42,6 +50,7 @@ constexpr int kHostWarps = 8;
 constexpr long long kHostTasks = 8192;
 constexpr int kHostGrid = 148;
 constexpr int kHostQueue = 16384;  // donated subtrees waiting for a warp
+constexpr int kHostChainMax = 1024;  // improving leaves of the reference's sequential search
 constexpr unsigned long long kHostVisitBudget = 1ull << 31;
 #ifndef ORCH_HOST_SLEEP
 #define ORCH_HOST_SLEEP 2000
@@ -75,6 +84,24 @@ struct HostState {
   int done_ctas;                            // pass 1 CTAs finished (the last one resets for pass 2)
   int have_best;                            // pass 2: best_path holds a V*-leaf
   uint8_t best_path[kHostMaxD];             // candidate position per depth
+  unsigned long long best_key;              // passes 2, 3: least path_key of a found leaf
+  int64_t best_leaf;                        // passes 2, 3: the recorded leaf's value
+  // pass 3 (one link of the reference's chain of improving leaves): the first
+  // leaf after after_path (when after_depth == d) with value <= thresh
+  int64_t thresh;
+  int after_depth;
+  uint8_t after_path[kHostMaxD];
+  // pass 4 (the reference's visit count): chain_bound[i] is the reference's
+  // incumbent value once the first i chain leaves have been offered
+  int chain_len;
+  int chain_done;                           // 1: complete, 2: beyond the budget or kHostChainMax
+  int64_t chain_last;                       // chain_bound[chain_len]
+  int64_t chain_bound[kHostChainMax + 1];
+  uint8_t chain_path[kHostChainMax][kHostMaxD];
+#ifdef ORCH_HOST_DEBUG
+  unsigned long long dbg_t0, dbg_found, dbg_end, dbg_task_max, dbg_donated, dbg_first_end;
+  unsigned long long dbg_visits0, dbg_visits_max;
+#endif
   unsigned q_ready[kHostQueue];             // pass << 30 | (index + 1) once published, 0 once read
   uint8_t q_depth[kHostQueue];
   uint8_t q_path[kHostQueue][kHostMaxD];
@@ -250,8 +277,9 @@ __device__ void prep_volume(Prep<MD>& S, int d, int64_t n, const int64_t* len, c
   __syncthreads();
 }
 
-// per warp: choice stack ch[64] (u8), then avail[64] and donated[64] (u32 masks)
-constexpr int kWarpStack = kHostMaxD + 2 * 4 * kHostMaxD;
+// per warp: choice stack ch[64] (u8), then avail[64] and donated[64] (u32
+// masks), then lo[65] and hi[65] (u16, pass 4: the chain leaves below the path)
+constexpr int kWarpStack = (kHostMaxD + 2 * 4 * kHostMaxD + 2 * 2 * (kHostMaxD + 1) + 15) & ~15;
 
 struct HostSmem {
   const int64_t* g2;
@@ -322,18 +350,71 @@ __device__ __forceinline__ int path_cmp(const uint8_t* a, const volatile uint8_t
   return 0;
 }
 
+#ifdef ORCH_HOST_DEBUG
+__device__ __forceinline__ unsigned long long dbg_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+// The first km positions of a path packed kb bits each, most significant
+// first (kb = bits of a node index): keys order as paths do, so a path whose
+// key (missing positions as 0: the least leaf below it) exceeds a found leaf's
+// key sorts after that leaf, and one atomicMin keeps the least key found.
+__device__ __forceinline__ unsigned long long path_key(const uint8_t* ch, int k, int kb, int km,
+                                                       int lane) {
+  const int m = k < km ? k : km;
+  unsigned hi = 0, lo = 0;
+  for (int l0 = 0; l0 < m; l0 += 32) {
+    const int l = l0 + lane;
+    if (l < m) {
+      const unsigned long long v = static_cast<unsigned long long>(ch[l]) << (64 - kb * (l + 1));
+      hi |= static_cast<unsigned>(v >> 32);
+      lo |= static_cast<unsigned>(v);
+    }
+  }
+  hi = __reduce_or_sync(~0u, hi);
+  lo = __reduce_or_sync(~0u, lo);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
 struct WarpStack {
   uint8_t* ch;        // candidate position chosen per depth
   unsigned* avail;    // positions with room per depth (as of choosing there)
   unsigned* donated;  // positions given away per depth (current path only)
+  uint16_t* lo;       // pass 4, per depth k: chain leaves [lo, hi) share the path's
+  uint16_t* hi;       //   first k positions; those below lo sort before the node
 };
+
+// Pass 4: the chain leaves below the node at depth k + 1 reached by position
+// j, from those [lo, hi) below its parent (sorted: ascending position at k).
+__device__ __forceinline__ void chain_step(const HostState& H, int k, int j, int lo, int hi,
+                                           int lane, int& nlo, int& nhi) {
+  int less = 0, same = 0;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const int x = i < hi ? H.chain_path[i][k] : 256;
+    less += __popc(__ballot_sync(~0u, x < j));
+    same += __popc(__ballot_sync(~0u, x == j));
+  }
+  nlo = lo + less;
+  nhi = nlo + same;
+}
+
+// the work queue's publication word for a subtree: launch tag, slot + 1 (never 0)
+__device__ __forceinline__ unsigned q_tag(int pass, unsigned slot) {
+  return (static_cast<unsigned>(pass & 3) << 30) | (slot + 1);
+}
 
 // Depth-first search of the subtree below the path ch[0, root) (state: this
 // lane's room / gained). pass 1 prunes lb >= best and lowers the global
 // incumbent at leaves; pass 2 prunes lb > vstar and paths after the best
-// V*-leaf, and records a V*-leaf if it sorts first. Donates siblings to idle
-// warps. Returns when the subtree is exhausted (or cut).
-__device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vstar, WarpStack W,
+// V*-leaf, and records a V*-leaf if it sorts first; pass 3 is pass 2 restricted
+// to leaves after H.after_path; pass 4 prunes a node on lb >= the incumbent the
+// reference holds when it gets there (chain_bound[lo]) and only counts.
+// Donates siblings to idle warps. Returns when the subtree is exhausted (or cut).
+__device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vstar, WarpStack W,
                          int root, int room, int64_t gained) {
   const int d = H.d, c = H.c, nodes = H.nodes, lane = threadIdx.x & 31;
   const bool active = lane < nodes;
@@ -344,6 +425,17 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
   int k = root, jstart = 0;
   bool descend = true;
   W.donated[root] = 0;
+  const int after = pass == 3 ? H.after_depth : 0;
+  const int kb = nodes > 1 ? 32 - __clz(nodes - 1) : 1, km = d < 64 / kb ? d : 64 / kb;
+  if (pass == 4) {  // the chain leaves below the subtree's root
+    int lo = 0, hi = H.chain_len;
+    for (int l = 0; l < root; ++l) chain_step(H, l, W.ch[l], lo, hi, lane, lo, hi);
+    if (lane == 0) {
+      W.lo[root] = static_cast<uint16_t>(lo);
+      W.hi[root] = static_cast<uint16_t>(hi);
+    }
+    __syncwarp();
+  }
   for (;;) {
     if (descend) {
       ++visits;
@@ -357,8 +449,9 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
         if (pass == 1) {
           best = static_cast<int64_t>(
               __shfl_sync(~0u, lane == 0 ? volatile_load(&H.best_value) : 0ull, 0));
-        } else if (__shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) &&
-                   path_cmp(W.ch, H.best_path, k, lane) > 0) {
+        } else if ((pass == 2 || pass == 3) &&
+                   path_key(W.ch, k, kb, km, lane) >
+                       __shfl_sync(~0u, lane == 0 ? volatile_load(&H.best_key) : 0ull, 0)) {
           break;  // everything left in this subtree sorts after the best V*-leaf
         }
         // donate the shallowest untried sibling when warps wait for work
@@ -407,8 +500,11 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
             __syncwarp();
             if (lane == 0)
               *reinterpret_cast<volatile unsigned*>(&H.q_ready[slot % kHostQueue]) =
-                  (static_cast<unsigned>(pass) << 30) | (slot + 1);
+                  q_tag(pass, slot);
             W.donated[lvl] |= 1u << q;
+#ifdef ORCH_HOST_DEBUG
+            if (lane == 0) atomicAdd(&H.dbg_donated, 1ull);
+#endif
             __syncwarp();
           }
         }
@@ -417,13 +513,31 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
           active ? total - gained - T.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room]
                  : 0;
       const int64_t lb = warp_max_nonneg(term);  // egress >= 0: clamping keeps the bound valid
-      bool prune = pass == 1 ? lb >= best : lb > vstar;
+      bool prune;
+      if (pass == 1) {
+        prune = lb >= best;
+      } else if (pass == 4) {
+        prune = k == d || lb >= H.chain_bound[W.lo[k]];
+      } else {
+        prune = lb > vstar;
+        if (!prune && after) {  // pass 3: only what sorts after the previous chain leaf
+          const int cmp = path_cmp(W.ch, H.after_path, k, lane);
+          prune = cmp < 0 || (cmp == 0 && k == d);
+        }
+      }
       if (!prune && k == d) {  // leaf: value == lb
         if (pass == 1) {
           if (lane == 0) atomicMin(&H.best_value, static_cast<unsigned long long>(lb));
           best = lb;
           prune = true;
         } else {  // a V*-leaf: keep it if it is the first in DFS order so far
+          // lock-free filter first: only a leaf whose key is not above every
+          // key found so far can be the first (keys tie on paths that share
+          // their first km positions: those compare in full under the lock)
+          const unsigned long long key = path_key(W.ch, d, kb, km, lane);
+          unsigned long long least = 0;
+          if (lane == 0) least = atomicMin(&H.best_key, key);
+          if (key > __shfl_sync(~0u, least, 0)) break;
           if (lane == 0)
             while (atomicCAS(&H.lock, 0, 1) != 0) {
             }
@@ -431,9 +545,13 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
           __threadfence();
           const bool first = !__shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) ||
                              path_cmp(W.ch, H.best_path, d, lane) < 0;
+#ifdef ORCH_HOST_DEBUG
+          if (lane == 0) atomicMax(&H.dbg_found, dbg_now());
+#endif
           if (first) {
             volatile uint8_t* bp = H.best_path;
             for (int l = lane; l < d; l += 32) bp[l] = W.ch[l];
+            if (lane == 0) *reinterpret_cast<volatile int64_t*>(&H.best_leaf) = lb;
             __threadfence();
             __syncwarp();
             if (lane == 0) *reinterpret_cast<volatile int*>(&H.have_best) = 1;
@@ -477,11 +595,22 @@ __device__ void host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vsta
       --room;
       gained += T.g2[k * nodes + m];
     }
+    if (pass == 4) {
+      int lo, hi;
+      chain_step(H, k, j, W.lo[k], W.hi[k], lane, lo, hi);
+      __syncwarp();
+      if (lane == 0) {
+        W.lo[k + 1] = static_cast<uint16_t>(lo);
+        W.hi[k + 1] = static_cast<uint16_t>(hi);
+      }
+      __syncwarp();
+    }
     ++k;
     if (k < d) W.donated[k] = 0;
     descend = true;
   }
   if (lane == 0) atomicAdd(&H.visits, visits & 65535);
+  return visits;
 }
 
 
@@ -521,6 +650,7 @@ __global__ void __launch_bounds__(1024, 1) k_host_setup(int d, int c, int64_t n,
     H->visits = 0;
     H->overflow = 0;
     H->have_best = 0;
+    H->best_key = ~0ull;
     int k0 = 0;
     long long tasks = 1;
     while (k0 < d && tasks * nodes <= kHostTasks) {
@@ -544,13 +674,19 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
   HostState& H = *Hp;
   // pass 1 CTAs never leave early: the last one to finish resets the queue
   if (pass == 2 && (H.overflow || static_cast<long long>(H.best_value) >= H.incumbent_value)) return;
+  if (pass == 3 && H.chain_done) return;
+#ifdef ORCH_HOST_DEBUG
+  if (threadIdx.x == 0) atomicMin(&H.dbg_t0, dbg_now());
+#endif
   const HostSmem T = host_load_tables(H, host_raw);
   const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   unsigned char* ws = host_raw + host_table_bytes(H.d, H.c) + warp * kWarpStack;
-  WarpStack W{ws, reinterpret_cast<unsigned*>(ws + kHostMaxD),
-              reinterpret_cast<unsigned*>(ws + kHostMaxD) + kHostMaxD};
-  const int64_t vstar = static_cast<int64_t>(H.best_value);
+  unsigned* masks = reinterpret_cast<unsigned*>(ws + kHostMaxD);
+  uint16_t* ranges = reinterpret_cast<uint16_t*>(masks + 2 * kHostMaxD);
+  WarpStack W{ws, masks, masks + kHostMaxD, ranges, ranges + kHostMaxD + 1};
+  const int64_t vstar = pass == 3 ? H.thresh : static_cast<int64_t>(H.best_value);
   const int c = H.c, nodes = H.nodes, k0 = H.k0;
+  const int kb = nodes > 1 ? 32 - __clz(nodes - 1) : 1, km = H.d < 64 / kb ? H.d : 64 / kb;
   const bool active = lane < nodes;
   bool waiting = false;
   for (;;) {
@@ -615,7 +751,7 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
       root = k0;
     } else {  // donated subtree: wait until published, then replay its path
       const unsigned slot = static_cast<unsigned>(qs) % kHostQueue;
-      const unsigned want = (static_cast<unsigned>(pass) << 30) | (static_cast<unsigned>(qs) + 1);
+      const unsigned want = q_tag(pass, static_cast<unsigned>(qs));
       if (lane == 0)
         while (volatile_u32(&H.q_ready[slot]) != want) {
         }
@@ -638,16 +774,35 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
         *reinterpret_cast<volatile unsigned*>(&H.q_ready[slot]) = 0u;
     }
     __syncwarp();
-    if (ok && pass == 2 && __shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) &&
-        path_cmp(W.ch, H.best_path, root, lane) > 0)
+    if (ok && (pass == 2 || pass == 3) &&
+        path_key(W.ch, root, kb, km, lane) >
+            __shfl_sync(~0u, lane == 0 ? volatile_load(&H.best_key) : 0ull, 0))
       ok = false;  // the whole subtree sorts after the best V*-leaf
+#ifdef ORCH_HOST_DEBUG
+    const unsigned long long ts = dbg_now();
+#endif
+#ifdef ORCH_HOST_DEBUG
+    const unsigned long long tv = ok ? host_dfs(H, T, pass, vstar, W, root, room, gained) : 0;
+    if (lane == 0) {
+      atomicMax(&H.dbg_task_max, dbg_now() - ts);
+      atomicMax(&H.dbg_visits_max, tv);
+      if (t == 0) {
+        H.dbg_first_end = dbg_now();
+        H.dbg_visits0 = tv;
+      }
+    }
+#else
     if (ok) host_dfs(H, T, pass, vstar, W, root, room, gained);
+#endif
     __syncwarp();
     if (lane == 0) {
       __threadfence();
       atomicSub(&H.pending, 1);
     }
   }
+#ifdef ORCH_HOST_DEBUG
+  if (threadIdx.x == 0) atomicMax(&H.dbg_end, dbg_now());
+#endif
   if (pass == 1) {  // the last CTA out resets the work distribution for pass 2
     __shared__ int last;
     __syncthreads();
@@ -668,6 +823,69 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
   }
 }
 
+// Before a pass 3 or pass 4 launch: the work distribution as after setup and a
+// fresh visit budget. mode 3: the chain's first link (leaves below the
+// incumbents' value); mode 5: the next link, after appending the last pass 3's
+// leaf to the chain (or closing the chain: no leaf, or the budget hit), so that
+// links run back to back without the host; mode 4: the counting pass, from the
+// root alone (work donation spreads it) so that every node it enters is one the
+// reference enters -- a root the incumbents already cut is its single visit.
+__global__ void k_host_reset(HostState* H, int mode) {
+#ifdef ORCH_HOST_DEBUG
+  if (!H->chain_done || mode != 5)
+    printf("reset mode %d: chain %d have %d leaf %lld thresh %lld visits %llu overflow %d | "
+           "found +%llu us, task0 end +%llu us, end +%llu us, longest task %llu us, donated %llu\n",
+           mode, H->chain_len, H->have_best, (long long)H->best_leaf, (long long)H->thresh,
+           H->visits, H->overflow, (H->dbg_found - H->dbg_t0) / 1000,
+           (H->dbg_first_end - H->dbg_t0) / 1000, (H->dbg_end - H->dbg_t0) / 1000,
+           H->dbg_task_max / 1000, H->dbg_donated);
+  printf("   task 0 visits %llu, most visits in a task %llu\n", H->dbg_visits0, H->dbg_visits_max);
+  H->dbg_visits0 = H->dbg_visits_max = 0;
+  H->dbg_t0 = ~0ull;
+  H->dbg_found = H->dbg_end = H->dbg_task_max = H->dbg_donated = H->dbg_first_end = 0;
+#endif
+  if (mode == 3) {
+    H->chain_len = 0;
+    H->chain_done = 0;
+    H->chain_bound[0] = H->chain_last = H->incumbent_value;
+    H->thresh = H->incumbent_value - 1;
+    H->after_depth = 0;
+  } else if (mode == 5) {
+    if (H->chain_done) return;
+    if (H->overflow || H->chain_len == kHostChainMax) {
+      H->chain_done = 2;
+      return;
+    }
+    if (!H->have_best) {
+      H->chain_done = 1;
+      return;
+    }
+    const int i = H->chain_len, d = H->d;
+    for (int l = 0; l < d; ++l) H->chain_path[i][l] = H->after_path[l] = H->best_path[l];
+    H->chain_bound[i + 1] = H->chain_last = H->best_leaf;
+    H->chain_len = i + 1;
+    H->thresh = H->best_leaf - 1;
+    H->after_depth = d;
+  }
+  H->task_counter = 0;
+  H->q_head = H->q_tail = 0;
+  H->idle = 0;
+  H->lock = 0;
+  H->done_ctas = 0;
+  H->have_best = 0;
+  H->best_key = ~0ull;
+  H->overflow = 0;
+  H->visits = 0;
+  if (mode == 4) {
+    if (H->tasks == 0) {
+      H->visits = 1;
+    } else {
+      H->k0 = 0;
+      H->tasks = 1;
+    }
+  }
+  H->pending = static_cast<int>(H->tasks);
+}
 
 // Final hosting, batch -> instance map (topology.cpp:283-290), egress figures;
 // with a balance result, its relabelling (batch b becomes instance b2i[b]).
@@ -1118,6 +1336,55 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
   return ORCH_OK;
 }
 
+// The reference's nodes_visited (topology.cpp:150-151, 263). Its sequential DFS
+// enters a node iff the parent was not cut by lb >= the incumbent it held at
+// that moment, and that incumbent changes only at its chain of strictly
+// improving leaves: each the first leaf in DFS order after the previous one
+// whose value is below it, starting from the incumbents' value. The chain is
+// found link by link (pass 3, launched in batches that the device chains
+// itself), then one pass replays the reference's cuts node by node and counts
+// (pass 4). Runs after the hosting search (its pass 1/2 state is consumed).
+// *visits = -1 when a pass exceeds the visit budget or the chain kHostChainMax
+// links.
+int reference_visits(orch_ctx* ctx, HostState* H, int d, int c, cudaStream_t st, int64_t* visits) {
+  const int sm = static_cast<int>(host_smem_bytes(d, c));
+  constexpr int kLinksPerSync = 8;
+  *visits = -1;
+  k_host_reset<<<1, 1, 0, st>>>(H, 3);
+  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
+  ctx->launches += 2;
+  int done = 0;
+  while (!done) {
+    for (int i = 0; i < kLinksPerSync; ++i) {
+      k_host_reset<<<1, 1, 0, st>>>(H, 5);
+      k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
+    }
+    ctx->launches += 2 * kLinksPerSync;
+    ORCH_CUDA_TRY(cudaGetLastError());
+    ORCH_CUDA_TRY(cudaMemcpyAsync(&done, &H->chain_done, sizeof done, cudaMemcpyDeviceToHost, st));
+    ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (done != 1) return ORCH_OK;
+  // the chain ends at the optimum pass 1 found (or is empty: the incumbents stand)
+  int64_t last = 0;
+  unsigned long long vstar = 0;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(&last, &H->chain_last, sizeof last, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(&vstar, &H->best_value, sizeof vstar, cudaMemcpyDeviceToHost, st));
+  k_host_reset<<<1, 1, 0, st>>>(H, 4);
+  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 4);
+  ctx->launches += 2;
+  ORCH_CUDA_TRY(cudaGetLastError());
+  unsigned long long count = 0;
+  int overflow = 0;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(&count, &H->visits, sizeof count, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(&overflow, &H->overflow, sizeof overflow, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
+  if (static_cast<unsigned long long>(last) != vstar)
+    return fail(ORCH_LOGIC_ERROR, "solve_hosting: the improving-leaf chain misses the optimum");
+  if (!overflow) *visits = static_cast<int64_t>(count);
+  return ORCH_OK;
+}
+
 }  // namespace
 }  // namespace orchb
 
@@ -1153,10 +1420,16 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
   int64_t hinfo[4];
   ORCH_CUDA_TRY(cudaMemcpyAsync(hinfo, info, sizeof hinfo, cudaMemcpyDeviceToHost, st));
   ORCH_CUDA_TRY(cudaStreamSynchronize(st));
-  if (h_info) memcpy(h_info, hinfo, sizeof hinfo);
-  if (hinfo[2] == -1)  // the exact answer is unknown: never return the incumbent silently
+  if (hinfo[2] == -1) {  // the exact answer is unknown: never return the incumbent silently
+    if (h_info) memcpy(h_info, hinfo, sizeof hinfo);
     return fail(ORCH_UNSUPPORTED,
                 "solve_hosting: the exact search exceeded its budget of 2^31 visited nodes");
+  }
+  if (h_info) {
+    rc = reference_visits(ctx, H, d, c, st, &hinfo[3]);
+    if (rc) return rc;
+    memcpy(h_info, hinfo, sizeof hinfo);
+  }
   return ORCH_OK;
 }
 

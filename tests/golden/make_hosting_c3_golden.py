@@ -18,7 +18,7 @@ def main():
     from paper_2503_23830_b200 import workload
     ref = RefLib()
     b = workload.make_batch(3, 64, 64, 7)
-    Vs, cs, hs, mx = [], [], [], []
+    Vs, cs, hs, mx, vis = [], [], [], [], []
     for name, kind in (("vision", 0), ("audio", 1), ("llm", 0)):
         L, O = b.llm_items() if name == "llm" else b.phase_items(name)[:2]
         di, _, _, _ = ref.balance(kind, 64, L, O)
@@ -30,9 +30,10 @@ def main():
             cs.append(c)
             hs.append(r["hosting"])
             mx.append(r["max_egress"])
+            vis.append(r["visited"])
     np.savez_compressed(os.path.join(HERE, "ref_hosting_c3.npz"), V=np.array(Vs, np.int64),
                         c=np.array(cs, np.int32), hosting=np.array(hs, np.int32),
-                        max_egress=np.array(mx, np.int64))
+                        max_egress=np.array(mx, np.int64), visited=np.array(vis, np.int64))
     print("cases", len(cs))
 
 

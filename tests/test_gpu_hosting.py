@@ -27,6 +27,7 @@ def test_solve_hosting_random(ctx, oracle):
         np.testing.assert_array_equal(a["hosting"], o["hosting"])
         assert a["max_egress"] == o["max_egress"]
         assert a["baseline_max"] == o["baseline_max"]
+        assert a["visited"] == o["visited"], (d, c)
 
 
 def test_solve_hosting_fixtures(ctx):
@@ -36,6 +37,7 @@ def test_solve_hosting_fixtures(ctx):
         a = ctx.solve_hosting(d, c, f["V"][k, :d * d])
         np.testing.assert_array_equal(a["hosting"], f["hosting"][k, :d])
         assert a["max_egress"] == f["max_egress"][k]
+        assert a["visited"] == f["visited"][k], (k, d, c)  # the reference's nodes_visited
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
@@ -98,6 +100,7 @@ def test_solve_hosting_c3_shapes(ctx, oracle):
         assert a["max_egress"] == f["max_egress"][k]
         o = oracle.solve_hosting(64, c, f["V"][k])
         np.testing.assert_array_equal(o["hosting"], f["hosting"][k])
+        assert a["visited"] == f["visited"][k], (k, a["visited"], int(f["visited"][k]))
 
 
 def test_solve_hosting_random_larger(ctx, oracle):
@@ -114,6 +117,7 @@ def test_solve_hosting_random_larger(ctx, oracle):
         a = ctx.solve_hosting(d, c, V)
         np.testing.assert_array_equal(a["hosting"], o["hosting"])
         assert a["max_egress"] == o["max_egress"]
+        assert a["visited"] == o["visited"], (d, c)
 
 
 def test_hosting_limits(ctx):

@@ -164,6 +164,7 @@ def test_hosting_fixtures(oracle):
         a = oracle.solve_hosting(d, c, V)
         np.testing.assert_array_equal(a["hosting"], f["hosting"][k, :d])
         assert a["max_egress"] == f["max_egress"][k]
+        assert a["visited"] == f["visited"][k]
 
 
 def test_hosting_c3_fixtures(oracle):
@@ -173,3 +174,4 @@ def test_hosting_c3_fixtures(oracle):
         a = oracle.solve_hosting(64, int(f["c"][k]), f["V"][k].reshape(64, 64))
         np.testing.assert_array_equal(a["hosting"], f["hosting"][k])
         assert a["max_egress"] == f["max_egress"][k]
+        assert a["visited"] == f["visited"][k]
