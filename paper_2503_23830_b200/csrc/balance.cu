@@ -137,6 +137,14 @@ int check_policy_args(const orch_policy* p, int d, int64_t n, int identity_only)
   return ORCH_OK;
 }
 
+// The single-CTA kernel serves the call (k_balance_small): it reads each input
+// once and writes each output once.
+bool takes_small_path(const orch_policy* pol, int d, int64_t n, int mode) {
+  const bool one_lane_per_batch = mode == 0 && (pol->kind == ORCH_QUADRATIC_TOLERANCE ||
+                                                pol->kind == ORCH_CONVTRANSFORMER);
+  return mode <= 1 && d <= (one_lane_per_batch ? 32 : kSmallMaxD) && n <= kSmallMaxItems;
+}
+
 // mode: 0 balance, 1 identity only, 2 padded search only, 3 padded feasibility probe
 int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const int64_t* len,
                 const int32_t* origin, int mode, int64_t probe, const orch_balance_out* out,
@@ -154,10 +162,7 @@ int run_balance(orch_ctx* ctx, const orch_policy* pol, int d, int64_t n, const i
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
 
   // quadratic tolerance and ConvTransformer keep one batch per lane (d <= 32)
-  const int small_max_d =
-      !identity_only && (kind == ORCH_QUADRATIC_TOLERANCE || kind == ORCH_CONVTRANSFORMER) ? 32
-                                                                                          : kSmallMaxD;
-  if (mode <= 1 && d <= small_max_d && n <= kSmallMaxItems) {
+  if (takes_small_path(pol, d, n, mode)) {
     Plan sp;
     SmallArgs a{};
     const size_t nn1 = static_cast<size_t>(n > 0 ? n : 1);
@@ -532,6 +537,8 @@ int orch_balance_layout1(orch_ctx* ctx, const orch_policy* policy, int32_t d, in
 // (pageable cudaMemcpyAsync calls cost ~10 us each; a call used to make eight).
 namespace {
 
+constexpr int64_t kZeroCopyItems = 256;
+
 int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
                   const int64_t* h_len, const int32_t* h_origin, int mode, int64_t probe,
                   int32_t* h_dest_inst, int32_t* h_dest_slot, int64_t* h_dst_off,
@@ -560,25 +567,32 @@ int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n
   orch_balance_out out{};
   // only the outputs this mode reads back are written by the pipeline
   const bool rows = n > 0 && mode < 2;
-  out.dest_inst = reinterpret_cast<int32_t*>(dp + o_di);
-  out.dest_slot = reinterpret_cast<int32_t*>(dp + o_ds);
-  out.dst_off = reinterpret_cast<int64_t*>(dp + o_doff);
-  out.bin_count = reinterpret_cast<int32_t*>(dp + o_bc);
-  out.bin_cost = reinterpret_cast<double*>(dp + o_cost);
-  out.summary = reinterpret_cast<orch_summary*>(dp + o_sum);
+  // Zero copy when the single-CTA kernel serves the call and the phase is small
+  // (C5: 64 items): it reads the pinned staging through the host mapping and
+  // writes its outputs back the same way, so a call is one launch and one
+  // synchronize with no copy operations.
+  const bool zero_copy = n <= kZeroCopyItems && orchb::takes_small_path(policy, d, n, mode);
+  char* base = zero_copy ? hp : dp;
+  out.dest_inst = reinterpret_cast<int32_t*>(base + o_di);
+  out.dest_slot = reinterpret_cast<int32_t*>(base + o_ds);
+  out.dst_off = reinterpret_cast<int64_t*>(base + o_doff);
+  out.bin_count = reinterpret_cast<int32_t*>(base + o_bc);
+  out.bin_cost = reinterpret_cast<double*>(base + o_cost);
+  out.summary = reinterpret_cast<orch_summary*>(base + o_sum);
   if (n > 0) {
     std::memcpy(hp + o_len, h_len, static_cast<size_t>(n) * 8);
     std::memcpy(hp + o_org, h_origin, static_cast<size_t>(n) * 4);
-    ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
+    if (!zero_copy) ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
   }
-  rc = orchb::run_balance(ctx, policy, d, n, reinterpret_cast<int64_t*>(dp + o_len),
-                          reinterpret_cast<int32_t*>(dp + o_org), mode, probe, &out,
-                          reinterpret_cast<int64_t*>(dp + o_bound),
-                          reinterpret_cast<int32_t*>(dp + o_probe), st);
+  rc = orchb::run_balance(ctx, policy, d, n, reinterpret_cast<int64_t*>(base + o_len),
+                          reinterpret_cast<int32_t*>(base + o_org), mode, probe, &out,
+                          reinterpret_cast<int64_t*>(base + o_bound),
+                          reinterpret_cast<int32_t*>(base + o_probe), st);
   if (rc) return rc;
   // one read-back: the per-item outputs (balance modes) through the probe word
   const size_t back = rows ? o_di : o_bc;
-  ORCH_CUDA_TRY(cudaMemcpyAsync(hp + back, dp + back, total - back, cudaMemcpyDeviceToHost, st));
+  if (!zero_copy)
+    ORCH_CUDA_TRY(cudaMemcpyAsync(hp + back, dp + back, total - back, cudaMemcpyDeviceToHost, st));
   ORCH_CUDA_TRY(cudaStreamSynchronize(st));
   orch_summary sum;
   std::memcpy(&sum, hp + o_sum, sizeof sum);

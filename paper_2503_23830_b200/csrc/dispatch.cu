@@ -1752,6 +1752,8 @@ struct StageLayout {
 };
 }  // namespace
 
+constexpr size_t kZeroCopyBytes = 16384;
+
 int orch_batch_costs_host(orch_ctx* ctx, const orch_cost_model* model, int32_t batch_padded,
                           int32_t d, int64_t n, const int64_t* h_len, const int32_t* h_bin_offset,
                           const int32_t* h_bin_member, double* h_cost, double* h_stats,
@@ -1776,15 +1778,18 @@ int orch_batch_costs_host(orch_ctx* ctx, const orch_cost_model* model, int32_t b
     memcpy(hp + o_mem, h_bin_member, nn * 4);
   }
   memcpy(hp + o_off, h_bin_offset, static_cast<size_t>(d + 1) * 4);
-  ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
   // The costs (d doubles) and stats go straight to the pinned mirror (mapped
   // into the device's address space under UVA): no device-to-host copy call,
-  // which is a third of a one-batch cost() round trip.
+  // which is a third of a one-batch cost() round trip. Small inputs (one
+  // batch: the per-batch cost() of stats_of) are read through the mapping too,
+  // so such a call is one launch and one synchronize.
+  const char* in = in_bytes <= kZeroCopyBytes ? hp : dp;
+  if (in == dp) ORCH_CUDA_TRY(cudaMemcpyAsync(dp, hp, in_bytes, cudaMemcpyHostToDevice, st));
   double* cost = reinterpret_cast<double*>(hp + o_cost);
   launch(ctx, [&] {
     k_bin_cost<<<blocks_for(static_cast<int64_t>(d) * 32, kThreads), kThreads, 0, st>>>(
-        *model, d, reinterpret_cast<const int32_t*>(dp + o_off),
-        reinterpret_cast<const int32_t*>(dp + o_mem), reinterpret_cast<const int64_t*>(dp + o_len),
+        *model, d, reinterpret_cast<const int32_t*>(in + o_off),
+        reinterpret_cast<const int32_t*>(in + o_mem), reinterpret_cast<const int64_t*>(in + o_len),
         nullptr, nullptr, nullptr, cost, nullptr);
   });
   if (h_stats)
