@@ -729,7 +729,22 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
     if (t >= 0) {  // initial prefix: digit k = candidate position among nodes with room
       const int ti = static_cast<int>(t);
       int div = static_cast<int>(H.tasks) / nodes;
+      int lo = 0, hi = pass == 4 ? H.chain_len : 0;
       for (int k = 0; k < k0; ++k) {
+        if (pass == 4) {
+          // the prefix node at depth k, entered by the reference (its ancestors
+          // were not cut): counted once, by the task whose later digits are all
+          // 0, then cut as the reference cuts it
+          if (lane == 0 && ti % ((div > 0 ? div : 1) * nodes) == 0) atomicAdd(&H.visits, 1ull);
+          const int64_t term =
+              active ? H.node_total[lane] - gained -
+                           T.og[(static_cast<size_t>(k) * nodes + lane) * (c + 1) + room]
+                     : 0;
+          if (warp_max_nonneg(term) >= H.chain_bound[lo]) {
+            ok = false;
+            break;
+          }
+        }
         const int p = (ti / (div > 0 ? div : 1)) % nodes;
         div /= nodes;
         const unsigned pm =
@@ -747,6 +762,7 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
           --room;
           gained += T.g2[k * nodes + m];
         }
+        if (pass == 4) chain_step(H, k, j, lo, hi, lane, lo, hi);
       }
       root = k0;
     } else {  // donated subtree: wait until published, then replay its path
@@ -827,9 +843,9 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
 // fresh visit budget. mode 3: the chain's first link (leaves below the
 // incumbents' value); mode 5: the next link, after appending the last pass 3's
 // leaf to the chain (or closing the chain: no leaf, or the budget hit), so that
-// links run back to back without the host; mode 4: the counting pass, from the
-// root alone (work donation spreads it) so that every node it enters is one the
-// reference enters -- a root the incumbents already cut is its single visit.
+// links run back to back without the host; mode 4: the counting pass (a root
+// the incumbents already cut is the reference's single visit; otherwise each
+// task walks its prefix nodes as the reference would: k_host_bb).
 __global__ void k_host_reset(HostState* H, int mode) {
 #ifdef ORCH_HOST_DEBUG
   if (!H->chain_done || mode != 5)
@@ -846,7 +862,8 @@ __global__ void k_host_reset(HostState* H, int mode) {
 #endif
   if (mode == 3) {
     H->chain_len = 0;
-    H->chain_done = 0;
+    // no leaf beats the incumbents (pass 1's optimum is theirs): an empty chain
+    H->chain_done = static_cast<long long>(H->best_value) >= H->incumbent_value ? 1 : 0;
     H->chain_bound[0] = H->chain_last = H->incumbent_value;
     H->thresh = H->incumbent_value - 1;
     H->after_depth = 0;
@@ -864,6 +881,8 @@ __global__ void k_host_reset(HostState* H, int mode) {
     for (int l = 0; l < d; ++l) H->chain_path[i][l] = H->after_path[l] = H->best_path[l];
     H->chain_bound[i + 1] = H->chain_last = H->best_leaf;
     H->chain_len = i + 1;
+    // a link at pass 1's optimum is the last: nothing after it can be lower
+    if (static_cast<unsigned long long>(H->best_leaf) == H->best_value) H->chain_done = 1;
     H->thresh = H->best_leaf - 1;
     H->after_depth = d;
   }
@@ -876,14 +895,7 @@ __global__ void k_host_reset(HostState* H, int mode) {
   H->best_key = ~0ull;
   H->overflow = 0;
   H->visits = 0;
-  if (mode == 4) {
-    if (H->tasks == 0) {
-      H->visits = 1;
-    } else {
-      H->k0 = 0;
-      H->tasks = 1;
-    }
-  }
+  if (mode == 4 && H->tasks == 0) H->visits = 1;  // the incumbents cut the root
   H->pending = static_cast<int>(H->tasks);
 }
 
@@ -1348,18 +1360,19 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
 // links.
 int reference_visits(orch_ctx* ctx, HostState* H, int d, int c, cudaStream_t st, int64_t* visits) {
   const int sm = static_cast<int>(host_smem_bytes(d, c));
-  constexpr int kLinksPerSync = 8;
+  int links = 2;  // links launched per host check: 2, 4, 8, 8, ...
   *visits = -1;
   k_host_reset<<<1, 1, 0, st>>>(H, 3);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
   ctx->launches += 2;
   int done = 0;
   while (!done) {
-    for (int i = 0; i < kLinksPerSync; ++i) {
+    for (int i = 0; i < links; ++i) {
       k_host_reset<<<1, 1, 0, st>>>(H, 5);
       k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
     }
-    ctx->launches += 2 * kLinksPerSync;
+    ctx->launches += 2 * links;
+    links = links < 8 ? 2 * links : 8;
     ORCH_CUDA_TRY(cudaGetLastError());
     ORCH_CUDA_TRY(cudaMemcpyAsync(&done, &H->chain_done, sizeof done, cudaMemcpyDeviceToHost, st));
     ORCH_CUDA_TRY(cudaStreamSynchronize(st));
