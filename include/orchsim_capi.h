@@ -212,7 +212,8 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_pa
 /* solve_hosting (topology.hpp:71, topology.cpp:179-265) on a host volume
  * matrix h_V[d*d] with c instances per node: exact (the reference's answer,
  * including its tie-breaking) by a parallel two-pass branch and bound on the
- * device; ORCH_UNSUPPORTED when d > 64 or d/c > 32 nodes. h_info (optional,
+ * device; ORCH_UNSUPPORTED when d > ORCH_MAX_INSTANCES or d/c > 32 nodes (d > 64:
+ * search tables and DFS stacks in global memory). h_info (optional,
  * [4]) as orch_nodewise's d_info below, except h_info[3]: the reference's own
  * nodes_visited (topology.cpp:150,263), replayed on the device from its chain of
  * improving leaves (-1 if that replay exceeds 2^31 nodes; h_info == NULL skips

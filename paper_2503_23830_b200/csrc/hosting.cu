@@ -28,6 +28,9 @@
 // warp donates the shallowest untried sibling of its current path to a global
 // queue. A subtree is identified by its path of candidate positions, and DFS
 // order is the lexicographic order of paths, so pass 2 stays exact.
+// d <= 64 keeps the tables and the warps' DFS stacks in shared memory; beyond
+// (orch_solve_hosting_host up to ORCH_MAX_INSTANCES, e.g. C4's d = 2560) they
+// stay in global memory and grid-wide kernels build the tables (k_hw_*).
 // The bound is the reference's lower_bound -- max over nodes of
 // (total - gained - optimistic gain) -- read in O(1): the unassigned batches
 // at depth k are exactly order[k..d), so the optimistic gain of node n with r
@@ -45,11 +48,11 @@ namespace {
 
 constexpr int kHostMaxD = 64;
 constexpr int kHostMaxNodes = 32;                  // lane = node
-constexpr int kOgMax = (kHostMaxD + 1) * (kHostMaxD + kHostMaxNodes);
 constexpr int kHostWarps = 8;
 constexpr long long kHostTasks = 8192;
 constexpr int kHostGrid = 148;
 constexpr int kHostQueue = 16384;  // donated subtrees waiting for a warp
+constexpr int kHostQueueWide = 4096;  // d > kHostMaxD: paths are d bytes
 constexpr int kHostChainMax = 1024;  // improving leaves of the reference's sequential search
 constexpr unsigned long long kHostVisitBudget = 1ull << 31;
 #ifndef ORCH_HOST_SLEEP
@@ -59,19 +62,34 @@ constexpr unsigned long long kHostVisitBudget = 1ull << 31;
 #define ORCH_HOST_CHECK 63
 #endif
 
+// Per-call buffers of the multi-CTA search, sized for this d (workspace): the
+// search tables, the stored paths (d candidate positions each) and the work
+// queue; with d > kHostMaxD also the warps' DFS stacks.
+struct HostBufs {
+  int32_t* order;       // branching order (descending regret, stable)
+  int32_t* incumbent;
+  // search tables by depth k (the batch order[k])
+  int64_t* g2;          // [k][node] gain of node for order[k]
+  uint8_t* no;          // [k][j] j-th candidate: descending gain, ties by node
+  uint8_t* pos;         // [k][node] inverse of no
+  int64_t* og;          // [k][node][r] sum of the top r gains over order[k..d)
+  uint8_t* best_path;   // passes 2, 3: candidate position per depth
+  uint8_t* after_path;  // pass 3
+  uint8_t* chain_path;  // pass 4: [kHostChainMax][d]
+  unsigned* q_ready;    // pass tag | (index + 1) once published, 0 once read
+  uint16_t* q_depth;
+  uint8_t* q_path;      // [q_cap][d]
+  uint8_t* stacks;      // wide: [kHostGrid * kHostWarps][wide_stack_bytes(d)]
+};
+
 struct HostState {
   int d, c, nodes, k0;
   long long tasks;                       // nodes^k0 prefixes, numbered in DFS order
-  int64_t gain[kHostMaxD * kHostMaxD];   // [node][batch]
-  int64_t node_total[kHostMaxD];
-  int32_t order[kHostMaxD];              // branching order (descending regret, stable)
-  int32_t incumbent[kHostMaxD];
+  int wide;                              // d > kHostMaxD: tables and stacks in global memory
+  unsigned q_cap;                        // work-queue slots
+  HostBufs b;
+  int64_t node_total[kHostMaxNodes];
   int64_t incumbent_value;
-  // search tables by depth k (the batch order[k])
-  int64_t g2[kHostMaxD * kHostMaxNodes];    // [k][node] gain of node for order[k]
-  uint8_t no[kHostMaxD * kHostMaxNodes];    // [k][j] j-th candidate: descending gain, ties by node
-  uint8_t pos[kHostMaxD * kHostMaxNodes];   // [k][node] inverse of no
-  int64_t og[kOgMax];                       // [k][node][r] sum of the top r gains over order[k..d)
   unsigned long long best_value;            // pass 1 incumbent value (starts at the incumbents')
   unsigned long long visits;
   int overflow;
@@ -82,29 +100,23 @@ struct HostState {
   int idle;                                 // warps waiting for work
   int lock;
   int done_ctas;                            // pass 1 CTAs finished (the last one resets for pass 2)
-  int have_best;                            // pass 2: best_path holds a V*-leaf
-  uint8_t best_path[kHostMaxD];             // candidate position per depth
+  int have_best;                            // pass 2: b.best_path holds a V*-leaf
   unsigned long long best_key;              // passes 2, 3: least path_key of a found leaf
   int64_t best_leaf;                        // passes 2, 3: the recorded leaf's value
   // pass 3 (one link of the reference's chain of improving leaves): the first
-  // leaf after after_path (when after_depth == d) with value <= thresh
+  // leaf after b.after_path (when after_depth == d) with value <= thresh
   int64_t thresh;
   int after_depth;
-  uint8_t after_path[kHostMaxD];
   // pass 4 (the reference's visit count): chain_bound[i] is the reference's
   // incumbent value once the first i chain leaves have been offered
   int chain_len;
   int chain_done;                           // 1: complete, 2: beyond the budget or kHostChainMax
   int64_t chain_last;                       // chain_bound[chain_len]
   int64_t chain_bound[kHostChainMax + 1];
-  uint8_t chain_path[kHostChainMax][kHostMaxD];
 #ifdef ORCH_HOST_DEBUG
   unsigned long long dbg_t0, dbg_found, dbg_end, dbg_task_max, dbg_donated, dbg_first_end;
   unsigned long long dbg_visits0, dbg_visits_max;
 #endif
-  unsigned q_ready[kHostQueue];             // pass << 30 | (index + 1) once published, 0 once read
-  uint8_t q_depth[kHostQueue];
-  uint8_t q_path[kHostQueue][kHostMaxD];
 };
 
 // ----------------------------------------------------------- preparation
@@ -277,9 +289,13 @@ __device__ void prep_volume(Prep<MD>& S, int d, int64_t n, const int64_t* len, c
   __syncthreads();
 }
 
-// per warp: choice stack ch[64] (u8), then avail[64] and donated[64] (u32
-// masks), then lo[65] and hi[65] (u16, pass 4: the chain leaves below the path)
-constexpr int kWarpStack = (kHostMaxD + 2 * 4 * kHostMaxD + 2 * 2 * (kHostMaxD + 1) + 15) & ~15;
+// per warp, for depths up to md: choice stack ch[md] (u8), then avail[md] and
+// donated[md] (u32 masks), then lo[md+1] and hi[md+1] (u16, pass 4: the chain
+// leaves below the path). In shared memory (md = kHostMaxD) unless wide.
+__host__ __device__ inline size_t warp_stack_bytes(int md) {
+  return ((static_cast<size_t>(md + 3) & ~size_t{3}) + 8 * static_cast<size_t>(md) +
+          4 * static_cast<size_t>(md + 1) + 15) & ~size_t{15};
+}
 
 struct HostSmem {
   const int64_t* g2;
@@ -296,21 +312,23 @@ __host__ __device__ inline size_t host_table_bytes(int d, int c) {  // 16-byte a
   return (b + 15) & ~size_t{15};
 }
 __host__ __device__ inline size_t host_smem_bytes(int d, int c) {
-  return host_table_bytes(d, c) + kHostWarps * kWarpStack;
+  if (d > kHostMaxD) return 0;  // wide: tables and stacks stay in global memory
+  return host_table_bytes(d, c) + kHostWarps * warp_stack_bytes(kHostMaxD);
 }
 
 __device__ HostSmem host_load_tables(const HostState& H, unsigned char* raw) {
   const int d = H.d, c = H.c, nodes = H.nodes;
+  if (H.wide) return HostSmem{H.b.g2, H.b.og, H.b.no, H.b.pos};
   int64_t* g2 = reinterpret_cast<int64_t*>(raw);
   int64_t* og = g2 + d * nodes;
   uint8_t* no = reinterpret_cast<uint8_t*>(og + (d + 1) * nodes * (c + 1));
   uint8_t* pos = no + d * nodes;
   for (int i = threadIdx.x; i < d * nodes; i += blockDim.x) {
-    g2[i] = H.g2[i];
-    no[i] = H.no[i];
-    pos[i] = H.pos[i];
+    g2[i] = H.b.g2[i];
+    no[i] = H.b.no[i];
+    pos[i] = H.b.pos[i];
   }
-  for (int i = threadIdx.x; i < (d + 1) * nodes * (c + 1); i += blockDim.x) og[i] = H.og[i];
+  for (int i = threadIdx.x; i < (d + 1) * nodes * (c + 1); i += blockDim.x) og[i] = H.b.og[i];
   __syncthreads();
   return HostSmem{g2, og, no, pos};
 }
@@ -394,7 +412,7 @@ __device__ __forceinline__ void chain_step(const HostState& H, int k, int j, int
   int less = 0, same = 0;
   for (int i0 = lo; i0 < hi; i0 += 32) {
     const int i = i0 + lane;
-    const int x = i < hi ? H.chain_path[i][k] : 256;
+    const int x = i < hi ? H.b.chain_path[static_cast<size_t>(i) * H.d + k] : 256;
     less += __popc(__ballot_sync(~0u, x < j));
     same += __popc(__ballot_sync(~0u, x == j));
   }
@@ -458,7 +476,7 @@ __device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass
         int want = 0;
         if (lane == 0) {
           const unsigned queued = volatile_u32(&H.q_tail) - volatile_u32(&H.q_head);
-          want = volatile_i32(&H.idle) > static_cast<int>(queued) && queued < kHostQueue - 2048;
+          want = volatile_i32(&H.idle) > static_cast<int>(queued) && queued < H.q_cap - H.q_cap / 8;
         }
         if (__shfl_sync(~0u, want, 0)) {
           int lvl = -1;
@@ -485,22 +503,22 @@ __device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass
               slot = atomicAdd(&H.q_tail, 1u);
             }
             slot = __shfl_sync(~0u, slot, 0);
+            const unsigned qi = slot % H.q_cap;
             if (lane == 0)  // the slot's previous subtree must have been read out
-              while (volatile_u32(&H.q_ready[slot % kHostQueue]) != 0u) {
+              while (volatile_u32(&H.b.q_ready[qi]) != 0u) {
               }
             __syncwarp();
-            uint8_t* dst = H.q_path[slot % kHostQueue];
+            uint8_t* dst = H.b.q_path + static_cast<size_t>(qi) * d;
             for (int l = lane; l < lvl; l += 32) dst[l] = W.ch[l];
             if (lane == 0) {
               dst[lvl] = static_cast<uint8_t>(q);
-              H.q_depth[slot % kHostQueue] = static_cast<uint8_t>(lvl + 1);
+              H.b.q_depth[qi] = static_cast<uint16_t>(lvl + 1);
             }
             __syncwarp();
             __threadfence();
             __syncwarp();
             if (lane == 0)
-              *reinterpret_cast<volatile unsigned*>(&H.q_ready[slot % kHostQueue]) =
-                  q_tag(pass, slot);
+              *reinterpret_cast<volatile unsigned*>(&H.b.q_ready[qi]) = q_tag(pass, slot);
             W.donated[lvl] |= 1u << q;
 #ifdef ORCH_HOST_DEBUG
             if (lane == 0) atomicAdd(&H.dbg_donated, 1ull);
@@ -521,7 +539,7 @@ __device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass
       } else {
         prune = lb > vstar;
         if (!prune && after) {  // pass 3: only what sorts after the previous chain leaf
-          const int cmp = path_cmp(W.ch, H.after_path, k, lane);
+          const int cmp = path_cmp(W.ch, H.b.after_path, k, lane);
           prune = cmp < 0 || (cmp == 0 && k == d);
         }
       }
@@ -544,12 +562,12 @@ __device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass
           __syncwarp();
           __threadfence();
           const bool first = !__shfl_sync(~0u, lane == 0 ? volatile_i32(&H.have_best) : 0, 0) ||
-                             path_cmp(W.ch, H.best_path, d, lane) < 0;
+                             path_cmp(W.ch, H.b.best_path, d, lane) < 0;
 #ifdef ORCH_HOST_DEBUG
           if (lane == 0) atomicMax(&H.dbg_found, dbg_now());
 #endif
           if (first) {
-            volatile uint8_t* bp = H.best_path;
+            volatile uint8_t* bp = H.b.best_path;
             for (int l = lane; l < d; l += 32) bp[l] = W.ch[l];
             if (lane == 0) *reinterpret_cast<volatile int64_t*>(&H.best_leaf) = lb;
             __threadfence();
@@ -614,13 +632,47 @@ __device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass
 }
 
 
+// The search state after the tables are built (one thread).
+__device__ void host_init_search(HostState* H, const HostBufs& b, int d, int c, int wide,
+                                 unsigned q_cap, int64_t incumbent_value, int64_t root_lb) {
+  const int nodes = d / c;
+  H->d = d;
+  H->c = c;
+  H->nodes = nodes;
+  H->wide = wide;
+  H->q_cap = q_cap;
+  H->b = b;
+  H->incumbent_value = incumbent_value;
+  H->best_value = static_cast<unsigned long long>(incumbent_value);
+  H->visits = 0;
+  H->overflow = 0;
+  H->have_best = 0;
+  H->best_key = ~0ull;
+  int k0 = 0;
+  long long tasks = 1;
+  while (k0 < d && tasks * nodes <= kHostTasks) {
+    tasks *= nodes;
+    ++k0;
+  }
+  if (root_lb >= incumbent_value) tasks = 0;  // no leaf can beat the incumbents
+  H->k0 = k0;
+  H->tasks = tasks;
+  H->task_counter = 0;
+  H->q_head = H->q_tail = 0;
+  H->pending = static_cast<int>(tasks);
+  H->idle = 0;
+  H->lock = 0;
+  H->done_ctas = 0;
+}
+
 // One CTA: volume matrix, preparation, search state of both passes.
 __global__ void __launch_bounds__(1024, 1) k_host_setup(int d, int c, int64_t n,
                                                         const int64_t* __restrict__ len,
                                                         const int32_t* __restrict__ origin,
                                                         const int32_t* __restrict__ dest,
                                                         const int64_t* __restrict__ Vin,
-                                                        int64_t* __restrict__ Vout, HostState* H) {
+                                                        int64_t* __restrict__ Vout, HostState* H,
+                                                        HostBufs b) {
   extern __shared__ __align__(16) unsigned char setup_raw[];
   Prep<kHostMaxD>& S = *reinterpret_cast<Prep<kHostMaxD>*>(setup_raw);
   const int nodes = d / c, t = threadIdx.x;
@@ -629,44 +681,18 @@ __global__ void __launch_bounds__(1024, 1) k_host_setup(int d, int c, int64_t n,
     for (int i = t; i < d * d; i += blockDim.x) Vout[i] = static_cast<int64_t>(S.V[i]);
   prep_run(S, d, c);
   for (int i = t; i < nodes * d; i += blockDim.x) {
-    H->gain[i] = S.gain[i];
-    H->g2[i] = S.g2[i];
-    H->no[i] = S.no[i];
-    H->pos[i] = S.pos[i];
+    b.g2[i] = S.g2[i];
+    b.no[i] = S.no[i];
+    b.pos[i] = S.pos[i];
   }
-  for (int i = t; i < (d + 1) * nodes * (c + 1); i += blockDim.x) H->og[i] = S.og[i];
+  for (int i = t; i < (d + 1) * nodes * (c + 1); i += blockDim.x) b.og[i] = S.og[i];
   if (t < nodes) H->node_total[t] = S.node_total[t];
   if (t < d) {
-    H->order[t] = S.order[t];
-    H->incumbent[t] = S.incumbent[t];
+    b.order[t] = S.order[t];
+    b.incumbent[t] = S.incumbent[t];
   }
-  for (int i = t; i < kHostQueue; i += blockDim.x) H->q_ready[i] = 0u;
-  if (t == 0) {
-    H->d = d;
-    H->c = c;
-    H->nodes = nodes;
-    H->incumbent_value = S.incumbent_value;
-    H->best_value = static_cast<unsigned long long>(S.incumbent_value);
-    H->visits = 0;
-    H->overflow = 0;
-    H->have_best = 0;
-    H->best_key = ~0ull;
-    int k0 = 0;
-    long long tasks = 1;
-    while (k0 < d && tasks * nodes <= kHostTasks) {
-      tasks *= nodes;
-      ++k0;
-    }
-    if (S.root_lb >= S.incumbent_value) tasks = 0;  // no leaf can beat the incumbents
-    H->k0 = k0;
-    H->tasks = tasks;
-    H->task_counter = 0;
-    H->q_head = H->q_tail = 0;
-    H->pending = static_cast<int>(tasks);
-    H->idle = 0;
-    H->lock = 0;
-    H->done_ctas = 0;
-  }
+  for (int i = t; i < kHostQueue; i += blockDim.x) b.q_ready[i] = 0u;
+  if (t == 0) host_init_search(H, b, d, c, 0, kHostQueue, S.incumbent_value, S.root_lb);
 }
 
 __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restrict__ Hp, int pass) {
@@ -680,10 +706,13 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
 #endif
   const HostSmem T = host_load_tables(H, host_raw);
   const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  unsigned char* ws = host_raw + host_table_bytes(H.d, H.c) + warp * kWarpStack;
-  unsigned* masks = reinterpret_cast<unsigned*>(ws + kHostMaxD);
-  uint16_t* ranges = reinterpret_cast<uint16_t*>(masks + 2 * kHostMaxD);
-  WarpStack W{ws, masks, masks + kHostMaxD, ranges, ranges + kHostMaxD + 1};
+  const int md = H.wide ? H.d : kHostMaxD;
+  unsigned char* ws =
+      H.wide ? H.b.stacks + (static_cast<size_t>(blockIdx.x) * kHostWarps + warp) * warp_stack_bytes(md)
+             : host_raw + host_table_bytes(H.d, H.c) + warp * warp_stack_bytes(md);
+  unsigned* masks = reinterpret_cast<unsigned*>(ws + ((md + 3) & ~3));
+  uint16_t* ranges = reinterpret_cast<uint16_t*>(masks + 2 * md);
+  WarpStack W{ws, masks, masks + md, ranges, ranges + md + 1};
   const int64_t vstar = pass == 3 ? H.thresh : static_cast<int64_t>(H.best_value);
   const int c = H.c, nodes = H.nodes, k0 = H.k0;
   const int kb = nodes > 1 ? 32 - __clz(nodes - 1) : 1, km = H.d < 64 / kb ? H.d : 64 / kb;
@@ -766,15 +795,15 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
       }
       root = k0;
     } else {  // donated subtree: wait until published, then replay its path
-      const unsigned slot = static_cast<unsigned>(qs) % kHostQueue;
+      const unsigned slot = static_cast<unsigned>(qs) % H.q_cap;
       const unsigned want = q_tag(pass, static_cast<unsigned>(qs));
       if (lane == 0)
-        while (volatile_u32(&H.q_ready[slot]) != want) {
+        while (volatile_u32(&H.b.q_ready[slot]) != want) {
         }
       __syncwarp();
       __threadfence();
-      root = *reinterpret_cast<volatile uint8_t*>(&H.q_depth[slot]);
-      const volatile uint8_t* src = H.q_path[slot];
+      root = *reinterpret_cast<volatile uint16_t*>(&H.b.q_depth[slot]);
+      const volatile uint8_t* src = H.b.q_path + static_cast<size_t>(slot) * H.d;
       for (int k = 0; k < root; ++k) {
         const int j = src[k];
         W.ch[k] = static_cast<uint8_t>(j);
@@ -787,7 +816,7 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
       __syncwarp();
       __threadfence();
       if (lane == 0)  // path copied out: the slot may be reused
-        *reinterpret_cast<volatile unsigned*>(&H.q_ready[slot]) = 0u;
+        *reinterpret_cast<volatile unsigned*>(&H.b.q_ready[slot]) = 0u;
     }
     __syncwarp();
     if (ok && (pass == 2 || pass == 3) &&
@@ -878,7 +907,8 @@ __global__ void k_host_reset(HostState* H, int mode) {
       return;
     }
     const int i = H->chain_len, d = H->d;
-    for (int l = 0; l < d; ++l) H->chain_path[i][l] = H->after_path[l] = H->best_path[l];
+    for (int l = 0; l < d; ++l)
+      H->b.chain_path[static_cast<size_t>(i) * d + l] = H->b.after_path[l] = H->b.best_path[l];
     H->chain_bound[i + 1] = H->chain_last = H->best_leaf;
     H->chain_len = i + 1;
     // a link at pass 1's optimum is the last: nothing after it can be lower
@@ -945,10 +975,10 @@ __global__ void __launch_bounds__(1024, 1) k_host_finish(const HostState* __rest
     if (t <= d) F.ooff[t] = r.bin_offset[t];
     for (int64_t i = t; i < r.n; i += blockDim.x) mem[i] = r.bin_member[i];
   }
-  if (t < d) F.a[t] = H.incumbent[t];
+  if (t < d) F.a[t] = H.b.incumbent[t];
   if (t < nodes) F.e[t] = F.e0[t] = 0;
   __syncthreads();
-  if (!incumbent && t < d) F.a[H.order[t]] = H.no[t * nodes + H.best_path[t]];
+  if (!incumbent && t < d) F.a[H.b.order[t]] = H.b.no[t * nodes + H.b.best_path[t]];
   __syncthreads();
   if (t == 0) {
     int next[kHostMaxNodes];
@@ -1315,20 +1345,323 @@ bool nodewise_small_fits(int d, int c, int64_t n) {
   return leaves <= kNwMaxLeaves;
 }
 
-int check_hosting_args(int d, int c) {
+// ------------------------------------------------- wide setup and finish
+// d > kHostMaxD (up to ORCH_MAX_INSTANCES, e.g. C4's 2560): the same tables as
+// prep_run, built by grid-wide kernels in global memory (V alone is d^2 words),
+// for orch_solve_hosting_host. Scratch per call:
+struct WideScratch {
+  int64_t* gain;           // [node][batch]
+  int64_t* regret;         // [batch]
+  int32_t* at;             // [batch] position in the branching order
+  int32_t* srt_at;         // [node][rank]: order position of the node's rank-th largest gain
+  int64_t* srt_g;          // [node][rank]: that gain
+  int32_t* greedy;         // [batch]
+  unsigned long long* sub; // [4][nodes]: identity, greedy gains kept; solution, identity egress
+  int32_t* a;              // [batch] final node
+};
+
+__global__ void k_hw_gain(const int64_t* __restrict__ V, int d, int c, int64_t* __restrict__ gain) {
+  const int nodes = d / c;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < static_cast<int64_t>(nodes) * d; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int nd = static_cast<int>(i / d), b = static_cast<int>(i % d);
+    int64_t g = 0;
+    for (int r = nd * c; r < (nd + 1) * c; ++r) g += V[static_cast<size_t>(r) * d + b];
+    gain[i] = g;
+  }
+}
+
+// regret per batch (top - second gain over the nodes); node totals (block 0)
+__global__ void k_hw_regret(const int64_t* __restrict__ gain, int d, int nodes,
+                            int64_t* __restrict__ regret, HostState* H) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < d) {
+    int64_t top = 0, second = 0;
+    for (int nd = 0; nd < nodes; ++nd) {
+      const int64_t g = gain[static_cast<size_t>(nd) * d + b];
+      if (g > top) {
+        second = top;
+        top = g;
+      } else if (g > second) {
+        second = g;
+      }
+    }
+    regret[b] = top - second;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // node totals: one warp per node, in turn
+    for (int nd = 0; nd < nodes; ++nd) {
+      int64_t t = 0;
+      for (int x = threadIdx.x; x < d; x += 32) t += gain[static_cast<size_t>(nd) * d + x];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(~0u, t, o);
+      if (threadIdx.x == 0) H->node_total[nd] = t;
+    }
+  }
+}
+
+// stable order by descending regret (topology.cpp:212-228): rank by counting
+__global__ void k_hw_order(const int64_t* __restrict__ regret, int d, int32_t* __restrict__ order,
+                           int32_t* __restrict__ at) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d) return;
+  const int64_t mine = regret[b];
+  int r = 0;
+  for (int x = 0; x < d; ++x) {
+    const int64_t o = regret[x];
+    r += o > mine || (o == mine && x < b);
+  }
+  order[r] = b;
+  at[b] = r;
+}
+
+// per depth k: candidate nodes by descending gain for order[k], ties by node
+__global__ void k_hw_tables(const int64_t* __restrict__ gain, const int32_t* __restrict__ order,
+                            int d, int nodes, int64_t* __restrict__ g2, uint8_t* __restrict__ no,
+                            uint8_t* __restrict__ pos) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d) return;
+  const int b = order[k];
+  int64_t g[kHostMaxNodes];
+  uint8_t srt[kHostMaxNodes];
+  for (int nd = 0; nd < nodes; ++nd) {
+    g[nd] = gain[static_cast<size_t>(nd) * d + b];
+    g2[static_cast<size_t>(k) * nodes + nd] = g[nd];
+    int j = nd - 1;
+    while (j >= 0 && g[srt[j]] < g[nd]) {
+      srt[j + 1] = srt[j];
+      --j;
+    }
+    srt[j + 1] = static_cast<uint8_t>(nd);
+  }
+  for (int j = 0; j < nodes; ++j) {
+    no[static_cast<size_t>(k) * nodes + j] = srt[j];
+    pos[static_cast<size_t>(k) * nodes + srt[j]] = static_cast<uint8_t>(j);
+  }
+}
+
+// per node: its gains in descending order (ties by batch) with their order positions
+__global__ void k_hw_sorted(const int64_t* __restrict__ gain, const int32_t* __restrict__ at, int d,
+                            int nodes, int32_t* __restrict__ srt_at, int64_t* __restrict__ srt_g) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < static_cast<int64_t>(nodes) * d; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int nd = static_cast<int>(i / d), b = static_cast<int>(i % d);
+    const int64_t* row = gain + static_cast<size_t>(nd) * d;
+    const int64_t mine = row[b];
+    int r = 0;
+    for (int x = 0; x < d; ++x) r += row[x] > mine || (row[x] == mine && x < b);
+    srt_at[static_cast<size_t>(nd) * d + r] = at[b];
+    srt_g[static_cast<size_t>(nd) * d + r] = mine;
+  }
+}
+
+// og[k][node][r]: the node's r largest gains among order[k..d) (r <= c)
+__global__ void k_hw_og(const int32_t* __restrict__ srt_at, const int64_t* __restrict__ srt_g, int d,
+                        int nodes, int c, int64_t* __restrict__ og) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < static_cast<int64_t>(nodes) * (d + 1); i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int nd = static_cast<int>(i / (d + 1)), k = static_cast<int>(i % (d + 1));
+    int64_t* out = og + (static_cast<size_t>(k) * nodes + nd) * (c + 1);
+    const int32_t* sa = srt_at + static_cast<size_t>(nd) * d;
+    const int64_t* sg = srt_g + static_cast<size_t>(nd) * d;
+    int64_t acc = 0;
+    int r = 0;
+    out[0] = 0;
+    for (int x = 0; x < d && r < c; ++x)
+      if (sa[x] >= k) {
+        acc += sg[x];
+        out[++r] = acc;
+      }
+    while (r < c) out[++r] = acc;
+  }
+}
+
+// greedy incumbent (topology.cpp:238-254), one warp: the gains of 32 depths at
+// a time staged in shared memory, then the sequential picks
+__global__ void k_hw_greedy(const int64_t* __restrict__ g2, const int32_t* __restrict__ order, int d,
+                            int nodes, int c, int32_t* __restrict__ greedy) {
+  __shared__ int64_t tile[32 * kHostMaxNodes];
+  const int lane = threadIdx.x;
+  int room = lane < nodes ? c : 0;
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    const int kn = d - k0 < 32 ? d - k0 : 32;
+    for (int i = lane; i < kn * nodes; i += 32) tile[i] = g2[static_cast<size_t>(k0) * nodes + i];
+    __syncwarp();
+    for (int k = 0; k < kn; ++k) {
+      const int pick = warp_argmax_first(room > 0 ? tile[k * nodes + lane] : -1);
+      if (lane == pick) {
+        --room;
+        greedy[order[k0 + k]] = pick;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// kept gains of the identity (sub[0]) and greedy (sub[1]) hostings
+__global__ void k_hw_values(const int64_t* __restrict__ gain, const int32_t* __restrict__ greedy,
+                            int d, int c, unsigned long long* __restrict__ sub) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d) return;
+  const int nodes = d / c, ni = b / c, ng = greedy[b];
+  atomicAdd(&sub[ni], static_cast<unsigned long long>(gain[static_cast<size_t>(ni) * d + b]));
+  atomicAdd(&sub[nodes + ng], static_cast<unsigned long long>(gain[static_cast<size_t>(ng) * d + b]));
+}
+
+// incumbent values, the bound at the root, the search state (one thread)
+__global__ void k_hw_init(HostState* H, HostBufs b, int d, int c,
+                          const unsigned long long* __restrict__ sub, int* __restrict__ g_better) {
+  const int nodes = d / c;
+  int64_t vi = INT64_MIN, vg = INT64_MIN, root = 0;
+  for (int nd = 0; nd < nodes; ++nd) {
+    const int64_t t = H->node_total[nd];
+    const int64_t ei = t - static_cast<int64_t>(sub[nd]), eg = t - static_cast<int64_t>(sub[nodes + nd]);
+    vi = ei > vi ? ei : vi;
+    vg = eg > vg ? eg : vg;
+    const int64_t e = t - b.og[static_cast<size_t>(nd) * (c + 1) + c];
+    root = e > root ? e : root;
+  }
+  *g_better = vg < vi;  // offer(greedy) replaces only when strictly better
+  host_init_search(H, b, d, c, 1, kHostQueueWide, vg < vi ? vg : vi, root);
+}
+
+__global__ void k_hw_incumbent(const int32_t* __restrict__ greedy, const int* __restrict__ g_better,
+                               int d, int c, int32_t* __restrict__ incumbent,
+                               unsigned* __restrict__ q_ready) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d) incumbent[i] = *g_better ? greedy[i] : i / c;
+  if (i < kHostQueueWide) q_ready[i] = 0u;
+}
+
+// final hosting and batch -> instance map (topology.cpp:283-290), one CTA
+__global__ void k_hw_assign(const HostState* __restrict__ Hp, int32_t* __restrict__ a,
+                            int32_t* __restrict__ hosting, int32_t* __restrict__ b2i,
+                            unsigned long long* __restrict__ e) {
+  const HostState& H = *Hp;
+  const int d = H.d, c = H.c, nodes = H.nodes;
+  const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value || H.overflow ||
+                         !H.have_best;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    const int v = incumbent ? H.b.incumbent[t]
+                            : H.b.no[static_cast<size_t>(t) * nodes + H.b.best_path[t]];
+    a[incumbent ? t : H.b.order[t]] = v;
+  }
+  if (threadIdx.x < 2 * nodes) e[threadIdx.x] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < d; t += blockDim.x) hosting[t] = a[t];
+  if (threadIdx.x == 0) {
+    int next[kHostMaxNodes];
+    for (int nd = 0; nd < nodes; ++nd) next[nd] = nd * c;
+    for (int x = 0; x < d; ++x) b2i[x] = next[a[x]]++;
+  }
+}
+
+// inter_node_egress of the solution (e[0..nodes)) and of the identity (e[nodes..))
+__global__ void k_hw_egress(const int64_t* __restrict__ V, const int32_t* __restrict__ a, int d,
+                            int c, unsigned long long* __restrict__ e) {
+  const int nodes = d / c;
+  __shared__ unsigned long long acc[2 * kHostMaxNodes];
+  if (threadIdx.x < 2 * kHostMaxNodes) acc[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < static_cast<int64_t>(d) * d; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int src = static_cast<int>(i / d), b = static_cast<int>(i % d), nd = src / c;
+    const unsigned long long v = static_cast<unsigned long long>(V[i]);
+    if (v) {
+      if (a[b] != nd) atomicAdd(&acc[nd], v);
+      if (b / c != nd) atomicAdd(&acc[nodes + nd], v);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * nodes && acc[threadIdx.x]) atomicAdd(&e[threadIdx.x], acc[threadIdx.x]);
+}
+
+__global__ void k_hw_info(const HostState* __restrict__ Hp, const unsigned long long* __restrict__ e,
+                          int64_t* __restrict__ info) {
+  const HostState& H = *Hp;
+  const int nodes = H.nodes;
+  const bool incumbent = static_cast<long long>(H.best_value) >= H.incumbent_value || H.overflow ||
+                         !H.have_best;
+  unsigned long long worst = 0, base = 0;
+  for (int nd = 0; nd < nodes; ++nd) {
+    worst = e[nd] > worst ? e[nd] : worst;
+    base = e[nodes + nd] > base ? e[nodes + nd] : base;
+  }
+  info[0] = static_cast<int64_t>(worst);
+  info[1] = static_cast<int64_t>(base);
+  info[2] = H.overflow ? -1 : (incumbent ? 0 : 1);
+  info[3] = static_cast<int64_t>(H.visits);
+}
+
+// setup, both passes and the finish of the wide search; V on the device
+int run_wide_hosting(orch_ctx* ctx, int d, int c, const int64_t* V, HostState* H, const HostBufs& hb,
+                     const WideScratch& w, int32_t* hosting, int32_t* b2i, int64_t* info,
+                     int* g_better, cudaStream_t st) {
+  const int nodes = d / c, T = 256;
+  const int nb = (d + T - 1) / T;
+  const int grid = kSMs * 8;
+  ORCH_CUDA_TRY(cudaMemsetAsync(w.sub, 0, sizeof(unsigned long long) * 4 * kHostMaxNodes, st));
+  k_hw_gain<<<grid, T, 0, st>>>(V, d, c, w.gain);
+  k_hw_regret<<<nb, T, 0, st>>>(w.gain, d, nodes, w.regret, H);
+  k_hw_order<<<nb, T, 0, st>>>(w.regret, d, hb.order, w.at);
+  k_hw_tables<<<nb, T, 0, st>>>(w.gain, hb.order, d, nodes, hb.g2, hb.no, hb.pos);
+  k_hw_sorted<<<grid, T, 0, st>>>(w.gain, w.at, d, nodes, w.srt_at, w.srt_g);
+  k_hw_og<<<grid, T, 0, st>>>(w.srt_at, w.srt_g, d, nodes, c, hb.og);
+  k_hw_greedy<<<1, 32, 0, st>>>(hb.g2, hb.order, d, nodes, c, w.greedy);
+  k_hw_values<<<nb, T, 0, st>>>(w.gain, w.greedy, d, c, w.sub);
+  k_hw_init<<<1, 1, 0, st>>>(H, hb, d, c, w.sub, g_better);
+  k_hw_incumbent<<<(kHostQueueWide > d ? kHostQueueWide + T - 1 : d + T - 1) / T, T, 0, st>>>(
+      w.greedy, g_better, d, c, hb.incumbent, hb.q_ready);
+  k_host_bb<<<kHostGrid, kHostWarps * 32, 0, st>>>(H, 1);
+  k_host_bb<<<kHostGrid, kHostWarps * 32, 0, st>>>(H, 2);
+  k_hw_assign<<<1, 1024, 0, st>>>(H, w.a, hosting, b2i, w.sub + 2 * kHostMaxNodes);
+  k_hw_egress<<<grid, T, 0, st>>>(V, w.a, d, c, w.sub + 2 * kHostMaxNodes);
+  k_hw_info<<<1, 1, 0, st>>>(H, w.sub + 2 * kHostMaxNodes, info);
+  ctx->launches += 15;
+  ORCH_CUDA_TRY(cudaGetLastError());
+  return ORCH_OK;
+}
+
+// max_d: kHostMaxD for orch_nodewise (its finish remaps the balance in shared
+// memory), ORCH_MAX_INSTANCES for orch_solve_hosting_host
+int check_hosting_args(int d, int c, int max_d = kHostMaxD) {
   if (d < 1 || c < 1)
     return fail(ORCH_INVALID_ARGUMENT, "topology needs at least one instance and one per node");
   if (d % c) return fail(ORCH_INVALID_ARGUMENT, "instance count must be divisible by instances per node");
-  if (d > kHostMaxD) return fail(ORCH_UNSUPPORTED, "node-wise hosting limited to d <= 64 on the device");
+  if (d > max_d)
+    return fail(ORCH_UNSUPPORTED, max_d == kHostMaxD
+                                      ? "orch_nodewise limited to d <= 64 on the device"
+                                      : "node-wise hosting limited to d <= 4096 on the device");
   if (d / c > kHostMaxNodes)
     return fail(ORCH_UNSUPPORTED, "node-wise hosting limited to 32 nodes on the device");
   return ORCH_OK;
 }
 
+// the search state and its per-call buffers (tables, paths, queue; wide: stacks)
+void plan_host_search(Plan& p, int d, int c, HostState** H, HostBufs* b) {
+  const size_t nodes = static_cast<size_t>(d / c), dd = static_cast<size_t>(d);
+  const bool wide = d > kHostMaxD;
+  const size_t q_cap = wide ? kHostQueueWide : kHostQueue;
+  p.add(H, 1);
+  p.add(&b->order, dd);
+  p.add(&b->incumbent, dd);
+  p.add(&b->g2, dd * nodes);
+  p.add(&b->no, dd * nodes);
+  p.add(&b->pos, dd * nodes);
+  p.add(&b->og, (dd + 1) * nodes * static_cast<size_t>(c + 1));
+  p.add(&b->best_path, dd);
+  p.add(&b->after_path, dd);
+  p.add(&b->chain_path, static_cast<size_t>(kHostChainMax) * dd);
+  p.add(&b->q_ready, q_cap);
+  p.add(&b->q_depth, q_cap);
+  p.add(&b->q_path, q_cap * dd);
+  b->stacks = nullptr;
+  if (wide) p.add(&b->stacks, static_cast<size_t>(kHostGrid) * kHostWarps * warp_stack_bytes(d));
+}
+
 // setup + both passes of the multi-CTA search (V from the items, or given)
 int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t* len,
                           const int32_t* origin, const int32_t* dest, const int64_t* Vin,
-                          int64_t* Vout, HostState* H, cudaStream_t st) {
+                          int64_t* Vout, HostState* H, const HostBufs& b, cudaStream_t st) {
   const int sm = static_cast<int>(host_smem_bytes(d, c));
   static PerDeviceOnce configured;
   const int rc_attr = configured([&]() -> int {
@@ -1341,7 +1674,8 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
     return ORCH_OK;
   });
   if (rc_attr) return rc_attr;
-  k_host_setup<<<1, 1024, sizeof(Prep<kHostMaxD>), st>>>(d, c, n, len, origin, dest, Vin, Vout, H);
+  k_host_setup<<<1, 1024, sizeof(Prep<kHostMaxD>), st>>>(d, c, n, len, origin, dest, Vin, Vout, H,
+                                                          b);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
   k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
   ctx->launches += 3;
@@ -1408,26 +1742,47 @@ extern "C" {
 int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
                             int32_t* h_hosting, int64_t* h_info, void* stream) {
   if (!ctx) return fail(ORCH_INVALID_ARGUMENT, "null context");
-  int rc = check_hosting_args(d, c);
+  int rc = check_hosting_args(d, c, ORCH_MAX_INSTANCES);
   if (rc) return rc;
   ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
   auto st = static_cast<cudaStream_t>(stream);
+  const bool wide = d > kHostMaxD;
+  const size_t dd = static_cast<size_t>(d), nodes = static_cast<size_t>(d / c);
   int64_t *V, *info;
   int32_t *hosting, *b2i;
+  int* g_better = nullptr;
   HostState* H;
+  HostBufs hb;
+  WideScratch w{};
   Plan all;
-  all.add(&V, static_cast<size_t>(d) * d);
+  all.add(&V, dd * dd);
   all.add(&info, 4);
-  all.add(&hosting, d);
-  all.add(&b2i, d);
-  all.add(&H, 1);
+  all.add(&hosting, dd);
+  all.add(&b2i, dd);
+  plan_host_search(all, d, c, &H, &hb);
+  if (wide) {
+    all.add(&w.gain, nodes * dd);
+    all.add(&w.regret, dd);
+    all.add(&w.at, dd);
+    all.add(&w.srt_at, nodes * dd);
+    all.add(&w.srt_g, nodes * dd);
+    all.add(&w.greedy, dd);
+    all.add(&w.sub, 4 * static_cast<size_t>(kHostMaxNodes));
+    all.add(&w.a, dd);
+    all.add(&g_better, 1);
+  }
   rc = all.commit(ctx, st);
   if (rc) return rc;
-  ORCH_CUDA_TRY(cudaMemcpyAsync(V, h_V, sizeof(int64_t) * d * d, cudaMemcpyHostToDevice, st));
-  rc = launch_hosting_search(ctx, d, c, 0, nullptr, nullptr, nullptr, V, nullptr, H, st);
-  if (rc) return rc;
-  k_host_finish<<<1, 1024, 0, st>>>(H, V, hosting, b2i, info, RemapArgs{});
-  ctx->launches += 1;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(V, h_V, sizeof(int64_t) * dd * dd, cudaMemcpyHostToDevice, st));
+  if (wide) {
+    rc = run_wide_hosting(ctx, d, c, V, H, hb, w, hosting, b2i, info, g_better, st);
+    if (rc) return rc;
+  } else {
+    rc = launch_hosting_search(ctx, d, c, 0, nullptr, nullptr, nullptr, V, nullptr, H, hb, st);
+    if (rc) return rc;
+    k_host_finish<<<1, 1024, 0, st>>>(H, V, hosting, b2i, info, RemapArgs{});
+    ctx->launches += 1;
+  }
   ORCH_CUDA_TRY(cudaGetLastError());
   ORCH_CUDA_TRY(cudaMemcpyAsync(h_hosting, hosting, sizeof(int32_t) * d, cudaMemcpyDeviceToHost, st));
   int64_t hinfo[4];
@@ -1495,17 +1850,18 @@ int orch_nodewise(orch_ctx* ctx, int32_t d, int32_t c, int64_t n, const int64_t*
   Plan plan;
   int64_t* V;
   HostState* H;
+  HostBufs hb;
   int32_t *hosting, *b2i, *scratch = nullptr;
   int64_t* info;
   plan.add(&V, static_cast<size_t>(d) * d);
-  plan.add(&H, 1);
+  plan_host_search(plan, d, c, &H, &hb);
   plan.add_or(&hosting, d_hosting, d);
   plan.add_or(&b2i, d_batch_to_instance, d);
   plan.add_or(&info, d_info, 4);
   if (n > kFinMaxItems) plan.add(&scratch, static_cast<size_t>(n));
   rc = plan.commit(ctx, st);
   if (rc) return rc;
-  rc = launch_hosting_search(ctx, d, c, n, d_len, d_origin, bal->dest_inst, nullptr, V, H, st);
+  rc = launch_hosting_search(ctx, d, c, n, d_len, d_origin, bal->dest_inst, nullptr, V, H, hb, st);
   if (rc) return rc;
   RemapArgs r{n, bal->dest_inst, bal->bin_count, bal->bin_len, bal->bin_tokens, bal->bin_cost,
               bal->bin_offset, bal->bin_member, scratch};

@@ -122,15 +122,49 @@ def test_solve_hosting_random_larger(ctx, oracle):
 
 def test_hosting_limits(ctx):
     from paper_2503_23830_b200.capi import OrchError
-    with pytest.raises(OrchError) as e:
+    with pytest.raises(OrchError) as e:  # 64 nodes: lane = node
         ctx.solve_hosting(64, 1, np.zeros((64, 64), np.int64))
-    assert e.value.code == 12
-    with pytest.raises(OrchError) as e:
-        ctx.solve_hosting(72, 8, np.zeros((72, 72), np.int64))
     assert e.value.code == 12
     with pytest.raises(OrchError) as e:
         ctx.solve_hosting(6, 4, np.zeros((6, 6), np.int64))
     assert e.value.code == 1
+    # orch_nodewise (the in-place relabelling of a balance) stays at d <= 64
+    rng = np.random.default_rng(1)
+    L, O = random_instance(rng, 72, 300)
+    Lt, Ot = torch.from_numpy(L).cuda(), torch.from_numpy(O).cuda()
+    bal = ctx.balance(0, 72, Lt, Ot)
+    with pytest.raises(OrchError) as e:
+        ctx.nodewise(72, 8, Lt, Ot, bal)
+    assert e.value.code == 12
+
+
+def test_solve_hosting_wide_fixtures(ctx):
+    """d = 72..256 (tables and warp stacks in global memory) against the
+    reference's answers and visit counts (tests/golden/ref_hosting_wide.npz)."""
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting_wide.npz"))
+    for k in range(len(f["d"])):
+        d, c = int(f["d"][k]), int(f["c"][k])
+        a = ctx.solve_hosting(d, c, f["V"][k][:d, :d])
+        np.testing.assert_array_equal(a["hosting"], f["hosting"][k][:d])
+        assert a["max_egress"] == f["max_egress"][k]
+        assert a["visited"] == f["visited"][k], (k, d, c)
+
+
+def test_solve_hosting_c4(ctx, oracle):
+    """C4 (d = 2560): the vision phase's volume matrix (the reference greedy's
+    balance, rebuilt here by the oracle) hosted on 2 and 32 nodes -- the
+    reference's hosting, egress and nodes_visited."""
+    import bench_configs as bc
+    cfg = bc.CONFIGS["C4x30"]
+    name, L, O, kind, lam, v = next(iter(cfg["phases"]()))
+    r = oracle.balance(kind, cfg["d"], L, O, lam=lam, v=v)
+    V = oracle.volume_matrix(cfg["d"], L, O, r.dest_inst)
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting_wide.npz"))
+    for k, c in enumerate(f["c4_c"]):
+        a = ctx.solve_hosting(2560, int(c), V)
+        np.testing.assert_array_equal(a["hosting"], f["c4_hosting"][k])
+        assert a["max_egress"] == f["c4_max_egress"][k]
+        assert a["visited"] == f["c4_visited"][k]
 
 
 def test_solve_hosting_repeated(ctx):

@@ -167,6 +167,17 @@ def test_hosting_fixtures(oracle):
         assert a["visited"] == f["visited"][k]
 
 
+def test_hosting_wide_fixtures(oracle):
+    """d = 72..256 volume matrices (make_hosting_wide_golden.py)."""
+    f = np.load(os.path.join(HERE, "golden", "ref_hosting_wide.npz"))
+    for k in range(len(f["d"])):
+        d, c = int(f["d"][k]), int(f["c"][k])
+        a = oracle.solve_hosting(d, c, f["V"][k][:d, :d])
+        np.testing.assert_array_equal(a["hosting"], f["hosting"][k][:d])
+        assert a["max_egress"] == f["max_egress"][k]
+        assert a["visited"] == f["visited"][k]
+
+
 def test_hosting_c3_fixtures(oracle):
     """DP=64 (C3) phase volume matrices on 2/4/8 GPUs (make_hosting_c3_golden.py)."""
     f = np.load(os.path.join(HERE, "golden", "ref_hosting_c3.npz"))
