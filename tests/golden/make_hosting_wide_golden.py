@@ -2,7 +2,7 @@
 (oracle/_ref) beyond d = 64: random volume matrices at d = 72..256 (kept when the
 reference's sequential search finishes in 5 s), and the C4 (d = 2560) vision
 phase's volume matrix -- rebuilt by the test from bench_configs through the
-oracle, so only its answers are stored -- on 2 and 32 nodes."""
+oracle, so only its answers are stored -- on 2, 16 and 32 nodes."""
 import os
 import sys
 
@@ -52,7 +52,7 @@ def main():
         vis.append(r["visited"])
     V4 = c4_vision_volume(orc)
     c4c, c4h, c4m, c4v = [], [], [], []
-    for c in (1280, 80):
+    for c in (1280, 160, 80):
         r = ref.solve_hosting(2560, c, V4)
         c4c.append(c)
         c4h.append(r["hosting"])

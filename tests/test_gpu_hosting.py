@@ -152,7 +152,7 @@ def test_solve_hosting_wide_fixtures(ctx):
 
 def test_solve_hosting_c4(ctx, oracle):
     """C4 (d = 2560): the vision phase's volume matrix (the reference greedy's
-    balance, rebuilt here by the oracle) hosted on 2 and 32 nodes -- the
+    balance, rebuilt here by the oracle) hosted on 2, 16 and 32 nodes -- the
     reference's hosting, egress and nodes_visited."""
     import bench_configs as bc
     cfg = bc.CONFIGS["C4x30"]
