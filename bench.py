@@ -538,42 +538,71 @@ def run_b200(args):
 
     # end-to-end through the C-ABI with host buffers: each step copies its
     # metadata from pinned host memory and reads back its assignment vectors
-    # and summaries, and completes before the next one starts (no overlap).
+    # and summaries. Two steps are in flight, as in a training loop's input
+    # pipeline: the host waits for step i's results (on the host) after issuing
+    # step i + 1, so step i + 1's copies and metadata overlap step i's rows;
+    # --e2e-sync completes every step before the next one starts.
     if comm_meta is None:
         h2d = sum(s["h_glen"].numel() * 8 + s["h_gorg"].numel() * 4 for s in st)
     else:
         h2d = sum(s["h_pos"].numel() * 8 + s["h_len"].numel() * 8 + s["h_org"].numel() * 4
                   for s in st)
     d2h = sum(s["n"] * 8 + 128 for s in st)
-    host_out = [(torch.empty(s["n"], dtype=torch.int32).pin_memory(),
-                 torch.empty(s["n"], dtype=torch.int32).pin_memory(),
-                 torch.empty(128, dtype=torch.uint8).pin_memory()) for s in st]
+    host_out = [[(torch.empty(s["n"], dtype=torch.int32).pin_memory(),
+                  torch.empty(s["n"], dtype=torch.int32).pin_memory(),
+                  torch.empty(128, dtype=torch.uint8).pin_memory()) for s in st]
+                for _ in range(2)]  # one set per buffer parity: two steps in flight
+    in_flight = []
 
-    def e2e_step():
+    def e2e_step(sync):
         b = step(h2d=True)
-        for s, (hi, hs, hsum) in zip(st, host_out):
+        done = []
+        for s, (hi, hs, hsum) in zip(st, host_out[b]):
             with torch.cuda.stream(s["ms"]):
                 bal = s["buf"][b]["bal"]
                 hi.copy_(bal.dest_inst[:s["n"]], non_blocking=True)
                 hs.copy_(bal.dest_slot[:s["n"]], non_blocking=True)
                 hsum[:bal.summary_raw.numel()].copy_(bal.summary_raw, non_blocking=True)
-        for ms in meta_streams:
-            ms.synchronize()
-        data_stream.synchronize()
+                ev = torch.cuda.Event()
+                ev.record(s["ms"])
+                done.append(ev)
+        ev = torch.cuda.Event()
+        ev.record(data_stream)
+        done.append(ev)
+        in_flight.append(done)
+        # step i - 1's results are on the host (step i's when synchronous)
+        while len(in_flight) > (0 if sync else 1):
+            for ev in in_flight.pop(0):
+                ev.synchronize()
 
-    for _ in range(max(args.warmup, 10)):
-        e2e_step()
-    barrier()
-    # the timed host loop runs without the cyclic garbage collector, so a
-    # collection pass cannot land inside the K synchronous steps
-    gc.collect()
-    gc.disable()
-    w0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - w0)
-    gc.enable()
+    def e2e_drain():
+        while in_flight:
+            for ev in in_flight.pop(0):
+                ev.synchronize()
+
+    def e2e_run(sync):
+        for _ in range(max(args.warmup, 10)):
+            e2e_step(sync)
+        e2e_drain()
+        barrier()
+        # the timed host loop runs without the cyclic garbage collector, so a
+        # collection pass cannot land inside the K steps
+        gc.collect()
+        gc.disable()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step(sync)
+        e2e_drain()
+        barrier()
+        secs = max_over_ranks(time.perf_counter() - w0)
+        gc.enable()
+        return secs
+
+    # both loops are measured; the line's e2e is the pipelined one unless
+    # --e2e-sync, and carries the other as e2e.sync_value / e2e.pipelined_value
+    e2e_sync_s = e2e_run(True)
+    e2e_pipe_s = e2e_run(False)
+    e2e_s = e2e_sync_s if args.e2e_sync else e2e_pipe_s
     if os.environ.get("ORCH_BENCH_TRACE"):  # the metadata sub-steps of the last e2e steps
         mm = meta_marks[-5 * 2 * len(st):]
         for i in range(0, len(mm), 5):
@@ -606,9 +635,14 @@ def run_b200(args):
                      "share_of_step": disp_ms / (t0.elapsed_time(t1) or 1.0)},
         "e2e": {"value": tokens * args.steps / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "note": "C-ABI with host metadata buffers, one synchronous step at a time; "
+                "note": ("C-ABI with host metadata buffers, one synchronous step at a time; "
+                         if args.e2e_sync else
+                         "C-ABI with host metadata buffers, two steps in flight (the host "
+                         "waits for step i's results after issuing step i+1); ") +
                         "token rows are device-resident activations (encoder/embedding "
-                        "outputs)"},
+                        "outputs)",
+                "sync_value": tokens * args.steps / e2e_sync_s,
+                "pipelined_value": tokens * args.steps / e2e_pipe_s},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
@@ -703,6 +737,8 @@ def main():
                          "the round-1 path that reads the counts on the data stream (nccl-sync)")
     ap.add_argument("--nccl-register", action="store_true",
                     help="--exchange nccl*: ncclCommRegister the row buffers")
+    ap.add_argument("--e2e-sync", action="store_true",
+                    help="e2e: complete every step before the next (default: two in flight)")
     args = ap.parse_args()
     CFG.clear()
     CFG.update(CONFIGS[args.config], name=args.config)
