@@ -360,12 +360,13 @@ def run_b200(args):
     # N>1 put: the phases of a step share one window (one barrier, one release),
     # each phase's output at its own offset
     win = None
-    if P > 1 and args.exchange == "put":
+    if P > 1 and args.exchange in ("put", "put-nccl"):
         off = 0
         for s in st:
             s["win_off"] = off
             off += s["wrows"] * R
-        win = Window(ctx_data, comm_data, off)
+        win = Window(ctx_data, comm_data, off,
+                     backend="nccl" if args.exchange == "put-nccl" else "ipc")
         wview = win.tensor_view(dev)
         for s in st:
             s["rout"] = wview[s["win_off"]:s["win_off"] + s["wrows"] * R]
@@ -672,6 +673,9 @@ def run_b200(args):
         line["roofline"] = {"bound": "nvlink", "achieved": busbw, "peak": nv["copy_engine"],
                             "unit": "GB/s", "frac": busbw / nv["copy_engine"], "traffic": None,
                             "kernel": {"put": "k_move_tma<kPut> (orch_put)",
+                                       "put-nccl": "k_move_tma<kPut> (orch_put) into NCCL "
+                                                   "symmetric-memory windows "
+                                                   "(orch_window_create_nccl)",
                                        "nccl": "pack + ncclSend/ncclRecv per peer + unpack, host "
                                                "counts from the metadata stream "
                                                "(orch_dispatch_nccl)",
@@ -731,8 +735,9 @@ def main():
                     help="N>1 put: the per-step barrier through the window's peer memory "
                          "(default), a 1-int ncclAllReduce, or none (diagnostics only)")
     ap.add_argument("--exchange", default="put",
-                    choices=["put", "nccl", "nccl-direct", "nccl-sync"],
-                    help="N>1: fused pack+put over NVLink (default); NCCL: pack, one send/recv "
+                    choices=["put", "put-nccl", "nccl", "nccl-direct", "nccl-sync"],
+                    help="N>1: fused pack+put over NVLink into CUDA IPC windows (default) or "
+                         "NCCL symmetric-memory windows (put-nccl); NCCL: pack, one send/recv "
                          "per peer, unpack (nccl), one send/recv per item run (nccl-direct), or "
                          "the round-1 path that reads the counts on the data stream (nccl-sync)")
     ap.add_argument("--nccl-register", action="store_true",

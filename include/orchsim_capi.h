@@ -417,6 +417,11 @@ int orch_barrier(orch_comm* comm, void* stream);
  * the acquire sets the window status, and a put whose acquire timed out sets
  * layout->status to ORCH_CUDA_ERROR and stores nothing. */
 int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out);
+/* The same window in NCCL symmetric memory instead of CUDA IPC: ncclMemAlloc +
+ * ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC) (NCCL >= 2.28), the peers'
+ * addresses from the device API's ncclGetPeerPointer. Puts, barrier, release
+ * and destroy are unchanged. Collective over the communicator. */
+int orch_window_create_nccl(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out);
 void* orch_window_ptr(const orch_window* w);
 size_t orch_window_bytes(const orch_window* w);
 int orch_window_destroy(orch_window* w); /* collective */

@@ -40,7 +40,7 @@ def _nccl_dirs():
 
 
 CU_SOURCES = ["context.cu", "balance.cu", "dispatch.cu", "exhaustive.cu", "hosting.cu", "compose.cu",
-              "exchange.cu"]
+              "exchange.cu", "nccl_window.cu"]
 HOST_SOURCES = ["host/core.cpp", "host/balancers.cpp", "host/topology.cpp", "host/exchange.cpp",
                 "host/runtime.cpp"]
 

@@ -30,7 +30,8 @@ EXPORTED = [
     "orch_comm_unique_id", "orch_comm_create",
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
     "orch_solve_hosting_host", "orch_nodewise", "orch_rearrange", "orch_backbone_targets",
-    "orch_barrier", "orch_window_create", "orch_window_ptr", "orch_window_bytes",
+    "orch_barrier", "orch_window_create", "orch_window_create_nccl", "orch_window_ptr",
+    "orch_window_bytes",
     "orch_window_destroy", "orch_window_barrier", "orch_dispatch_put", "orch_put",
     "orch_gather_window_create", "orch_gather_window_destroy", "orch_allgather_items_put",
     "orch_gather_window_stamps", "orch_window_release", "orch_window_status", "orch_put_at",
@@ -263,15 +264,18 @@ class XPlan:
 
 
 class Window:
-    """orch_window: an IPC-shared row buffer of one rank (collective create)."""
+    """orch_window: a peer-mapped row buffer of one rank (collective create):
+    CUDA IPC (backend "ipc") or NCCL symmetric memory (backend "nccl",
+    orch_window_create_nccl)."""
 
-    def __init__(self, ctx: "Context", comm: Comm, nbytes: int, _handle=None):
+    def __init__(self, ctx: "Context", comm: Comm, nbytes: int, _handle=None, backend="ipc"):
         self.h = C.c_void_p()
         if _handle is not None:
             self.h = _handle
         else:
-            _check(lib().orch_window_create(ctx.h, comm.h, C.c_size_t(nbytes),
-                                            C.byref(self.h)))
+            create = {"ipc": lib().orch_window_create,
+                      "nccl": lib().orch_window_create_nccl}[backend]
+            _check(create(ctx.h, comm.h, C.c_size_t(nbytes), C.byref(self.h)))
         self.nbytes = nbytes
         self.ptr = lib().orch_window_ptr(self.h)
 

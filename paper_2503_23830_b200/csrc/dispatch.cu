@@ -45,6 +45,7 @@ struct orch_window {
   std::vector<char*> peers;       // host copy, peers[rank] == base
   char** peers_dev = nullptr;     // device copy [P]
   bool loopback = false;          // peers are other windows of this process (no IPC)
+  ncclWindow_t nccl_win = nullptr;  // orch_window_create_nccl: NCCL symmetric memory
 };
 
 struct orch_gather_window {
@@ -55,6 +56,10 @@ struct orch_gather_window {
 };
 
 namespace orchb {
+
+// nccl_window.cu: every rank's address of an NCCL symmetric window (the device
+// API's ncclGetPeerPointer lives in its own translation unit)
+cudaError_t nccl_window_peers(ncclWindow_t win, int P, char** peers_dev);
 
 namespace {
 
@@ -1975,14 +1980,22 @@ void window_free(orch_window* w) {
   int dev0 = 0;
   cudaGetDevice(&dev0);
   cudaSetDevice(w->comm->device);
-  if (!w->loopback)
+  if (w->nccl_win) {  // collective, like the registration
+    cudaDeviceSynchronize();
+    ncclCommWindowDeregister(w->comm->comm, w->nccl_win);
+  } else if (!w->loopback) {
     for (int q = 0; q < static_cast<int>(w->peers.size()); ++q)
       if (q != w->comm->rank && w->peers[q]) cudaIpcCloseMemHandle(w->peers[q]);
+  }
   if (w->peers_dev) cudaFree(w->peers_dev);
-  if (w->base) cudaFree(w->base);
+  if (w->base) {
+    if (w->comm->comm && w->nccl_win) ncclMemFree(w->base);
+    else cudaFree(w->base);
+  }
   delete w;
   cudaSetDevice(dev0);
 }
+
 
 // What every rank contributes to the window set-up all-gather.
 struct WindowCard {
@@ -2054,6 +2067,75 @@ int orch_window_create(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window
   if (rc) {
     window_free(w);
     return rc;
+  }
+  *out = w;
+  return ORCH_OK;
+}
+
+int orch_window_create_nccl(orch_ctx* ctx, orch_comm* comm, size_t bytes, orch_window** out) {
+  if (!ctx || !comm || !out || bytes == 0) return fail(ORCH_INVALID_ARGUMENT, "bad window arguments");
+  if (comm->loopback || !comm->comm)
+    return fail(ORCH_INVALID_ARGUMENT, "loopback communicator: use orch_window_create_local");
+  ORCH_CUDA_TRY(cudaSetDevice(comm->device));
+  const int P = comm->size;
+  // every rank's size first (the puts and barriers address peers with this
+  // rank's flags offset and capacity, so all sizes must agree)
+  uint64_t* sz = nullptr;
+  ORCH_CUDA_TRY(cudaMalloc(&sz, sizeof(uint64_t) * (P + 1)));
+  const uint64_t mine = bytes;
+  cudaError_t e = cudaMemcpy(sz, &mine, sizeof mine, cudaMemcpyHostToDevice);
+  ncclResult_t nr = e == cudaSuccess ? ncclAllGather(sz, sz + 1, 1, ncclUint64, comm->comm, 0)
+                                     : ncclSuccess;
+  std::vector<uint64_t> all(P);
+  if (e == cudaSuccess && nr == ncclSuccess)
+    e = cudaMemcpy(all.data(), sz + 1, sizeof(uint64_t) * P, cudaMemcpyDeviceToHost);
+  cudaFree(sz);
+  if (e != cudaSuccess) return fail(ORCH_CUDA_ERROR, std::string("window sizes: ") + cudaGetErrorString(e));
+  if (nr != ncclSuccess) return fail(ORCH_NCCL_ERROR, std::string("window sizes: ") + ncclGetErrorString(nr));
+  for (int q = 0; q < P; ++q)
+    if (all[q] != bytes)
+      return fail(ORCH_INVALID_ARGUMENT,
+                  "orch_window_create_nccl: ranks passed different window sizes (rank " +
+                      std::to_string(q) + ": " + std::to_string(all[q]) + " bytes, rank " +
+                      std::to_string(comm->rank) + ": " + std::to_string(bytes) + ")");
+  auto* w = new orch_window();
+  w->comm = comm;
+  w->bytes = bytes;
+  w->peers.assign(P, nullptr);
+  w->flags_off = (bytes + 255) & ~size_t{255};
+  const size_t total = (w->flags_off + kFlagBytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) &
+                       ~size_t{NCCL_WIN_REQUIRED_ALIGNMENT - 1};
+  void* base = nullptr;
+  nr = ncclMemAlloc(&base, total);
+  if (nr != ncclSuccess) {
+    delete w;
+    return fail(ORCH_NCCL_ERROR, std::string("ncclMemAlloc: ") + ncclGetErrorString(nr));
+  }
+  w->base = static_cast<char*>(base);
+  e = cudaMemset(w->base + w->flags_off, 0, kFlagBytes);
+  if (e != cudaSuccess) {
+    ncclMemFree(base);
+    w->base = nullptr;
+    delete w;
+    return fail(ORCH_CUDA_ERROR, std::string("window flags: ") + cudaGetErrorString(e));
+  }
+  nr = ncclCommWindowRegister(comm->comm, base, total, &w->nccl_win, NCCL_WIN_COLL_SYMMETRIC);
+  if (nr != ncclSuccess) {
+    ncclMemFree(base);
+    w->base = nullptr;
+    w->nccl_win = nullptr;
+    delete w;
+    return fail(ORCH_NCCL_ERROR, std::string("ncclCommWindowRegister: ") + ncclGetErrorString(nr));
+  }
+  e = cudaMalloc(&w->peers_dev, sizeof(char*) * P);
+  if (e == cudaSuccess) e = nccl_window_peers(w->nccl_win, P, w->peers_dev);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(w->peers.data(), w->peers_dev, sizeof(char*) * P, cudaMemcpyDeviceToHost);
+  // (this rank's own entry is its address in NCCL's flat mapping of the
+  // window: another virtual address of the same memory as base)
+  if (e != cudaSuccess) {
+    window_free(w);
+    return fail(ORCH_CUDA_ERROR, std::string("NCCL window peers: ") + cudaGetErrorString(e));
   }
   *out = w;
   return ORCH_OK;

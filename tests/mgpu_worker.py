@@ -133,6 +133,23 @@ def main():
                     ok = ok and int(lay.status.item()) == 0 and win.status() == 0
                     dist.barrier()
                 win.close()
+                # the same put into NCCL symmetric-memory windows (ncclMemAlloc +
+                # ncclCommWindowRegister, peers from ncclGetPeerPointer)
+                nwin = Window(ctx, comm, wbytes, backend="nccl")
+                nv = nwin.tensor_view(torch.device("cuda", local))
+                for _ in range(2):
+                    nv.zero_()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    ctx.put(d, gl, go, bal, lay, R, rin, nwin, comm)
+                    ctx.window_barrier(nwin)
+                    ok = ok and torch.equal(nv[:k].cpu(), torch.from_numpy(outs[rank]))
+                    ctx.window_release(nwin)
+                    torch.cuda.synchronize()
+                    ok = ok and int(lay.status.item()) == 0 and nwin.status() == 0
+                    dist.barrier()
+                nv = None
+                nwin.close()
                 cases += 1
                 if not ok:
                     failures += 1
