@@ -10,7 +10,9 @@ Per phase: [all-gather of lengths] -> cost model + ordering + greedy
 assignment + never-worse (one balance call) -> [node-wise hosting] -> send/recv
 layout -> row movement. At N GPUs the 8 instances are spread 8/N per GPU
 (strong scaling: the job is fixed); the rows move by the fused pack+put into
-the peers' windows (window barrier + release per step) or, with
+the peers' windows -- NCCL symmetric-memory windows (ncclCommWindowRegister,
+peers from ncclGetPeerPointer) by default, CUDA IPC windows with --exchange put
+-- closed by a window barrier + release per step, or, with
 --exchange nccl, by pack -> grouped ncclSend/ncclRecv -> unpack.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
@@ -221,8 +223,8 @@ def run_reference(args):
 def run_b200(args):
     import torch
     import torch.distributed as dist
-    from paper_2503_23830_b200.capi import (Balance, Comm, Context, GatherWindow, Layout, Window,
-                                            XPlan)
+    from paper_2503_23830_b200.capi import (Balance, Comm, Context, GatherWindow, Layout, OrchError,
+                                            Window, XPlan)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -365,8 +367,15 @@ def run_b200(args):
         for s in st:
             s["win_off"] = off
             off += s["wrows"] * R
-        win = Window(ctx_data, comm_data, off,
-                     backend="nccl" if args.exchange == "put-nccl" else "ipc")
+        if args.exchange == "put-nccl":
+            try:
+                win = Window(ctx_data, comm_data, off, backend="nccl")
+            except OrchError as e:  # NCCL without symmetric memory: the same put, IPC windows
+                print(f"[bench] NCCL symmetric window unavailable ({e}); CUDA IPC windows",
+                      file=sys.stderr)
+                args.exchange = "put"
+        if win is None:
+            win = Window(ctx_data, comm_data, off)
         wview = win.tensor_view(dev)
         for s in st:
             s["rout"] = wview[s["win_off"]:s["win_off"] + s["wrows"] * R]
@@ -734,10 +743,10 @@ def main():
     ap.add_argument("--barrier", default="window", choices=["window", "nccl", "none"],
                     help="N>1 put: the per-step barrier through the window's peer memory "
                          "(default), a 1-int ncclAllReduce, or none (diagnostics only)")
-    ap.add_argument("--exchange", default="put",
+    ap.add_argument("--exchange", default="put-nccl",
                     choices=["put", "put-nccl", "nccl", "nccl-direct", "nccl-sync"],
-                    help="N>1: fused pack+put over NVLink into CUDA IPC windows (default) or "
-                         "NCCL symmetric-memory windows (put-nccl); NCCL: pack, one send/recv "
+                    help="N>1: fused pack+put over NVLink into NCCL symmetric-memory windows "
+                         "(put-nccl, default) or CUDA IPC windows (put); NCCL: pack, one send/recv "
                          "per peer, unpack (nccl), one send/recv per item run (nccl-direct), or "
                          "the round-1 path that reads the counts on the data stream (nccl-sync)")
     ap.add_argument("--nccl-register", action="store_true",

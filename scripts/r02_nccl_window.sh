@@ -4,8 +4,8 @@
 o=gpurun_out/nccl_window; mkdir -p $o
 N=$(nvidia-smi -L | wc -l)
 timeout 900 python -m pytest -q -x tests/test_multigpu.py > $o/pytest_mgpu.log 2>&1; echo "mgpu tests rc=$? $(tail -1 $o/pytest_mgpu.log)"
-for cfg in C2 C5; do
-  for ex in put put-nccl nccl; do
+for cfg in ${CFGS:-C2 C5}; do
+  for ex in ${EXS:-put put-nccl nccl}; do
     timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
       --master-port $((29500 + RANDOM % 300)) bench.py --gpus $N --config $cfg --exchange $ex \
       > $o/${N}gpu_${cfg}_$ex.json 2> $o/${N}gpu_${cfg}_$ex.err
