@@ -7,7 +7,8 @@ the consumer release k_window_release and the gather window's k_gather_put --
 with each emulated rank on its own stream. Expected placements come from the
 oracle's layout (apply() on rows, core.cpp:120-161); rows are tagged and
 compared on the device (tests/rowcheck.py). The NCCL entry points are covered
-by tests/test_multigpu.py on 2+ GPUs.
+by tests/test_multigpu.py on 2+ GPUs; the NCCL symmetric-memory window also on
+a one-rank communicator here.
 """
 import numpy as np
 import pytest
@@ -362,3 +363,34 @@ def test_bench_chain_emulated(ctx, oracle, P):
     for cm in comms:
         cm.close()
     ctx.close()
+
+
+def test_nccl_symmetric_window_one_rank(ctx, oracle):
+    """orch_window_create_nccl on a one-rank NCCL communicator (the driver's
+    one-GPU run): ncclMemAlloc + ncclCommWindowRegister, the rank's address from
+    the device API's ncclGetPeerPointer (NCCL's flat mapping of the window, not
+    the allocation's own address), then the put, barrier and release through it,
+    byte-exact; two steps."""
+    from paper_2503_23830_b200.capi import Comm, Window
+    rng = np.random.default_rng(11)
+    d, R = 8, 4096
+    length, origin = random_instance(rng, d, 400, 1, 40)
+    o, e, L, O, bal, lay = balance_case(ctx, oracle, 0, d, 1, length, origin)
+    comm = Comm(1, 0, Comm.unique_id())
+    big, ins, in_base = rank_inputs(e, 1, R, seed=5)
+    win = Window(ctx, comm, max(int(e["out_tokens"][0]), 1) * R, backend="nccl")
+    view = win.tensor_view(torch.device("cuda", 0))
+    idx = source_rows(length, origin, o.dest_inst, e["rank_src_off"], e["rank_dst_off"], d, 1,
+                      in_base)
+    for _ in range(2):
+        view.zero_()
+        ctx.put(d, L, O, bal, lay, R, ins[0], win, comm)
+        ctx.window_barrier(win)
+        torch.cuda.synchronize()
+        assert int(lay.status.item()) == 0 and win.status() == 0
+        assert rows_equal(view, big, idx[0], R), first_mismatch(view, big, idx[0], R)
+        ctx.window_release(win)
+    torch.cuda.synchronize()
+    view = None
+    win.close()
+    comm.close()
