@@ -537,7 +537,7 @@ int orch_balance_layout1(orch_ctx* ctx, const orch_policy* policy, int32_t d, in
 // (pageable cudaMemcpyAsync calls cost ~10 us each; a call used to make eight).
 namespace {
 
-constexpr int64_t kZeroCopyItems = 256;
+constexpr int64_t kZeroCopyItems = 4096;
 
 int host_pipeline(orch_ctx* ctx, const orch_policy* policy, int32_t d, int64_t n,
                   const int64_t* h_len, const int32_t* h_origin, int mode, int64_t probe,
