@@ -203,6 +203,54 @@ __global__ void qt_e(const int64_t* gxs, int n, int d, int64_t v, uint8_t* out, 
   if (lane == 0) *cyc = t1 - t0;
 }
 
+// F: E with the sums and square sums in doubles (exact while n * max_len^2 < 2^53)
+// lane = batch keeps its row beats_j; the champion chain is walked on a
+// packed next-champion word (4 bits per batch, 15 = none) built by one OR
+// reduction, so a walk step is a 32-bit shift and mask
+__global__ void qt_f(const int64_t* gxs, int n, int d, int64_t v, uint8_t* out, long long* cyc) {
+  __shared__ int64_t xs[512];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = gxs[i];
+  __syncthreads();
+  const int lane = threadIdx.x;
+  double qs = 0, qq = 0;
+  unsigned beats = 0;
+  const unsigned dmask = (1u << d) - 1u;
+  const unsigned above = lane >= 31 ? 0u : (dmask & (~0u << (lane + 1)));
+  unsigned W = 0xffffffffu;  // every batch: no later batch beats it
+  const double vd = static_cast<double>(v);
+  __syncwarp();
+  const long long t0 = clock64();
+  int64_t x_next = xs[0];
+  for (int k = 0; k < n; ++k) {
+    const double x = static_cast<double>(x_next);
+    if (k + 1 < n) x_next = xs[k + 1];
+    const double xx = x * x;
+    int best = 0;
+    for (;;) {
+      const unsigned t = (W >> (4 * best)) & 0xfu;
+      if (t == 0xfu) break;
+      best = static_cast<int>(t);
+    }
+    const bool me = lane == best;
+    if (lane == 0) out[k] = static_cast<uint8_t>(best);
+    qs += me ? x : 0.0;
+    qq += me ? xx : 0.0;
+    const double bs = __shfl_sync(~0u, qs, best);
+    const double bq = __shfl_sync(~0u, qq, best);
+    const bool near = fabs(qs - bs) < vd;
+    const bool on = lane < d && !me;
+    const bool b_beats_me = on & (near ? bq < qq : bs < qs);
+    const bool i_beat_b = on & (near ? qq < bq : qs < bs);
+    const unsigned row = __ballot_sync(~0u, i_beat_b);
+    beats = me ? row : ((beats & ~(1u << best)) | (b_beats_me ? 1u << best : 0u));
+    const unsigned m = beats & above;
+    const unsigned nx = m ? static_cast<unsigned>(__ffs(m) - 1) : 0xfu;
+    W = __reduce_or_sync(~0u, lane < 8 ? nx << (4 * lane) : 0u);
+  }
+  const long long t1 = clock64();
+  if (lane == 0) *cyc = t1 - t0;
+}
+
 // C: one thread, all states in registers, 16 independent comparisons per item
 __global__ void qt_c(const int64_t* gxs, int n, int d, int64_t v, uint8_t* out, long long* cyc) {
   __shared__ int64_t xs[512];
@@ -277,9 +325,9 @@ int main() {
     cudaMalloc(&dout, n);
     cudaMalloc(&dc, 8);
     cudaMemcpy(dx, xs.data(), n * 8, cudaMemcpyHostToDevice);
-    const char* names[5] = {"A current", "B replicated", "C one thread", "D packed next",
-                            "E branch-free"};
-    for (int var = 0; var < 5; ++var) {
+    const char* names[6] = {"A current", "B replicated", "C one thread", "D packed next",
+                            "E branch-free", "F doubles"};
+    for (int var = 0; var < 6; ++var) {
       long long best_c = 1ll << 60;
       for (int r = 0; r < 5; ++r) {
         cudaMemset(dout, 0xff, n);
@@ -288,8 +336,12 @@ int main() {
         if (var == 2) qt_c<<<1, 32>>>(dx, n, d, v, dout, dc);
         if (var == 3) qt_d<<<1, 32>>>(dx, n, d, v, dout, dc);
         if (var == 4) qt_e<<<1, 32>>>(dx, n, d, v, dout, dc);
-        long long c;
+        if (var == 5) qt_f<<<1, 32>>>(dx, n, d, v, dout, dc);
+        long long c = -1;
+        const cudaError_t err = cudaDeviceSynchronize();
+        if (err != cudaSuccess) printf("variant %d: %s\n", var, cudaGetErrorString(err));
         cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+        cudaMemset(dc, 0, 8);
         best_c = c < best_c ? c : best_c;
       }
       std::vector<uint8_t> got(n);
