@@ -222,6 +222,14 @@ int orch_encode_lengths(orch_ctx* ctx, int64_t num_examples, const int32_t* d_pa
 int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
                             int32_t* h_hosting, int64_t* h_info, void* stream);
 
+/* inter_node_egress (topology.hpp:68, topology.cpp:61-89) of a given hosting on
+ * the device: h_egress[n] = sum of V[i][b] over source instances i on node n
+ * (= i / c) and batches b hosted elsewhere (h_hosting[b] != n), for any node
+ * count d / c. The caller validates the hosting (the C++ adapter throws as the
+ * reference does); hosting entries are taken as node indices in [0, d / c). */
+int orch_inter_node_egress_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
+                                const int32_t* h_hosting, int64_t* h_egress, void* stream);
+
 /* nodewise_rearrange (topology.hpp:87, topology.cpp:267-303) applied in place
  * to a balance result: volume matrix of the result, optimal hosting, then
  * destination batch b is relabelled batch_to_instance[b] (dest_inst and the

@@ -29,7 +29,8 @@ EXPORTED = [
     "orch_layout", "orch_pack", "orch_exchange", "orch_unpack", "orch_dispatch",
     "orch_comm_unique_id", "orch_comm_create",
     "orch_comm_destroy", "orch_comm_rank", "orch_comm_size", "orch_allgather_items",
-    "orch_solve_hosting_host", "orch_nodewise", "orch_rearrange", "orch_backbone_targets",
+    "orch_solve_hosting_host", "orch_inter_node_egress_host", "orch_nodewise", "orch_rearrange",
+    "orch_backbone_targets",
     "orch_barrier", "orch_window_create", "orch_window_create_nccl", "orch_window_ptr",
     "orch_window_bytes",
     "orch_window_destroy", "orch_window_barrier", "orch_dispatch_put", "orch_put",
@@ -484,6 +485,18 @@ class Context:
             return dict(hosting=hosting)
         return dict(hosting=hosting, max_egress=int(inf[0]), baseline_max=int(inf[1]),
                     leaf_used=int(inf[2]), visited=int(inf[3]))
+
+    def inter_node_egress(self, d, c, V, hosting):
+        """orch_inter_node_egress_host: per-node egress of a hosting (node per batch)."""
+        import numpy as np
+        V = np.ascontiguousarray(V, dtype=np.int64).reshape(-1)
+        h = np.ascontiguousarray(hosting, dtype=np.int32)
+        e = np.zeros(d // c, np.int64)
+        _check(lib().orch_inter_node_egress_host(self.h, C.c_int32(d), C.c_int32(c),
+                                                 V.ctypes.data_as(C.c_void_p),
+                                                 h.ctypes.data_as(C.c_void_p),
+                                                 e.ctypes.data_as(C.c_void_p), _stream()))
+        return e
 
     def nodewise(self, d, c, length, origin, bal: "Balance", out=None, stream=None):
         """Relabels bal's destination batches in place; returns device tensors

@@ -1,6 +1,7 @@
-// orchsim topology subset over the B200 C-ABI: the volume matrix of a
-// rearrangement is accumulated by the sm_100a kernel (orch_volume_matrix);
-// semantics of /root/reference/proj/src/topology.cpp:12-53.
+// orchsim topology over the B200 C-ABI: the volume matrix of a rearrangement
+// (orch_volume_matrix), node egress (orch_inter_node_egress_host) and the
+// hosting search (orch_solve_hosting_host) run on the device; semantics of
+// /root/reference/proj/src/topology.cpp:12-316.
 #include <algorithm>
 #include <numeric>
 
@@ -64,45 +65,63 @@ std::vector<int> identity_hosting(const ClusterTopology& topo) {  // topology.cp
   return h;
 }
 
-std::vector<std::int64_t> inter_node_egress(const VolumeMatrix& v, const ClusterTopology& topo,
-                                            const std::vector<int>& hosting) {  // :61-89
-  validate_topology(topo);
-  const int d = topo.instance_count, nodes = topo.node_count();
-  if (v.dimension() != d || static_cast<int>(hosting.size()) != d)
-    throw std::invalid_argument("volume matrix / hosting size does not match topology");
-  std::vector<int> per(static_cast<std::size_t>(nodes), 0);
+namespace {
+
+// A hosting must name a node for every batch and give each node exactly c
+// batches (topology.cpp:61-80); the egress itself is summed on the device.
+void require_balanced_hosting(const ClusterTopology& topo, const std::vector<int>& hosting) {
+  std::vector<int> load(static_cast<std::size_t>(topo.node_count()), 0);
   for (int node : hosting) {
-    if (node < 0 || node >= nodes) throw std::invalid_argument("hosting references unknown node");
-    ++per[node];
+    if (node < 0 || node >= topo.node_count())
+      throw std::invalid_argument("hosting references unknown node");
+    ++load[static_cast<std::size_t>(node)];
   }
-  for (int k : per)
-    if (k != topo.instances_per_node)
-      throw std::invalid_argument("hosting must place exactly c batches per node");
-  std::vector<std::int64_t> e(static_cast<std::size_t>(nodes), 0);
-  for (int i = 0; i < d; ++i)
-    for (int b = 0; b < d; ++b)
-      if (hosting[b] != topo.node_of(i)) e[topo.node_of(i)] += v.at(i, b);
+  if (std::any_of(load.begin(), load.end(), [&](int k) { return k != topo.instances_per_node; }))
+    throw std::invalid_argument("hosting must place exactly c batches per node");
+}
+
+std::vector<std::int64_t> device_egress(const VolumeMatrix& v, const ClusterTopology& topo,
+                                        const std::vector<int>& hosting) {
+  const std::vector<int32_t> h(hosting.begin(), hosting.end());
+  std::vector<std::int64_t> e(static_cast<std::size_t>(topo.node_count()));
+  b200::check(orch_inter_node_egress_host(b200::context(), topo.instance_count,
+                                          topo.instances_per_node, v.data(), h.data(), e.data(),
+                                          nullptr));
   return e;
 }
 
-HostingSolution solve_hosting(const VolumeMatrix& volumes, const ClusterTopology& topo) {
+// solve_hosting's search on the device; info = {max egress, identity hosting's
+// max egress, leaf used, the reference's nodes_visited}
+HostingSolution search(const VolumeMatrix& v, const ClusterTopology& topo, std::int64_t info[4]) {
   validate_topology(topo);
-  const int d = topo.instance_count;
-  if (volumes.dimension() != d)
+  if (v.dimension() != topo.instance_count)
     throw std::invalid_argument("volume matrix dimension does not match topology");
-  std::vector<std::int64_t> flat(static_cast<std::size_t>(d) * d);
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) flat[static_cast<std::size_t>(i) * d + j] = volumes.at(i, j);
-  std::vector<int32_t> h(static_cast<std::size_t>(d));
-  std::int64_t info[4] = {0, 0, 0, 0};
-  b200::check(orch_solve_hosting_host(b200::context(), d, topo.instances_per_node, flat.data(),
-                                      h.data(), info, nullptr));
+  std::vector<int32_t> h(static_cast<std::size_t>(topo.instance_count));
+  b200::check(orch_solve_hosting_host(b200::context(), topo.instance_count,
+                                      topo.instances_per_node, v.data(), h.data(), info, nullptr));
   HostingSolution sol;
   sol.hosting.assign(h.begin(), h.end());
-  sol.per_node_egress = inter_node_egress(volumes, topo, sol.hosting);
+  sol.per_node_egress = device_egress(v, topo, sol.hosting);
   sol.max_egress = info[0];
-  sol.nodes_visited = info[3];  // the reference's count, replayed on the device
+  sol.nodes_visited = info[3];
   return sol;
+}
+
+}  // namespace
+
+std::vector<std::int64_t> inter_node_egress(const VolumeMatrix& v, const ClusterTopology& topo,
+                                            const std::vector<int>& hosting) {  // :61-89
+  validate_topology(topo);
+  if (v.dimension() != topo.instance_count ||
+      static_cast<int>(hosting.size()) != topo.instance_count)
+    throw std::invalid_argument("volume matrix / hosting size does not match topology");
+  require_balanced_hosting(topo, hosting);
+  return device_egress(v, topo, hosting);
+}
+
+HostingSolution solve_hosting(const VolumeMatrix& volumes, const ClusterTopology& topo) {
+  std::int64_t info[4] = {0, 0, 0, 0};  // topology.cpp:179-265
+  return search(volumes, topo, info);
 }
 
 NodewiseResult nodewise_rearrange(const std::vector<MiniBatch>& batches, const Rearrangement& re,
@@ -110,23 +129,22 @@ NodewiseResult nodewise_rearrange(const std::vector<MiniBatch>& batches, const R
   validate_topology(topo);
   if (re.instance_count() != topo.instance_count)
     throw std::invalid_argument("rearrangement instance count does not match topology");
-  const int d = topo.instance_count;
-  const VolumeMatrix v = volume_matrix(batches, re);
-  HostingSolution sol = solve_hosting(v, topo);
-  const auto baseline = inter_node_egress(v, topo, identity_hosting(topo));
-  std::vector<int> b2i(static_cast<std::size_t>(d), -1);
-  std::vector<int> next(static_cast<std::size_t>(topo.node_count()));
-  for (int n = 0; n < topo.node_count(); ++n) next[n] = n * topo.instances_per_node;
-  for (int b = 0; b < d; ++b) b2i[b] = next[sol.hosting[b]]++;
-  std::map<SlotRef, SlotRef> moves;
-  for (const auto& kv : re.moves()) moves.emplace(kv.first, SlotRef{b2i[kv.second.instance], kv.second.slot});
+  std::int64_t info[4] = {0, 0, 0, 0};
+  HostingSolution sol = search(volume_matrix(batches, re), topo, info);
+  // within a node, its batches take its instances in ascending batch order
+  std::vector<int> seat(static_cast<std::size_t>(topo.node_count()), 0);
   NodewiseResult r;
-  r.rearrangement = Rearrangement(d, std::move(moves));
-  r.hosting = sol.hosting;
+  r.batch_to_instance.resize(sol.hosting.size());
+  for (std::size_t b = 0; b < sol.hosting.size(); ++b)
+    r.batch_to_instance[b] = sol.hosting[b] * topo.instances_per_node + seat[sol.hosting[b]]++;
+  std::map<SlotRef, SlotRef> moves;
+  for (const auto& kv : re.moves())
+    moves.emplace(kv.first, SlotRef{r.batch_to_instance[kv.second.instance], kv.second.slot});
+  r.rearrangement = Rearrangement(topo.instance_count, std::move(moves));
+  r.hosting = std::move(sol.hosting);
   r.max_egress = sol.max_egress;
-  r.per_node_egress = sol.per_node_egress;
-  r.baseline_max_egress = *std::max_element(baseline.begin(), baseline.end());
-  r.batch_to_instance = std::move(b2i);
+  r.per_node_egress = std::move(sol.per_node_egress);
+  r.baseline_max_egress = info[1];  // the identity hosting's, from the same device pass
   r.nodes_visited = sol.nodes_visited;
   return r;
 }

@@ -35,6 +35,7 @@
 // (total - gained - optimistic gain) -- read in O(1): the unassigned batches
 // at depth k are exactly order[k..d), so the optimistic gain of node n with r
 // slots left is a table og[k][n][r] built once.
+#include <algorithm>
 #include <cstring>
 #include <climits>
 #include <cstdlib>
@@ -1592,6 +1593,25 @@ __global__ void k_hw_info(const HostState* __restrict__ Hp, const unsigned long 
   info[3] = static_cast<int64_t>(H.visits);
 }
 
+// inter_node_egress of one hosting for any node count: per-CTA node totals in
+// shared memory, one atomic per node and CTA
+__global__ void k_node_egress(const int64_t* __restrict__ V, const int32_t* __restrict__ hosting,
+                              int d, int c, unsigned long long* __restrict__ e) {
+  extern __shared__ unsigned long long eg_acc[];
+  const int nodes = d / c;
+  for (int i = threadIdx.x; i < nodes; i += blockDim.x) eg_acc[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+       i < static_cast<int64_t>(d) * d; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int src = static_cast<int>(i / d), b = static_cast<int>(i % d), nd = src / c;
+    const int64_t v = V[i];
+    if (v && hosting[b] != nd) atomicAdd(&eg_acc[nd], static_cast<unsigned long long>(v));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nodes; i += blockDim.x)
+    if (eg_acc[i]) atomicAdd(&e[i], eg_acc[i]);
+}
+
 // setup, both passes and the finish of the wide search; V on the device
 int run_wide_hosting(orch_ctx* ctx, int d, int c, const int64_t* V, HostState* H, const HostBufs& hb,
                      const WideScratch& w, int32_t* hosting, int32_t* b2i, int64_t* info,
@@ -1798,6 +1818,37 @@ int orch_solve_hosting_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* 
     if (rc) return rc;
     memcpy(h_info, hinfo, sizeof hinfo);
   }
+  return ORCH_OK;
+}
+
+int orch_inter_node_egress_host(orch_ctx* ctx, int32_t d, int32_t c, const int64_t* h_V,
+                                const int32_t* h_hosting, int64_t* h_egress, void* stream) {
+  if (!ctx || !h_V || !h_hosting || !h_egress) return fail(ORCH_INVALID_ARGUMENT, "null argument");
+  if (d < 1 || c < 1 || d % c)
+    return fail(ORCH_INVALID_ARGUMENT, "instance count must be divisible by instances per node");
+  if (d > ORCH_MAX_INSTANCES)
+    return fail(ORCH_UNSUPPORTED, "inter_node_egress limited to d <= 4096 on the device");
+  ORCH_CUDA_TRY(cudaSetDevice(ctx->device));
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t dd = static_cast<size_t>(d), nodes = static_cast<size_t>(d / c);
+  int64_t* V;
+  int32_t* hosting;
+  unsigned long long* e;
+  Plan plan;
+  plan.add(&V, dd * dd);
+  plan.add(&hosting, dd);
+  plan.add(&e, nodes);
+  int rc = plan.commit(ctx, st);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaMemcpyAsync(V, h_V, sizeof(int64_t) * dd * dd, cudaMemcpyHostToDevice, st));
+  ORCH_CUDA_TRY(cudaMemcpyAsync(hosting, h_hosting, sizeof(int32_t) * dd, cudaMemcpyHostToDevice, st));
+  ORCH_CUDA_TRY(cudaMemsetAsync(e, 0, sizeof(unsigned long long) * nodes, st));
+  const int grid = static_cast<int>(std::min<int64_t>((static_cast<int64_t>(dd * dd) + 255) / 256, kSMs * 4));
+  k_node_egress<<<grid, 256, sizeof(unsigned long long) * nodes, st>>>(V, hosting, d, c, e);
+  ctx->launches += 1;
+  ORCH_CUDA_TRY(cudaGetLastError());
+  ORCH_CUDA_TRY(cudaMemcpyAsync(h_egress, e, sizeof(int64_t) * nodes, cudaMemcpyDeviceToHost, st));
+  ORCH_CUDA_TRY(cudaStreamSynchronize(st));
   return ORCH_OK;
 }
 

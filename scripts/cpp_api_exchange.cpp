@@ -9,7 +9,10 @@
 //   * make_exchange_plan (AllToAll, AllGather) and simulate_exchange
 //     (exchange.cpp:49-113) on a topology of `c` instances per node;
 //   * gather_lengths' metadata volume and a stale-plan rejection;
-//   * permutation_invariance_check (topology.cpp:305-316).
+//   * permutation_invariance_check (topology.cpp:305-316);
+//   * d <= 64: nodewise_rearrange on 2 and 8 nodes (topology.cpp:267-303) --
+//     hosting, egress, the identity baseline, nodes_visited, the relabelled
+//     moves -- and inter_node_egress of the identity hosting.
 // Doubles are printed as IEEE bit patterns so the two builds compare exactly.
 #include <algorithm>
 #include <chrono>
@@ -134,6 +137,40 @@ int main(int argc, char** argv) {
         median_us(reps, [&] { perm_ok = permutation_invariance_check(in, in, model); });
     const bool perm_changed = permutation_invariance_check(in, res.new_batches, model);
 
+    // node-wise hosting on 2 and 8 nodes (d <= 64: the reference's search is
+    // exponential beyond)
+    std::string hosting = "[";
+    double t_host = 0.0;
+    for (int nodes : {2, 8}) {
+      if (d > 64 || d % nodes || nodes > d) continue;
+      ClusterTopology tn = topo;
+      tn.instances_per_node = d / nodes;
+      NodewiseResult nw;
+      const double t = median_us(d >= 64 ? 3 : reps, [&] { nw = nodewise_rearrange(in, res.rearrangement, tn); });
+      if (nodes == 8) t_host = t;
+      const VolumeMatrix vm = volume_matrix(in, res.rearrangement);
+      const std::vector<int64_t> base = inter_node_egress(vm, tn, identity_hosting(tn));
+      uint64_t h = 1469598103934665603ull;
+      for (int b = 0; b < d; ++b) {
+        h = (h ^ static_cast<uint64_t>(nw.hosting[b])) * 1099511628211ull;
+        h = (h ^ static_cast<uint64_t>(nw.batch_to_instance[b])) * 1099511628211ull;
+      }
+      for (const auto& kv : nw.rearrangement.moves()) {
+        h = (h ^ static_cast<uint64_t>(kv.second.instance)) * 1099511628211ull;
+        h = (h ^ static_cast<uint64_t>(kv.second.slot)) * 1099511628211ull;
+      }
+      std::string eg, be;
+      for (size_t k = 0; k < nw.per_node_egress.size(); ++k)
+        eg += (k ? ", " : "") + std::to_string(nw.per_node_egress[k]);
+      for (size_t k = 0; k < base.size(); ++k) be += (k ? ", " : "") + std::to_string(base[k]);
+      hosting += std::string(hosting.size() > 1 ? ", " : "") + "{\"nodes\": " +
+                 std::to_string(nodes) + ", \"max\": " + std::to_string(nw.max_egress) +
+                 ", \"baseline\": " + std::to_string(nw.baseline_max_egress) +
+                 ", \"visited\": " + std::to_string(nw.nodes_visited) + ", \"egress\": [" + eg +
+                 "], \"identity_egress\": [" + be + "], \"hash\": \"" + std::to_string(h) + "\"}";
+    }
+    hosting += "]";
+
     uint64_t moved_sum = 1469598103934665603ull;
     for (const auto& b : xa.first)
       for (const auto& it : b.items) moved_sum = (moved_sum ^ static_cast<uint64_t>(it.example_id)) * 1099511628211ull;
@@ -159,7 +196,8 @@ int main(int argc, char** argv) {
         "\"simulate_us\": %.1f, \"perm_check_us\": %.1f, \"pre\": [\"%llu\", \"%llu\", \"%llu\"], "
         "\"post\": [\"%llu\", \"%llu\", \"%llu\"], \"volumes\": \"%016llx\", \"moved\": "
         "\"%016llx\", \"a2a\": %s, \"ag\": %s, \"stale_rejected\": %d, \"metadata_volume\": %lld, "
-        "\"views\": %zu, \"perm_same\": %d, \"perm_new\": %d}\n",
+        "\"views\": %zu, \"perm_same\": %d, \"perm_new\": %d, \"hosting_us\": %.1f, "
+        "\"hosting\": %s}\n",
         argv[f], static_cast<long long>(n), d, t_stats, t_plan, t_sim, t_perm,
         static_cast<unsigned long long>(bits(pre.max)), static_cast<unsigned long long>(bits(pre.mean)),
         static_cast<unsigned long long>(bits(pre.ratio)), static_cast<unsigned long long>(bits(post.max)),
@@ -168,7 +206,7 @@ int main(int argc, char** argv) {
         static_cast<unsigned long long>(moved_sum), report(xa.second).c_str(),
         report(xg.second).c_str(), stale_rejected ? 1 : 0,
         static_cast<long long>(g.metadata_volume), g.views.size(), perm_ok ? 1 : 0,
-        perm_changed ? 1 : 0);
+        perm_changed ? 1 : 0, t_host, hosting.c_str());
     std::fflush(stdout);
   }
   return 0;

@@ -208,3 +208,22 @@ def test_nodewise_small_path(ctx, oracle, d, c):
         for j in range(d):
             seg = mem[off[j]:off[j + 1]]
             assert (di[seg] == j).all() and (o.dest_slot[seg] == np.arange(len(seg))).all()
+
+
+def test_inter_node_egress(ctx, oracle):
+    """orch_inter_node_egress_host (topology.cpp:61-89) for any node count
+    (c = 1 .. d): the solution's and the identity hosting's egress against the
+    oracle's search and a direct sum."""
+    rng = np.random.default_rng(61)
+    for d, c in [(8, 1), (8, 4), (16, 2), (64, 8), (64, 1), (300, 3), (256, 128)]:
+        V = rng.integers(0, 1000, (d, d)) * (rng.random((d, d)) < 0.4)
+        nodes = d // c
+        for hosting in (np.arange(d) // c, rng.permutation(np.arange(d) // c)):
+            e = ctx.inter_node_egress(d, c, V, hosting)
+            src_node = np.arange(d) // c
+            want = np.array([V[src_node == nd][:, hosting != nd].sum() for nd in range(nodes)])
+            np.testing.assert_array_equal(e, want)
+        if d <= 12:
+            o = oracle.solve_hosting(d, c, V)
+            np.testing.assert_array_equal(ctx.inter_node_egress(d, c, V, o["hosting"]),
+                                          o["per_node_egress"])

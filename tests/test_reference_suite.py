@@ -100,7 +100,7 @@ def test_cpp_api_exchange_matches_reference(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         out[name] = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(out["b200"]) == len(out["ref"]) == len(files)
-    timing = ("stats_us", "plan_us", "simulate_us", "perm_check_us", "file")
+    timing = ("stats_us", "plan_us", "simulate_us", "perm_check_us", "hosting_us", "file")
     for a, b in zip(out["b200"], out["ref"]):
         print({k: (a[k], b[k]) for k in timing if k != "file"}, a["n"], a["d"])
         assert a["stale_rejected"] == 1
