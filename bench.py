@@ -546,12 +546,15 @@ def run_b200(args):
     except Exception:
         traffic_alg = None
 
+    # steps the e2e host loop keeps in flight beyond the one it waits for
+    E2E_DEPTH = int(os.environ.get("ORCH_E2E_DEPTH", "1"))
     # end-to-end through the C-ABI with host buffers: each step copies its
     # metadata from pinned host memory and reads back its assignment vectors
-    # and summaries. Two steps are in flight, as in a training loop's input
-    # pipeline: the host waits for step i's results (on the host) after issuing
-    # step i + 1, so step i + 1's copies and metadata overlap step i's rows;
-    # --e2e-sync completes every step before the next one starts.
+    # and summaries (its own set of pinned buffers). Steps stay in flight as in
+    # a training loop's input pipeline: the host waits for step i's results
+    # (on the host) after issuing step i + E2E_DEPTH, so the next steps' copies
+    # and metadata overlap step i's rows; --e2e-sync completes every step
+    # before the next one starts.
     if comm_meta is None:
         h2d = sum(s["h_glen"].numel() * 8 + s["h_gorg"].numel() * 4 for s in st)
     else:
@@ -561,13 +564,16 @@ def run_b200(args):
     host_out = [[(torch.empty(s["n"], dtype=torch.int32).pin_memory(),
                   torch.empty(s["n"], dtype=torch.int32).pin_memory(),
                   torch.empty(128, dtype=torch.uint8).pin_memory()) for s in st]
-                for _ in range(2)]  # one set per buffer parity: two steps in flight
+                for _ in range(E2E_DEPTH + 1)]  # one set per step in flight
     in_flight = []
+    e2e_count = [0]
 
     def e2e_step(sync):
         b = step(h2d=True)
+        hb = e2e_count[0] % len(host_out)
+        e2e_count[0] += 1
         done = []
-        for s, (hi, hs, hsum) in zip(st, host_out[b]):
+        for s, (hi, hs, hsum) in zip(st, host_out[hb]):
             with torch.cuda.stream(s["ms"]):
                 bal = s["buf"][b]["bal"]
                 hi.copy_(bal.dest_inst[:s["n"]], non_blocking=True)
@@ -580,8 +586,8 @@ def run_b200(args):
         ev.record(data_stream)
         done.append(ev)
         in_flight.append(done)
-        # step i - 1's results are on the host (step i's when synchronous)
-        while len(in_flight) > (0 if sync else 1):
+        # step i - E2E_DEPTH's results are on the host (step i's when synchronous)
+        while len(in_flight) > (0 if sync else E2E_DEPTH):
             for ev in in_flight.pop(0):
                 ev.synchronize()
 
@@ -647,8 +653,9 @@ def run_b200(args):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "note": ("C-ABI with host metadata buffers, one synchronous step at a time; "
                          if args.e2e_sync else
-                         "C-ABI with host metadata buffers, two steps in flight (the host "
-                         "waits for step i's results after issuing step i+1); ") +
+                         f"C-ABI with host metadata buffers, {E2E_DEPTH + 1} steps in flight "
+                         f"(the host waits for step i's results after issuing step "
+                         f"i+{E2E_DEPTH}); ") +
                         "token rows are device-resident activations (encoder/embedding "
                         "outputs)",
                 "sync_value": tokens * args.steps / e2e_sync_s,
