@@ -260,8 +260,19 @@ def run_b200(args):
     meta_ctx = [Context(local) if per_phase and i else ctx0 for i in range(len(phases))]
     meta_streams = [torch.cuda.Stream(device=dev, priority=prio) if per_phase and i else ms0
                     for i in range(len(phases))]
-    gwins = [GatherWindow(meta_ctx[i], comm_meta, len(ph[1]))
-             if comm_meta is not None and args.gather == "put" else None
+    window_kind = ["nccl" if args.exchange == "put-nccl" else "ipc"]
+
+    def make_gwin(i, n):  # NCCL symmetric memory with --exchange put-nccl (IPC if refused)
+        if window_kind[0] == "nccl":
+            try:
+                return GatherWindow(meta_ctx[i], comm_meta, n, backend="nccl")
+            except OrchError as e:
+                print(f"[bench] NCCL symmetric window unavailable ({e}); CUDA IPC windows",
+                      file=sys.stderr)
+                window_kind[0] = "ipc"
+        return GatherWindow(meta_ctx[i], comm_meta, n)
+
+    gwins = [make_gwin(i, len(ph[1])) if comm_meta is not None and args.gather == "put" else None
              for i, ph in enumerate(phases)]
     data_stream = torch.cuda.Stream(device=dev)
 
@@ -367,14 +378,16 @@ def run_b200(args):
         for s in st:
             s["win_off"] = off
             off += s["wrows"] * R
-        if args.exchange == "put-nccl":
+        if args.exchange == "put-nccl" and window_kind[0] == "nccl":
             try:
                 win = Window(ctx_data, comm_data, off, backend="nccl")
             except OrchError as e:  # NCCL without symmetric memory: the same put, IPC windows
                 print(f"[bench] NCCL symmetric window unavailable ({e}); CUDA IPC windows",
                       file=sys.stderr)
-                args.exchange = "put"
+                window_kind[0] = "ipc"
         if win is None:
+            if args.exchange == "put-nccl":
+                args.exchange = "put"
             win = Window(ctx_data, comm_data, off)
         wview = win.tensor_view(dev)
         for s in st:
@@ -600,18 +613,26 @@ def run_b200(args):
         for _ in range(max(args.warmup, 10)):
             e2e_step(sync)
         e2e_drain()
-        barrier()
         # the timed host loop runs without the cyclic garbage collector, so a
-        # collection pass cannot land inside the K steps
+        # collection pass cannot land inside the K steps; the collection runs
+        # before the barrier, so the ranks enter the loop together (a collection
+        # after it skewed their starts by a few ms, which the first step paid)
         gc.collect()
         gc.disable()
+        barrier()
         w0 = time.perf_counter()
+        marks = []
         for _ in range(args.steps):
             e2e_step(sync)
+            marks.append(time.perf_counter())
         e2e_drain()
         barrier()
         secs = max_over_ranks(time.perf_counter() - w0)
         gc.enable()
+        if os.environ.get("ORCH_BENCH_E2E_TRACE"):  # host time per step (diagnostics)
+            gaps = np.diff([w0] + marks) * 1e3
+            print(f"[e2e r{rank} sync={sync}] ms/step " + " ".join(f"{g:.2f}" for g in gaps),
+                  file=sys.stderr)
         return secs
 
     # both loops are measured; the line's e2e is the pipelined one unless
@@ -673,6 +694,7 @@ def run_b200(args):
         busbw = a2a_bytes * args.steps / (disp_ms / 1e3) / 1e9
         line["exchange"] = args.exchange
         line["gather"] = args.gather
+        line["windows"] = window_kind[0] if (win is not None or any(gwins)) else None
         line["nodewise_hosting"] = bool(args.nodewise)
         nv = nvlink_peaks(world)
         line["a2a"] = {"bytes_per_rank_per_step": a2a_bytes, "max_egress_bytes": egress,

@@ -506,7 +506,10 @@ int orch_allgather_items(orch_ctx* ctx, orch_comm* comm, int64_t local_n, int64_
  * that does not arrive within ~4 s sets ORCH_CUDA_ERROR instead of hanging. */
 typedef struct orch_gather_window orch_gather_window;
 int orch_gather_window_create(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
-                              orch_gather_window** out); /* collective */
+                              orch_gather_window** out);
+/* The same in NCCL symmetric memory (orch_window_create_nccl). Collective. */
+int orch_gather_window_create_nccl(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
+                                   orch_gather_window** out); /* collective */
 int orch_gather_window_destroy(orch_gather_window* g);   /* collective */
 /* P gather windows of loopback communicators (see orch_window_create_local). */
 int orch_gather_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t nranks,

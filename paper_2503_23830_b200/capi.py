@@ -34,7 +34,8 @@ EXPORTED = [
     "orch_barrier", "orch_window_create", "orch_window_create_nccl", "orch_window_ptr",
     "orch_window_bytes",
     "orch_window_destroy", "orch_window_barrier", "orch_dispatch_put", "orch_put",
-    "orch_gather_window_create", "orch_gather_window_destroy", "orch_allgather_items_put",
+    "orch_gather_window_create", "orch_gather_window_create_nccl", "orch_gather_window_destroy",
+    "orch_allgather_items_put",
     "orch_gather_window_stamps", "orch_window_release", "orch_window_status", "orch_put_at",
     "orch_comm_create_local", "orch_window_create_local", "orch_gather_window_create_local",
     "orch_exchange_report", "orch_exchange_report_host", "orch_allgather_volumes",
@@ -306,15 +307,17 @@ class Window:
 
 
 class GatherWindow:
-    """orch_gather_window: peer-memory all-gather of item records (collective)."""
+    """orch_gather_window: peer-memory all-gather of item records (collective);
+    backend "ipc" (CUDA IPC) or "nccl" (NCCL symmetric memory)."""
 
-    def __init__(self, ctx: "Context", comm: Comm, max_n: int, _handle=None):
+    def __init__(self, ctx: "Context", comm: Comm, max_n: int, _handle=None, backend="ipc"):
         self.h = C.c_void_p()
         if _handle is not None:
             self.h = _handle
         else:
-            _check(lib().orch_gather_window_create(ctx.h, comm.h, C.c_int64(max_n),
-                                                   C.byref(self.h)))
+            create = {"ipc": lib().orch_gather_window_create,
+                      "nccl": lib().orch_gather_window_create_nccl}[backend]
+            _check(create(ctx.h, comm.h, C.c_int64(max_n), C.byref(self.h)))
         self.max_n = max_n
 
     @staticmethod

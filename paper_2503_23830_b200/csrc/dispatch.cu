@@ -2361,6 +2361,21 @@ int orch_gather_window_create(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
   return ORCH_OK;
 }
 
+int orch_gather_window_create_nccl(orch_ctx* ctx, orch_comm* comm, int64_t max_n,
+                                   orch_gather_window** out) {
+  if (!ctx || !comm || !out || max_n < 1) return fail(ORCH_INVALID_ARGUMENT, "bad gather window arguments");
+  orch_window* w = nullptr;
+  int rc = orch_window_create_nccl(ctx, comm, gather_window_bytes(max_n, comm->size), &w);
+  if (rc) return rc;
+  rc = gather_window_wrap(w, max_n, out);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  rc = orch_barrier(comm, nullptr);
+  if (rc) return rc;
+  ORCH_CUDA_TRY(cudaDeviceSynchronize());
+  return ORCH_OK;
+}
+
 int orch_gather_window_create_local(orch_ctx* ctx, orch_comm* const* comms, int32_t P,
                                     int64_t max_n, orch_gather_window** out) {
   if (!ctx || !comms || !out || max_n < 1 || P < 1 || P > 8)

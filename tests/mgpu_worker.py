@@ -36,6 +36,7 @@ def main():
     failures = 0
     cases = 0
     gwin = GatherWindow(ctx, comm, 300)
+    gwin_nccl = GatherWindow(ctx, comm, 300, backend="nccl")  # NCCL symmetric memory
     for seed in range(6):
         for kind in (0, 1, 2, 3):
             for R in (32, 8192):
@@ -60,6 +61,14 @@ def main():
                 go2 = torch.full((n,), -1, dtype=torch.int32, device="cuda")
                 gst = torch.zeros(1, dtype=torch.int32, device="cuda")
                 ctx.allgather_items_put(gwin, torch.from_numpy(mine.astype(np.int64)).cuda(),
+                                        torch.from_numpy(L[mine]).cuda(),
+                                        torch.from_numpy(O[mine]).cuda(), n, gl2, go2, gst)
+                torch.cuda.synchronize()
+                ok = ok and np.array_equal(gl2.cpu().numpy(), L)
+                ok = ok and np.array_equal(go2.cpu().numpy(), O) and int(gst.item()) == 0
+                gl2.fill_(-1)
+                go2.fill_(-1)
+                ctx.allgather_items_put(gwin_nccl, torch.from_numpy(mine.astype(np.int64)).cuda(),
                                         torch.from_numpy(L[mine]).cuda(),
                                         torch.from_numpy(O[mine]).cuda(), n, gl2, go2, gst)
                 torch.cuda.synchronize()
@@ -164,6 +173,7 @@ def main():
     t = torch.tensor([failures])
     dist.all_reduce(t)
     gwin.close()
+    gwin_nccl.close()
     comm.close()
     if rank == 0:
         print(f"MGPU world={world} cases={cases} failures={int(t.item())}", flush=True)
