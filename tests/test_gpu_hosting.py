@@ -227,3 +227,22 @@ def test_inter_node_egress(ctx, oracle):
             o = oracle.solve_hosting(d, c, V)
             np.testing.assert_array_equal(ctx.inter_node_egress(d, c, V, o["hosting"]),
                                           o["per_node_egress"])
+
+
+@pytest.mark.parametrize("d,c", [(8, 8), (32, 1), (96, 96), (72, 9), (128, 64)])
+def test_solve_hosting_edge_shapes(ctx, oracle, d, c):
+    """One node (nothing to choose), 32 nodes of one instance (every lane a
+    node), all-zero and single-entry volume matrices, ties everywhere: hosting,
+    egress and nodes_visited against the oracle's restatement of the reference."""
+    rng = np.random.default_rng(d * 7 + c)
+    cases = [np.zeros((d, d), np.int64), np.ones((d, d), np.int64)]
+    one = np.zeros((d, d), np.int64)
+    one[d - 1, 0] = 5
+    cases.append(one)
+    if d <= 72:  # (a random matrix on 2 x 64 is beyond the sequential oracle's patience)
+        cases.append(rng.integers(0, 3, (d, d)) * (rng.random((d, d)) < 0.2))
+    for V in cases:
+        o = oracle.solve_hosting(d, c, V)
+        a = ctx.solve_hosting(d, c, V)
+        np.testing.assert_array_equal(a["hosting"], o["hosting"])
+        assert a["max_egress"] == o["max_egress"] and a["visited"] == o["visited"], (d, c)
