@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int64_t rounds = 0;
 #ifdef ORCH_SMALL_PROFILE
   // diagnostics build: cycles per round stage, summed over the rounds
-  long long prof[4] = {0, 0, 0, 0}, t_prev = clock64();
+  long long prof[5] = {0, 0, 0, 0, 0}, t_prev = clock64();
 #define LPT_STAGE(i)                       \
   do {                                     \
     const long long t_ = clock64();        \
@@ -188,13 +188,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   while (next < n) {
     const int m = static_cast<int>(n - next < d ? n - next : d);
     // this round's candidate items, fetched now so the L2 latency hides behind the sort
-    int64_t xr[kPer];
+    // (raw 32-bit registers, predicated loads: nothing consumes them before
+    // the k search, so the key build and sort run while they are in flight --
+    // a conversion or select here made every round wait ~1.2k cycles for them)
+    uint32_t xr[kPer];
     int32_t pr[kPer];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int r = tid + i * kThreads;
-      xr[i] = r < m ? static_cast<int64_t>(xs[next + r]) : 0;
-      pr[i] = r < m && !s_bin ? order[next + r] : 0;
+      xr[i] = 0u;
+      pr[i] = 0;
+      if (r < m) {
+        xr[i] = xs[next + r];
+        if (!s_bin) pr[i] = order[next + r];
+      }
     }
     // ---- rank the bins by (load, index)
     if (tid == 0) {
@@ -203,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_k = m;
     }
     __syncthreads();
+    LPT_STAGE(4);
     unsigned mx = 0;
     bool wd = false;
     for (int i = tid; i < Sh::kSlots; i += kThreads) {
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kPer; ++i) {
       const int r0 = warp * 32 + i * kThreads, r = r0 + lane;
       if (r0 >= m) break;
-      const bool bad = r < m && !(load[rank_bin[r]] - L0 < xr[i]);
+      const bool bad = r < m && !(load[rank_bin[r]] - L0 < static_cast<int64_t>(xr[i]));
       const unsigned bm = __ballot_sync(~0u, bad);
       if (bm) {
         if (lane == 0) atomicMin(&s_k, r0 + __ffs(bm) - 1);
@@ -284,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           dst_off[pos] = load[b];
         }
         ++cnt[b];
-        load[b] += xr[i];
+        load[b] += static_cast<int64_t>(xr[i]);
       }
     }
     __syncthreads();
@@ -297,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) g_small_prof[8 + i] = prof[i];
     g_small_prof[12] = rounds;
+    g_small_prof[13] = prof[4];
   }
 #endif
 #undef LPT_STAGE

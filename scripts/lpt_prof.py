@@ -40,8 +40,8 @@ def main():
             st = list(buf)
             r = max(st[12], 1)
             print(f"{cname} {name} n={len(L)} d={cfg['d']} balance_us={sorted(times)[2]:.1f} "
-                  f"rounds={st[12]} cycles/round: keys {st[8] / r:.0f} sort {st[9] / r:.0f} "
-                  f"k {st[10] / r:.0f} assign {st[11] / r:.0f}", flush=True)
+                  f"rounds={st[12]} cycles/round: start {st[13] / r:.0f} keys {st[8] / r:.0f} "
+                  f"sort {st[9] / r:.0f} k {st[10] / r:.0f} assign {st[11] / r:.0f}", flush=True)
 
 
 if __name__ == "__main__":
