@@ -10,4 +10,4 @@ ORCH_LIB_PATH=paper_2503_23830_b200/lib/checked/liborchsim_b200.so timeout 1800 
   python -m pytest tests -m gpu -q -p no:cacheprovider --ignore=tests/test_reference_suite.py \
   > $o/pytest_checked.log 2>&1
 echo "checked suite rc=$? $(tail -1 $o/pytest_checked.log)"
-grep -c "ORCH_DCHECK failed" $o/pytest_checked.log
+grep -c "ORCH_DCHECK failed" $o/pytest_checked.log || true
