@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
         int64_t qs = 0, qq = 0;
         int32_t cnt = 0;
         unsigned beats = 0;  // all sums equal and zero: nothing beats anything
-        int64_t x_next = n > 0 ? static_cast<int64_t>(S.xs[0]) : 0;
+        uint32_t x_next = n > 0 ? S.xs[0] : 0u;  // raw: widened where used
         if (d <= 8) {
           // d <= 8 (C5): the champion chain is walked on a packed word, 4 bits
           // per batch j = nxt_j (15: nothing later beats j), rebuilt by one OR
@@ -642,8 +642,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
           // (scripts/qt_bench.cu).
           unsigned W = 0xffffffffu;
           for (int k = 0; k < n; ++k) {
-            const int64_t x = x_next;
-            if (k + 1 < n) x_next = static_cast<int64_t>(S.xs[k + 1]);
+            const int64_t x = static_cast<int64_t>(x_next);
+            if (k + 1 < n) x_next = S.xs[k + 1];
             const int64_t xx = x * x;
             int best = 0;
             for (;;) {
@@ -674,8 +674,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_balance_small(SmallArgs a)
           }
         } else {
         for (int k = 0; k < n; ++k) {
-          const int64_t x = x_next;
-          if (k + 1 < n) x_next = static_cast<int64_t>(S.xs[k + 1]);  // off the critical path
+          const int64_t x = static_cast<int64_t>(x_next);
+          if (k + 1 < n) x_next = S.xs[k + 1];  // off the critical path
           // the scan's last champion, by pointer jumping along the chain
           // 0 -> nxt_0 -> ... (a batch nothing later beats points to itself):
           // ceil(log2 d) dependent shuffles, no branches
