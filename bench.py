@@ -71,10 +71,13 @@ def peaks():
 
 def nvlink_peaks(n_gpus):
     """NVLink ceilings measured by scripts/p2pbench.cu (profiles/nvlink_peaks.json):
-    the all-to-all pattern at this GPU count when measured, else at 2 GPUs."""
+    the all-to-all pattern at this GPU count when measured, else at the largest
+    measured count below it (e.g. 8 GPUs -> the 4-GPU measurement)."""
     with open(os.path.join(ROOT, "profiles", "nvlink_peaks.json")) as f:
         p = json.load(f)["by_gpus"]
-    key = str(n_gpus) if str(n_gpus) in p else "2"
+    counts = sorted(int(k) for k in p)
+    below = [k for k in counts if k <= n_gpus]
+    key = str(below[-1] if below else counts[0])
     a2a = p[key]["a2a"]
     return dict(copy_engine=a2a["ce"], kernel_push=max(a2a["tma"], a2a["stg"]), nccl=a2a["nccl"],
                 measured_at_gpus=int(key))
