@@ -317,9 +317,13 @@ __host__ __device__ inline size_t host_smem_bytes(int d, int c) {
   return host_table_bytes(d, c) + kHostWarps * warp_stack_bytes(kHostMaxD);
 }
 
-__device__ HostSmem host_load_tables(const HostState& H, unsigned char* raw) {
+// kWide: the tables stay in global memory. A template, so that the narrow
+// search's table and stack pointers are known to be shared-memory ones (LDS/STS
+// instead of generic loads and stores in the DFS loop).
+template <bool kWide>
+__device__ __forceinline__ HostSmem host_load_tables(const HostState& H, unsigned char* raw) {
   const int d = H.d, c = H.c, nodes = H.nodes;
-  if (H.wide) return HostSmem{H.b.g2, H.b.og, H.b.no, H.b.pos};
+  if constexpr (kWide) return HostSmem{H.b.g2, H.b.og, H.b.no, H.b.pos};
   int64_t* g2 = reinterpret_cast<int64_t*>(raw);
   int64_t* og = g2 + d * nodes;
   uint8_t* no = reinterpret_cast<uint8_t*>(og + (d + 1) * nodes * (c + 1));
@@ -433,7 +437,7 @@ __device__ __forceinline__ unsigned q_tag(int pass, unsigned slot) {
 // to leaves after H.after_path; pass 4 prunes a node on lb >= the incumbent the
 // reference holds when it gets there (chain_bound[lo]) and only counts.
 // Donates siblings to idle warps. Returns when the subtree is exhausted (or cut).
-__device__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vstar, WarpStack W,
+__device__ __forceinline__ unsigned long long host_dfs(HostState& H, const HostSmem& T, int pass, int64_t vstar, WarpStack W,
                          int root, int room, int64_t gained) {
   const int d = H.d, c = H.c, nodes = H.nodes, lane = threadIdx.x & 31;
   const bool active = lane < nodes;
@@ -696,6 +700,7 @@ __global__ void __launch_bounds__(1024, 1) k_host_setup(int d, int c, int64_t n,
   if (t == 0) host_init_search(H, b, d, c, 0, kHostQueue, S.incumbent_value, S.root_lb);
 }
 
+template <bool kWide>
 __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restrict__ Hp, int pass) {
   extern __shared__ __align__(16) unsigned char host_raw[];
   HostState& H = *Hp;
@@ -705,12 +710,14 @@ __global__ void __launch_bounds__(kHostWarps * 32) k_host_bb(HostState* __restri
 #ifdef ORCH_HOST_DEBUG
   if (threadIdx.x == 0) atomicMin(&H.dbg_t0, dbg_now());
 #endif
-  const HostSmem T = host_load_tables(H, host_raw);
+  const HostSmem T = host_load_tables<kWide>(H, host_raw);
   const int warp = __shfl_sync(~0u, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int md = H.wide ? H.d : kHostMaxD;
-  unsigned char* ws =
-      H.wide ? H.b.stacks + (static_cast<size_t>(blockIdx.x) * kHostWarps + warp) * warp_stack_bytes(md)
-             : host_raw + host_table_bytes(H.d, H.c) + warp * warp_stack_bytes(md);
+  const int md = kWide ? H.d : kHostMaxD;
+  unsigned char* ws;
+  if constexpr (kWide)
+    ws = H.b.stacks + (static_cast<size_t>(blockIdx.x) * kHostWarps + warp) * warp_stack_bytes(md);
+  else
+    ws = host_raw + host_table_bytes(H.d, H.c) + warp * warp_stack_bytes(md);
   unsigned* masks = reinterpret_cast<unsigned*>(ws + ((md + 3) & ~3));
   uint16_t* ranges = reinterpret_cast<uint16_t*>(masks + 2 * md);
   WarpStack W{ws, masks, masks + md, ranges, ranges + md + 1};
@@ -1631,8 +1638,8 @@ int run_wide_hosting(orch_ctx* ctx, int d, int c, const int64_t* V, HostState* H
   k_hw_init<<<1, 1, 0, st>>>(H, hb, d, c, w.sub, g_better);
   k_hw_incumbent<<<(kHostQueueWide > d ? kHostQueueWide + T - 1 : d + T - 1) / T, T, 0, st>>>(
       w.greedy, g_better, d, c, hb.incumbent, hb.q_ready);
-  k_host_bb<<<kHostGrid, kHostWarps * 32, 0, st>>>(H, 1);
-  k_host_bb<<<kHostGrid, kHostWarps * 32, 0, st>>>(H, 2);
+  k_host_bb<true><<<kHostGrid, kHostWarps * 32, 0, st>>>(H, 1);
+  k_host_bb<true><<<kHostGrid, kHostWarps * 32, 0, st>>>(H, 2);
   k_hw_assign<<<1, 1024, 0, st>>>(H, w.a, hosting, b2i, w.sub + 2 * kHostMaxNodes);
   k_hw_egress<<<grid, T, 0, st>>>(V, w.a, d, c, w.sub + 2 * kHostMaxNodes);
   k_hw_info<<<1, 1, 0, st>>>(H, w.sub + 2 * kHostMaxNodes, info);
@@ -1686,18 +1693,18 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
   static PerDeviceOnce configured;
   const int rc_attr = configured([&]() -> int {
     const int mx = static_cast<int>(host_smem_bytes(kHostMaxD, 2));  // the largest table set
-    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_bb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     ORCH_CUDA_TRY(cudaFuncSetAttribute(k_host_setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sizeof(Prep<kHostMaxD>))));
-    ORCH_CUDA_TRY(max_carveout(k_host_bb));
+    ORCH_CUDA_TRY(max_carveout(k_host_bb<false>));
     ORCH_CUDA_TRY(max_carveout(k_host_setup));
     return ORCH_OK;
   });
   if (rc_attr) return rc_attr;
   k_host_setup<<<1, 1024, sizeof(Prep<kHostMaxD>), st>>>(d, c, n, len, origin, dest, Vin, Vout, H,
                                                           b);
-  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
-  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
+  k_host_bb<false><<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 1);
+  k_host_bb<false><<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 2);
   ctx->launches += 3;
   return ORCH_OK;
 }
@@ -1714,16 +1721,17 @@ int launch_hosting_search(orch_ctx* ctx, int d, int c, int64_t n, const int64_t*
 // links.
 int reference_visits(orch_ctx* ctx, HostState* H, int d, int c, cudaStream_t st, int64_t* visits) {
   const int sm = static_cast<int>(host_smem_bytes(d, c));
+  auto* bb = d > kHostMaxD ? k_host_bb<true> : k_host_bb<false>;
   int links = 2;  // links launched per host check: 2, 4, 8, 8, ...
   *visits = -1;
   k_host_reset<<<1, 1, 0, st>>>(H, 3);
-  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
+  bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
   ctx->launches += 2;
   int done = 0;
   while (!done) {
     for (int i = 0; i < links; ++i) {
       k_host_reset<<<1, 1, 0, st>>>(H, 5);
-      k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
+      bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 3);
     }
     ctx->launches += 2 * links;
     links = links < 8 ? 2 * links : 8;
@@ -1738,7 +1746,7 @@ int reference_visits(orch_ctx* ctx, HostState* H, int d, int c, cudaStream_t st,
   ORCH_CUDA_TRY(cudaMemcpyAsync(&last, &H->chain_last, sizeof last, cudaMemcpyDeviceToHost, st));
   ORCH_CUDA_TRY(cudaMemcpyAsync(&vstar, &H->best_value, sizeof vstar, cudaMemcpyDeviceToHost, st));
   k_host_reset<<<1, 1, 0, st>>>(H, 4);
-  k_host_bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 4);
+  bb<<<kHostGrid, kHostWarps * 32, sm, st>>>(H, 4);
   ctx->launches += 2;
   ORCH_CUDA_TRY(cudaGetLastError());
   unsigned long long count = 0;
